@@ -503,3 +503,106 @@ class RefTree:
 
 def reference_available() -> bool:
     return os.path.exists(REF_SO)
+
+
+# ---- operator-level wrappers of the restatement (kernels.cpp) -------------------------
+class _Tables(C.Structure):
+    _fields_ = [("order", C.c_int), ("n", C.c_int), ("idx_max_degree", C.c_int),
+                ("idx_size", C.c_int), ("_exps", C.c_void_p), ("_deg", C.c_void_p),
+                ("_fact", C.c_void_p), ("_pi", C.c_void_p), ("_pa", C.c_void_p),
+                ("n_m2l", C.c_int), ("_m", C.c_void_p), ("_l", C.c_void_p), ("_d", C.c_void_p),
+                ("_wf", C.c_void_p), ("_wr", C.c_void_p), ("n_m2m", C.c_int), ("_ms", C.c_void_p),
+                ("_msh", C.c_void_p), ("_md", C.c_void_p), ("n_l2l", C.c_int), ("_ls", C.c_void_p),
+                ("_lsh", C.c_void_p), ("_ld", C.c_void_p), ("_lw", C.c_void_p), ("_ew", C.c_void_p)]
+
+
+class OracleOps:
+    """Batched single-instance calls into the C restatement's operators."""
+
+    def __init__(self, orc: "Oracle", order: int):
+        self.lib = orc.lib
+        self.kt = _Tables()
+        L = self.lib
+        L.orc_tables_init.argtypes = [C.POINTER(_Tables), C.c_int]
+        L.orc_tables_free.argtypes = [C.POINTER(_Tables)]
+        rc = L.orc_tables_init(C.byref(self.kt), order)
+        if rc:
+            raise OracleError(ERRORS.get(rc, str(rc)))
+        self.order = order
+        self.n = self.kt.n
+        kp = C.POINTER(_Tables)
+        L.orc_p2m.argtypes = [kp, C.c_int64, _dp, _dp, _dp, _dp]
+        L.orc_m2m.argtypes = [kp, _dp, _dp, _dp]
+        L.orc_m2l.argtypes = [kp, _dp, _dp, _dp]
+        L.orc_m2l_mutual.argtypes = [kp, _dp, _dp, _dp, _dp, _dp]
+        L.orc_l2l.argtypes = [kp, _dp, _dp, _dp]
+        L.orc_l2p.argtypes = [kp, _dp, _dp, C.c_int64, _dp, _dp, _dp]
+        L.orc_p2p.restype = C.c_uint64
+        L.orc_p2p.argtypes = [C.c_int64, _dp, _dp, _dp, _dp, C.c_int64, _dp, _dp, _dp, _dp, C.c_int, C.c_int]
+        L.orc_evaluate_multipole.argtypes = [kp, _dp, _dp, _dp, _dp]
+
+    def __del__(self):
+        try:
+            self.lib.orc_tables_free(C.byref(self.kt))
+        except Exception:
+            pass
+
+    @staticmethod
+    def _a(x, n=None):
+        a = np.ascontiguousarray(x, dtype=np.float64)
+        return a if n is None else a.reshape(n)
+
+    def p2m(self, xyzq, center):
+        b = self._a(xyzq).reshape(-1, 4)
+        pos = np.ascontiguousarray(b[:, :3])
+        q = np.ascontiguousarray(b[:, 3])
+        M = np.zeros(self.n)
+        self.lib.orc_p2m(C.byref(self.kt), len(b), _ptr(pos, _dp), _ptr(q, _dp), _ptr(self._a(center), _dp),
+                         _ptr(M, _dp))
+        return M
+
+    def m2m(self, child, shift):
+        out = np.zeros(self.n)
+        self.lib.orc_m2m(C.byref(self.kt), _ptr(self._a(child), _dp), _ptr(self._a(shift), _dp), _ptr(out, _dp))
+        return out
+
+    def m2l(self, M, R):
+        out = np.zeros(self.n)
+        rc = self.lib.orc_m2l(C.byref(self.kt), _ptr(self._a(M), _dp), _ptr(self._a(R), _dp), _ptr(out, _dp))
+        if rc:
+            raise OracleError(ERRORS.get(rc, str(rc)))
+        return out
+
+    def l2l(self, parent, shift):
+        out = np.zeros(self.n)
+        self.lib.orc_l2l(C.byref(self.kt), _ptr(self._a(parent), _dp), _ptr(self._a(shift), _dp), _ptr(out, _dp))
+        return out
+
+    def l2p(self, L, center, xyzq, with_acc=True):
+        b = self._a(xyzq).reshape(-1, 4)
+        pos = np.ascontiguousarray(b[:, :3])
+        phi = np.zeros(len(b))
+        acc = np.zeros((len(b), 3)) if with_acc else None
+        self.lib.orc_l2p(C.byref(self.kt), _ptr(self._a(L), _dp), _ptr(self._a(center), _dp), len(b),
+                         _ptr(pos, _dp), _ptr(phi, _dp), _ptr(acc, _dp) if with_acc else None)
+        return phi, acc
+
+    def p2p(self, txyzq, sxyzq=None, with_acc=True):
+        t = self._a(txyzq).reshape(-1, 4)
+        self_ = sxyzq is None
+        s = t if self_ else self._a(sxyzq).reshape(-1, 4)
+        tp, tq = np.ascontiguousarray(t[:, :3]), np.ascontiguousarray(t[:, 3])
+        sp, sq = (tp, tq) if self_ else (np.ascontiguousarray(s[:, :3]), np.ascontiguousarray(s[:, 3]))
+        phi = np.zeros(len(t))
+        acc = np.zeros((len(t), 3)) if with_acc else None
+        ev = self.lib.orc_p2p(len(t), _ptr(tp, _dp), _ptr(tq, _dp), _ptr(phi, _dp), _ptr(acc, _dp) if with_acc else None,
+                              len(s), _ptr(sp, _dp), _ptr(sq, _dp), None, None, int(self_), 0)
+        return phi, acc, ev
+
+    def evaluate_multipole(self, M, x, center):
+        out = C.c_double()
+        rc = self.lib.orc_evaluate_multipole(C.byref(self.kt), _ptr(self._a(M), _dp), _ptr(self._a(x), _dp),
+                                             _ptr(self._a(center), _dp), C.byref(out))
+        if rc:
+            raise OracleError(ERRORS.get(rc, str(rc)))
+        return out.value

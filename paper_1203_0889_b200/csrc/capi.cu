@@ -1,0 +1,698 @@
+// capi.cu — the extern "C" boundary (include/fmm_b200.h). Converts internal errors to
+// fmm_status codes + messages, owns the stage sequence of fmm_evaluate (engine.cpp:69-106)
+// and the CUDA-event stage timing (RunResult's t_build/t_upward/t_traversal/t_downward,
+// engine.hpp:38-49, measured on the device).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "context.cuh"
+
+using fmmb::Error;
+using fmmb::fail;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guard(fmm_ctx* c, F&& f) {
+  try {
+    f();
+    if (c) c->err.clear();
+    return FMM_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    if (c) c->err = e.what();
+    return e.status;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    if (c) c->err = e.what();
+    return FMM_ERR_CUDA;
+  }
+}
+
+void require_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    fail(FMM_ERR_NO_DEVICE, "no CUDA device available (the B200 path has no CPU fallback)");
+}
+
+enum { EV_BUILD0 = 0, EV_BUILD1, EV_TRAV1, EV_UP1, EV_M2L1, EV_P2P1, EV_DOWN1, EV_P2PK0, EV_P2PK1, EV_M2LK0,
+       EV_M2LK1, EV_COUNT };
+
+float ms_between(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();
+    return 0.f;
+  }
+  return ms;
+}
+
+void do_m2l(fmm_ctx* c) {
+  CK(cudaMemsetAsync(c->L.ensure((size_t)c->ncells * c->ncoef), 0, sizeof(double) * c->ncells * c->ncoef,
+                     c->stream));
+  CK(cudaEventRecord(c->ev[EV_M2LK0], c->stream));
+  fmmb::run_m2l(c, c->stream);
+  CK(cudaEventRecord(c->ev[EV_M2LK1], c->stream));
+}
+
+void do_p2p(fmm_ctx* c) {
+  CK(cudaMemsetAsync(c->phi_p2p.ensure(c->N), 0, sizeof(double) * c->N, c->stream));
+  CK(cudaMemsetAsync(c->acc_p2p.ensure(3 * c->N), 0, sizeof(double) * 3 * c->N, c->stream));
+  CK(cudaEventRecord(c->ev[EV_P2PK0], c->stream));
+  fmmb::run_p2p(c, c->stream);
+  CK(cudaEventRecord(c->ev[EV_P2PK1], c->stream));
+}
+
+void set_device(fmm_ctx* c) { CK(cudaSetDevice(c->cfg.device)); }
+
+}  // namespace
+
+extern "C" {
+
+const char* fmm_version(void) { return "paper_1203_0889_b200 0.1 (sm_100a)"; }
+
+const char* fmm_last_error(const fmm_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+int fmm_create(const fmm_config* cfg, fmm_ctx** out) {
+  if (!cfg || !out) return FMM_ERR_ARG;
+  *out = nullptr;
+  return guard(nullptr, [&] {
+    if (cfg->order < 1) fail(FMM_ERR_ORDER, "expansion order must be >= 1");
+    if (cfg->order > FMM_MAX_ORDER) fail(FMM_ERR_UNSUPPORTED, "expansion order above FMM_MAX_ORDER (10)");
+    if (cfg->n_crit < 1) fail(FMM_ERR_NCRIT, "n_crit must be >= 1");
+    if (!(cfg->theta > 0.0 && cfg->theta < 1.0)) fail(FMM_ERR_THETA, "theta must be in (0,1)");
+    if (cfg->mutual) fail(FMM_ERR_UNSUPPORTED, "mutual mode is not implemented on the GPU path");
+    if (cfg->precision != FMM_PREC_FP64 && cfg->precision != FMM_PREC_FP32_P2P)
+      fail(FMM_ERR_ARG, "unknown precision mode");
+    require_device();
+    auto* c = new fmm_ctx();
+    c->cfg = *cfg;
+    c->ncoef = fmmb::n_coef(cfg->order);
+    try {
+      set_device(c);
+      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      CK(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+      for (int i = 0; i < EV_COUNT; ++i) CK(cudaEventCreate(&c->ev[i]));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+void fmm_destroy(fmm_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->cfg.device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+  delete ctx;
+}
+
+int fmm_set_bodies(fmm_ctx* c, const double* xyzq, int64_t n) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (n <= 0) fail(FMM_ERR_EMPTY_INPUT, "empty input");
+    if (!xyzq) fail(FMM_ERR_ARG, "null bodies");
+    set_device(c);
+    c->N = n;
+    CK(cudaMemcpyAsync(c->xyzq_in.ensure(n), xyzq, n * sizeof(double4), cudaMemcpyHostToDevice, c->stream));
+    c->have_bodies = true;
+    c->have_tree = c->have_lists = c->have_M = c->have_L = c->have_out = false;
+  });
+}
+
+int fmm_set_bodies_device(fmm_ctx* c, const double* d_xyzq, int64_t n) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (n <= 0) fail(FMM_ERR_EMPTY_INPUT, "empty input");
+    if (!d_xyzq) fail(FMM_ERR_ARG, "null bodies");
+    set_device(c);
+    c->N = n;
+    CK(cudaMemcpyAsync(c->xyzq_in.ensure(n), d_xyzq, n * sizeof(double4), cudaMemcpyDeviceToDevice, c->stream));
+    c->have_bodies = true;
+    c->have_tree = c->have_lists = c->have_M = c->have_L = c->have_out = false;
+  });
+}
+
+int fmm_build_tree(fmm_ctx* c) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    set_device(c);
+    CK(cudaEventRecord(c->ev[EV_BUILD0], c->stream));
+    fmmb::build_tree(c);
+    CK(cudaEventRecord(c->ev[EV_BUILD1], c->stream));
+    c->have_lists = c->have_M = c->have_L = c->have_out = false;
+  });
+}
+
+int fmm_traverse(fmm_ctx* c) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    set_device(c);
+    fmmb::traverse(c);
+    CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
+  });
+}
+
+int fmm_upward(fmm_ctx* c) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    set_device(c);
+    fmmb::run_upward(c, c->stream);
+    CK(cudaEventRecord(c->ev[EV_UP1], c->stream));
+  });
+}
+
+int fmm_m2l(fmm_ctx* c) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    set_device(c);
+    do_m2l(c);
+    CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
+  });
+}
+
+int fmm_p2p(fmm_ctx* c) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    set_device(c);
+    do_p2p(c);
+    CK(cudaEventRecord(c->ev[EV_P2P1], c->stream));
+  });
+}
+
+int fmm_downward(fmm_ctx* c) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    set_device(c);
+    if (!c->have_L) {  // no M2L ran: locals are zero
+      CK(cudaMemsetAsync(c->L.ensure((size_t)c->ncells * c->ncoef), 0, sizeof(double) * c->ncells * c->ncoef,
+                         c->stream));
+      c->have_L = true;
+    }
+    if (!c->phi_p2p.p) {
+      CK(cudaMemsetAsync(c->phi_p2p.ensure(c->N), 0, sizeof(double) * c->N, c->stream));
+      CK(cudaMemsetAsync(c->acc_p2p.ensure(3 * c->N), 0, sizeof(double) * 3 * c->N, c->stream));
+    }
+    fmmb::run_downward(c, c->stream);
+    CK(cudaEventRecord(c->ev[EV_DOWN1], c->stream));
+  });
+}
+
+int fmm_evaluate(fmm_ctx* c) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    set_device(c);
+    c->kernel_launches = 0;
+    CK(cudaEventRecord(c->ev[EV_BUILD0], c->stream));
+    fmmb::build_tree(c);
+    CK(cudaEventRecord(c->ev[EV_BUILD1], c->stream));
+    fmmb::traverse(c);
+    CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
+    fmmb::run_upward(c, c->stream);
+    CK(cudaEventRecord(c->ev[EV_UP1], c->stream));
+    do_m2l(c);
+    CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
+    do_p2p(c);
+    CK(cudaEventRecord(c->ev[EV_P2P1], c->stream));
+    fmmb::run_downward(c, c->stream);
+    CK(cudaEventRecord(c->ev[EV_DOWN1], c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    fmm_stage_times& t = c->times;
+    t.build_ms = ms_between(c->ev[EV_BUILD0], c->ev[EV_BUILD1]);
+    t.traverse_ms = ms_between(c->ev[EV_BUILD1], c->ev[EV_TRAV1]);
+    t.upward_ms = ms_between(c->ev[EV_TRAV1], c->ev[EV_UP1]);
+    t.m2l_ms = ms_between(c->ev[EV_UP1], c->ev[EV_M2L1]);
+    t.p2p_ms = ms_between(c->ev[EV_M2L1], c->ev[EV_P2P1]);
+    t.downward_ms = ms_between(c->ev[EV_P2P1], c->ev[EV_DOWN1]);
+    t.total_ms = ms_between(c->ev[EV_BUILD0], c->ev[EV_DOWN1]);
+    t.p2p_kernel_ms = ms_between(c->ev[EV_P2PK0], c->ev[EV_P2PK1]);
+    t.m2l_kernel_ms = ms_between(c->ev[EV_M2LK0], c->ev[EV_M2LK1]);
+    t.p2p_launches = 1;
+    t.m2l_launches = 1;
+    t.kernel_launches = c->kernel_launches;
+  });
+}
+
+int fmm_synchronize(fmm_ctx* c) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    set_device(c);
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(c->stream2));
+  });
+}
+
+int fmm_get_results(fmm_ctx* c, double* phi, double* acc, int order) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_out) fail(FMM_ERR_STATE, "get_results: no results (run the downward pass)");
+    set_device(c);
+    const int64_t n = c->N;
+    if (order == 0) {
+      if (phi) CK(cudaMemcpyAsync(phi, c->phi.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      if (acc) {
+        if (!c->cfg.with_acc) fail(FMM_ERR_STATE, "acceleration was not requested (with_acc = 0)");
+        CK(cudaMemcpyAsync(acc, c->acc.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      }
+      CK(cudaStreamSynchronize(c->stream));
+      return;
+    }
+    std::vector<double> p(n), a(acc ? 3 * n : 0);
+    std::vector<int32_t> perm(n);
+    CK(cudaMemcpyAsync(p.data(), c->phi.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(perm.data(), c->perm.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    if (acc) {
+      if (!c->cfg.with_acc) fail(FMM_ERR_STATE, "acceleration was not requested (with_acc = 0)");
+      CK(cudaMemcpyAsync(a.data(), c->acc.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < n; ++i) {
+      if (phi) phi[perm[i]] = p[i];
+      if (acc)
+        for (int d = 0; d < 3; ++d) acc[3 * (int64_t)perm[i] + d] = a[3 * i + d];
+    }
+  });
+}
+
+int fmm_results_device(fmm_ctx* c, const double** d_phi, const double** d_acc) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_out) fail(FMM_ERR_STATE, "results_device: no results");
+    if (d_phi) *d_phi = c->phi.p;
+    if (d_acc) *d_acc = c->cfg.with_acc ? c->acc.p : nullptr;
+  });
+}
+
+int fmm_get_tree_info(fmm_ctx* c, fmm_tree_info* info) {
+  if (!c || !info) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_tree) fail(FMM_ERR_STATE, "no tree");
+    std::memset(info, 0, sizeof(*info));
+    info->nbodies = c->N;
+    info->ncells = c->ncells;
+    info->nleaves = c->nleaves;
+    info->depth = c->depth;
+    for (int d = 0; d < 3; ++d) info->center[d] = c->center[d];
+    info->half_side = c->half_side;
+    info->n_m2l = c->have_lists ? c->n_m2l : -1;
+    info->n_p2p = c->have_lists ? c->n_p2p : -1;
+    info->p2p_body_pairs = c->have_lists ? c->p2p_body_pairs : -1;
+    for (int l = 0; l < FMM_MAX_LEVEL + 2; ++l) info->level_start[l] = c->level_start[l];
+  });
+}
+
+int fmm_get_stage_times(fmm_ctx* c, fmm_stage_times* t) {
+  if (!c || !t) return FMM_ERR_ARG;
+  *t = c->times;
+  return FMM_OK;
+}
+
+int fmm_get_cells(fmm_ctx* c, int32_t* level, uint64_t* key, double* center3, double* radius, int32_t* body_begin,
+                  int32_t* body_end, int32_t* child_begin, int32_t* child_count, int32_t* parent) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_tree) fail(FMM_ERR_STATE, "no tree");
+    set_device(c);
+    const int64_t n = c->ncells;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    };
+    cp(level, c->c_level.p, n * 4);
+    cp(key, c->c_key.p, n * 8);
+    cp(body_begin, c->c_body_begin.p, n * 4);
+    cp(body_end, c->c_body_end.p, n * 4);
+    cp(child_begin, c->c_child_begin.p, n * 4);
+    cp(child_count, c->c_child_count.p, n * 4);
+    cp(parent, c->c_parent.p, n * 4);
+    std::vector<double4> cr;
+    if (center3 || radius) {
+      cr.resize(n);
+      cp(cr.data(), c->c_cr.p, n * sizeof(double4));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < n && (center3 || radius); ++i) {
+      if (center3) {
+        center3[3 * i] = cr[i].x;
+        center3[3 * i + 1] = cr[i].y;
+        center3[3 * i + 2] = cr[i].z;
+      }
+      if (radius) radius[i] = cr[i].w;
+    }
+  });
+}
+
+int fmm_get_permutation(fmm_ctx* c, int64_t* perm) {
+  if (!c || !perm) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_tree) fail(FMM_ERR_STATE, "no tree");
+    set_device(c);
+    std::vector<int32_t> p(c->N);
+    CK(cudaMemcpyAsync(p.data(), c->perm.p, c->N * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < c->N; ++i) perm[i] = p[i];
+  });
+}
+
+int fmm_get_lists(fmm_ctx* c, int64_t* m2l_offsets, int32_t* m2l_sources, int64_t* p2p_offsets,
+                  int32_t* p2p_sources) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_lists) fail(FMM_ERR_STATE, "no lists");
+    set_device(c);
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    };
+    cp(m2l_offsets, c->m2l_off.p, (c->ncells + 1) * 8);
+    cp(m2l_sources, c->m2l_src.p, c->n_m2l * 4);
+    cp(p2p_offsets, c->p2p_off.p, (c->ncells + 1) * 8);
+    cp(p2p_sources, c->p2p_src.p, c->n_p2p * 4);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int fmm_get_expansions(fmm_ctx* c, double* multipole, double* local) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    set_device(c);
+    const size_t bytes = sizeof(double) * c->ncells * c->ncoef;
+    if (multipole) {
+      if (!c->have_M) fail(FMM_ERR_STATE, "no multipoles");
+      CK(cudaMemcpyAsync(multipole, c->M.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    }
+    if (local) {
+      if (!c->have_L) fail(FMM_ERR_STATE, "no locals");
+      CK(cudaMemcpyAsync(local, c->L.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int fmm_load_tree(fmm_ctx* c, int64_t ncells, const int32_t* level, const uint64_t* key, const double* center3,
+                  const double* radius, const int32_t* body_begin, const int32_t* body_end,
+                  const int32_t* child_begin, const int32_t* child_count, const int32_t* parent,
+                  const int64_t* perm) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_bodies) fail(FMM_ERR_STATE, "load_tree: set bodies first");
+    if (ncells <= 0 || !level || !key || !center3 || !radius || !body_begin || !body_end || !child_begin ||
+        !child_count || !parent || !perm)
+      fail(FMM_ERR_ARG, "load_tree: bad arguments");
+    set_device(c);
+    cudaStream_t s = c->stream;
+    std::vector<double4> cr(ncells);
+    int depth = 0;
+    for (int l = 0; l < FMM_MAX_LEVEL + 2; ++l) c->level_start[l] = 0;
+    std::vector<int32_t> leaves;
+    for (int64_t i = 0; i < ncells; ++i) {
+      cr[i] = make_double4(center3[3 * i], center3[3 * i + 1], center3[3 * i + 2], radius[i]);
+      depth = level[i] > depth ? level[i] : depth;
+      if (child_count[i] == 0) leaves.push_back(static_cast<int32_t>(i));
+      if (i > 0 && level[i] < level[i - 1]) fail(FMM_ERR_ARG, "load_tree: cells not level-contiguous");
+    }
+    for (int l = 0; l <= FMM_MAX_LEVEL + 1; ++l) {
+      int64_t first = ncells;
+      for (int64_t i = 0; i < ncells; ++i)
+        if (level[i] >= l) { first = i; break; }
+      c->level_start[l] = static_cast<int32_t>(first);
+    }
+    std::vector<int32_t> p32(c->N);
+    for (int64_t i = 0; i < c->N; ++i) p32[i] = static_cast<int32_t>(perm[i]);
+    auto up = [&](void* dst, const void* src, size_t bytes) {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    };
+    up(c->c_level.ensure(ncells), level, ncells * 4);
+    up(c->c_key.ensure(ncells), key, ncells * 8);
+    up(c->c_cr.ensure(ncells), cr.data(), ncells * sizeof(double4));
+    up(c->c_body_begin.ensure(ncells), body_begin, ncells * 4);
+    up(c->c_body_end.ensure(ncells), body_end, ncells * 4);
+    up(c->c_child_begin.ensure(ncells), child_begin, ncells * 4);
+    up(c->c_child_count.ensure(ncells), child_count, ncells * 4);
+    up(c->c_parent.ensure(ncells), parent, ncells * 4);
+    up(c->leaves.ensure(leaves.size()), leaves.data(), leaves.size() * 4);
+    up(c->perm.ensure(c->N), p32.data(), c->N * 4);
+    c->ncells = ncells;
+    c->nleaves = static_cast<int64_t>(leaves.size());
+    c->depth = depth;
+    c->center[0] = center3[0];
+    c->center[1] = center3[1];
+    c->center[2] = center3[2];
+    c->half_side = radius[0];
+    fmmb::gather_bodies(c);
+    CK(cudaStreamSynchronize(s));  // host staging vectors go out of scope
+    c->have_tree = true;
+    c->have_lists = c->have_M = c->have_L = c->have_out = false;
+  });
+}
+
+int fmm_load_lists(fmm_ctx* c, int64_t n_m2l, const int32_t* m2l_pairs, int64_t n_p2p, const int32_t* p2p_pairs) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_tree) fail(FMM_ERR_STATE, "load_lists: no tree");
+    if (n_m2l < 0 || n_p2p < 0 || (n_m2l && !m2l_pairs) || (n_p2p && !p2p_pairs)) fail(FMM_ERR_ARG, "bad lists");
+    set_device(c);
+    int2* dm = c->pairs_b.ensure(n_m2l + 1);
+    int2* dp = c->pairs_c.ensure(n_p2p + 1);
+    if (n_m2l) CK(cudaMemcpyAsync(dm, m2l_pairs, n_m2l * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
+    if (n_p2p) CK(cudaMemcpyAsync(dp, p2p_pairs, n_p2p * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
+    fmmb::lists_from_pairs(c, dm, n_m2l, dp, n_p2p);
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int fmm_load_multipoles(fmm_ctx* c, const double* multipole) {
+  if (!c || !multipole) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_tree) fail(FMM_ERR_STATE, "load_multipoles: no tree");
+    set_device(c);
+    const size_t n = (size_t)c->ncells * c->ncoef;
+    CK(cudaMemcpyAsync(c->M.ensure(n), multipole, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->have_M = true;
+  });
+}
+
+int fmm_reset_accumulators(fmm_ctx* c) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_tree) fail(FMM_ERR_STATE, "no tree");
+    set_device(c);
+    const size_t n = (size_t)c->ncells * c->ncoef;
+    CK(cudaMemsetAsync(c->L.ensure(n), 0, n * sizeof(double), c->stream));
+    CK(cudaMemsetAsync(c->phi_p2p.ensure(c->N), 0, c->N * sizeof(double), c->stream));
+    CK(cudaMemsetAsync(c->acc_p2p.ensure(3 * c->N), 0, 3 * c->N * sizeof(double), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->have_L = true;
+  });
+}
+
+// ---------------------------------------------------------------------- operators ----
+static int check_order(int order) {
+  if (order < 1) return FMM_ERR_ORDER;
+  if (order > FMM_MAX_ORDER) return FMM_ERR_UNSUPPORTED;
+  return FMM_OK;
+}
+
+int fmm_op_p2m(int order, int64_t count, const int32_t* body_offsets, const double* xyzq, const double* centers3,
+               double* M) {
+  if (int rc = check_order(order)) return rc;
+  return guard(nullptr, [&] {
+    require_device();
+    const int64_t nb = count > 0 ? body_offsets[count] : 0;
+    fmmb::op_expansion(fmmb::OP_P2M, order, count, body_offsets, nullptr, centers3, xyzq, nb, M, nullptr);
+  });
+}
+
+int fmm_op_m2m(int order, int64_t count, const double* child_m, const double* shifts3, double* parent_m) {
+  if (int rc = check_order(order)) return rc;
+  return guard(nullptr, [&] {
+    require_device();
+    fmmb::op_expansion(fmmb::OP_M2M, order, count, nullptr, child_m, shifts3, nullptr, 0, parent_m, nullptr);
+  });
+}
+
+int fmm_op_m2l(int order, int64_t count, const double* source_m, const double* disp3, double* target_l) {
+  if (int rc = check_order(order)) return rc;
+  return guard(nullptr, [&] {
+    for (int64_t k = 0; k < count; ++k) {
+      const double* r = disp3 + 3 * k;
+      if ((r[0] * r[0] + r[1] * r[1]) + r[2] * r[2] == 0.0)
+        fail(FMM_ERR_SINGULAR_M2L, "singular M2L displacement");
+    }
+    require_device();
+    fmmb::op_expansion(fmmb::OP_M2L, order, count, nullptr, source_m, disp3, nullptr, 0, target_l, nullptr);
+  });
+}
+
+int fmm_op_l2l(int order, int64_t count, const double* parent_l, const double* shifts3, double* child_l) {
+  if (int rc = check_order(order)) return rc;
+  return guard(nullptr, [&] {
+    require_device();
+    fmmb::op_expansion(fmmb::OP_L2L, order, count, nullptr, parent_l, shifts3, nullptr, 0, child_l, nullptr);
+  });
+}
+
+int fmm_op_l2p(int order, int64_t count, const int32_t* body_offsets, const double* L, const double* centers3,
+               const double* xyzq, double* phi, double* acc) {
+  if (int rc = check_order(order)) return rc;
+  return guard(nullptr, [&] {
+    require_device();
+    const int64_t nb = count > 0 ? body_offsets[count] : 0;
+    fmmb::op_expansion(fmmb::OP_L2P, order, count, body_offsets, L, centers3, xyzq, nb, phi, acc);
+  });
+}
+
+int fmm_op_p2p(int64_t count, const int32_t* ranges4, const double* xyzq, int precision, double* phi, double* acc) {
+  return guard(nullptr, [&] {
+    require_device();
+    int64_t nb = 0;
+    for (int64_t k = 0; k < count; ++k)
+      for (int j = 0; j < 4; ++j) nb = ranges4[4 * k + j] > nb ? ranges4[4 * k + j] : nb;
+    fmmb::op_p2p(count, ranges4, xyzq, nb, precision, phi, acc);
+  });
+}
+
+int fmm_op_evaluate_multipole(int order, int64_t count, const double* M, const double* x3, const double* centers3,
+                              double* out) {
+  if (int rc = check_order(order)) return rc;
+  return guard(nullptr, [&] {
+    std::vector<double> v(6 * (count > 0 ? count : 0));
+    for (int64_t k = 0; k < count; ++k) {
+      const double r[3] = {x3[3 * k] - centers3[3 * k], x3[3 * k + 1] - centers3[3 * k + 1],
+                           x3[3 * k + 2] - centers3[3 * k + 2]};
+      if ((r[0] * r[0] + r[1] * r[1]) + r[2] * r[2] == 0.0)
+        fail(FMM_ERR_SINGULAR_EVAL, "singular evaluation point");
+      for (int d = 0; d < 3; ++d) {
+        v[6 * k + d] = x3[3 * k + d];
+        v[6 * k + 3 + d] = centers3[3 * k + d];
+      }
+    }
+    require_device();
+    fmmb::op_expansion(fmmb::OP_EVAL, order, count, nullptr, M, v.data(), nullptr, 0, out, nullptr);
+  });
+}
+
+int fmm_op_laplace_derivatives(int max_degree, int64_t count, const double* r3, double* out) {
+  if (max_degree < 0 || max_degree + 1 > FMM_MAX_ORDER) return FMM_ERR_UNSUPPORTED;
+  return guard(nullptr, [&] {
+    require_device();
+    fmmb::op_expansion(fmmb::OP_DERIV, max_degree + 1, count, nullptr, nullptr, r3, nullptr, 0, out, nullptr);
+  });
+}
+
+int fmm_op_compute_bounds(const double* xyzq, int64_t n, double* center3, double* half_side) {
+  return guard(nullptr, [&] {
+    if (n <= 0) fail(FMM_ERR_EMPTY_INPUT, "empty input");
+    require_device();
+    fmmb::op_bounds(xyzq, n, center3, half_side);
+  });
+}
+
+int fmm_op_morton_key(int64_t count, const double* p3, const double* center3, double half_side, int level,
+                      uint64_t* out) {
+  return guard(nullptr, [&] {
+    if (level < 0 || level > FMM_MAX_LEVEL) fail(FMM_ERR_LEVEL_OVERFLOW, "level overflow");
+    require_device();
+    fmmb::op_morton(count, p3, center3, half_side, level, out);
+  });
+}
+
+int fmm_op_mac(int64_t count, const double* tcenter3, const double* tradius, const double* scenter3,
+               const double* sradius, double theta, int32_t* out) {
+  return guard(nullptr, [&] {
+    require_device();
+    fmmb::op_mac(count, tcenter3, tradius, scenter3, sradius, theta, out);
+  });
+}
+
+// ----------------------------------------------------------------- synthetic inputs ----
+// BASELINE.json configs: the reference's xorshift64* (dataset.cpp:10-34),
+// position drawn before charge, Vec3(u(),u(),u()) evaluated right-to-left by g++ (z first).
+int fmm_generate_bodies(int config, int64_t n, uint64_t seed, double* xyzq) {
+  return guard(nullptr, [&] {
+    if (n <= 0) fail(FMM_ERR_EMPTY_INPUT, "empty input");
+    if (!xyzq) fail(FMM_ERR_ARG, "null output");
+    auto splitmix = [](uint64_t x) {
+      x += 0x9E3779B97F4A7C15ULL;
+      x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+      x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+      return x ^ (x >> 31);
+    };
+    uint64_t st = splitmix(seed);
+    if (st == 0) st = 0x9E3779B97F4A7C15ULL;
+    auto next = [&]() {
+      st ^= st >> 12;
+      st ^= st << 25;
+      st ^= st >> 27;
+      return st * 2685821657736338717ULL;
+    };
+    auto u01 = [&]() { return static_cast<double>(next() >> 11) * 0x1.0p-53; };
+    auto uni = [&](double lo, double hi) { return lo + (hi - lo) * u01(); };
+    const double dn = static_cast<double>(n);
+    const double two_pi = 6.283185307179586;
+    for (int64_t i = 0; i < n; ++i) {
+      double* b = xyzq + 4 * i;
+      switch (config) {
+        case 1:
+        case 2:
+        case 4:  // uniform in [-1,1]^3, q in (0, 1/N]
+          b[2] = uni(-1.0, 1.0);
+          b[1] = uni(-1.0, 1.0);
+          b[0] = uni(-1.0, 1.0);
+          b[3] = (1.0 - u01()) / dn;
+          break;
+        case 3: {  // Plummer sphere, scale radius 1, r <= 100, isotropic; q = 1/N
+          double r;
+          do {
+            const double U = u01();
+            r = 1.0 / std::sqrt(std::pow(U, -2.0 / 3.0) - 1.0);
+          } while (!(r <= 100.0) || !std::isfinite(r));
+          double v[3], s;
+          do {
+            v[2] = uni(-1.0, 1.0);
+            v[1] = uni(-1.0, 1.0);
+            v[0] = uni(-1.0, 1.0);
+            s = (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2];
+          } while (s > 1.0 || s < 1e-8);
+          const double inv = r / std::sqrt(s);
+          b[0] = v[0] * inv;
+          b[1] = v[1] * inv;
+          b[2] = v[2] * inv;
+          b[3] = 1.0 / dn;
+          break;
+        }
+        case 5: {  // unit sphere surface (normalised Gaussian 3-vectors), q in [-1,1]/N
+          double v[3], s;
+          do {
+            for (int d = 2; d >= 0; --d) {
+              const double u1 = u01(), u2 = u01();
+              v[d] = std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(two_pi * u2);
+            }
+            s = (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2];
+          } while (s == 0.0);
+          const double inv = 1.0 / std::sqrt(s);
+          b[0] = v[0] * inv;
+          b[1] = v[1] * inv;
+          b[2] = v[2] * inv;
+          b[3] = uni(-1.0, 1.0) / dn;
+          break;
+        }
+        default:
+          fail(FMM_ERR_ARG, "unknown config (1..5)");
+      }
+    }
+  });
+}
+
+}  // extern "C"

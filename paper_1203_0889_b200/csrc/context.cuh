@@ -1,0 +1,123 @@
+// context.cuh — the fmm_ctx state: device-resident bodies, tree, interaction lists,
+// expansions and outputs, plus the stage entry points implemented across the .cu files.
+//
+// HBM layout (all tree-order unless noted):
+//   xyzq_in   double4[N]   input bodies (input order)
+//   bodies    double4[N]   x,y,z,q in tree order (FP64 P2P, P2M, L2P)
+//   bodyf     float4[N]    x-cx,y-cy,z-cz,q relative to the body's own leaf centre (FP32 P2P)
+//   perm      int32[N]     tree-order body -> input index
+//   cells     SoA: level i32, key u64, cr double4 (cx,cy,cz,radius), body_begin/end,
+//             child_begin/count, parent (i32) — reference Cell (tree.hpp:21-36), BFS order
+//   lists     CSR by target cell: m2l_off int64[ncells+1], m2l_src int32[n_m2l]; same for p2p
+//   M, L      double[ncells * n_coef] reference coefficient order (multi_index.cpp:16-20)
+//   phi, acc  double[N], double[3N] outputs in tree order
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+struct fmm_ctx {
+  fmm_config cfg{};
+  int ncoef = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // concurrent stream (P2P alongside the expansion chain)
+  std::string err;
+
+  // bodies
+  int64_t N = 0;
+  fmmb::DBuf<double4> xyzq_in;
+  fmmb::DBuf<double4> bodies;
+  fmmb::DBuf<float4> bodyf;
+  fmmb::DBuf<int32_t> perm;
+  fmmb::DBuf<int32_t> leaf_of_body;  // tree-order body -> leaf cell index
+
+  // tree
+  int64_t ncells = 0, nleaves = 0;
+  int depth = 0;
+  int32_t level_start[FMM_MAX_LEVEL + 2] = {};
+  double center[3] = {0, 0, 0};
+  double half_side = 0;
+  fmmb::DBuf<int32_t> c_level, c_body_begin, c_body_end, c_child_begin, c_child_count, c_parent;
+  fmmb::DBuf<uint64_t> c_key;
+  fmmb::DBuf<double4> c_cr;
+  fmmb::DBuf<int32_t> leaves;  // leaf cell indices, ascending
+
+  // lists (CSR by target)
+  int64_t n_m2l = 0, n_p2p = 0, p2p_body_pairs = 0;
+  fmmb::DBuf<int64_t> m2l_off, p2p_off;
+  fmmb::DBuf<int32_t> m2l_src, p2p_src;
+  fmmb::DBuf<int32_t> m2l_targets;  // cells with non-empty M2L lists
+  int64_t n_m2l_targets = 0;
+
+  // P2P work list (cost sorted)
+  fmmb::DBuf<int4> p2p_items;       // target leaf, list begin, list end, partial slot (-1 = direct)
+  int64_t n_p2p_items = 0;
+  fmmb::DBuf<double> p2p_partial;   // [slot][target body][4] (phi, ax, ay, az)
+  fmmb::DBuf<int4> p2p_reduce;      // target leaf, first slot, n slots, body begin
+  int64_t n_p2p_reduce = 0;
+
+  // expansions and outputs
+  fmmb::DBuf<double> M, L;
+  fmmb::DBuf<double> phi, acc;
+  fmmb::DBuf<double> phi_p2p, acc_p2p;  // near-field part (tree order)
+
+  // scratch
+  fmmb::DBuf<unsigned char> tmp;
+  fmmb::DBuf<uint64_t> keys_a, keys_b;
+  fmmb::DBuf<int32_t> idx_a, idx_b;
+  fmmb::DBuf<int64_t> scan_a;
+  fmmb::DBuf<int2> pairs_a, pairs_b, pairs_c;
+  fmmb::DBuf<int32_t> i32_a, i32_b, i32_c;
+  fmmb::DBuf<int64_t> d_counters;
+  fmmb::DBuf<double> small;
+
+  // state
+  bool have_bodies = false, have_tree = false, have_lists = false, have_M = false,
+       have_L = false, have_out = false;
+
+  // timing
+  fmm_stage_times times{};
+  cudaEvent_t ev[16] = {};
+  int kernel_launches = 0;
+};
+
+namespace fmmb {
+
+// tree_build.cu
+void build_tree(fmm_ctx* c);
+void gather_bodies(fmm_ctx* c);  // bodies/bodyf/leaf_of_body from perm + tree
+// traverse.cu
+void traverse(fmm_ctx* c);
+void lists_from_pairs(fmm_ctx* c, const int2* d_m2l, int64_t n_m2l, const int2* d_p2p,
+                      int64_t n_p2p);
+// p2p.cu
+void build_p2p_worklist(fmm_ctx* c);
+void run_p2p(fmm_ctx* c, cudaStream_t s);
+// expansions.cu
+void run_upward(fmm_ctx* c, cudaStream_t s);
+void run_m2l(fmm_ctx* c, cudaStream_t s);
+void run_downward(fmm_ctx* c, cudaStream_t s);  // L2L + L2P + combine with P2P part
+
+// CUB temp helper
+void* temp_storage(fmm_ctx* c, size_t bytes);
+
+}  // namespace fmmb
+
+namespace fmmb {
+// Single-operator entry points (fmm_op_*), device implementations; host buffers in/out.
+void op_bounds(const double* xyzq, int64_t n, double* center3, double* half_side);
+void op_morton(int64_t count, const double* p3, const double* center3, double half_side, int level,
+               uint64_t* out);
+void op_mac(int64_t count, const double* tc3, const double* tr, const double* sc3, const double* sr,
+            double theta, int32_t* out);
+void op_p2p(int64_t count, const int32_t* ranges4, const double* xyzq, int64_t nbodies, int precision,
+            double* phi, double* acc);
+void op_expansion(int kind, int order, int64_t count, const int32_t* offsets, const double* in,
+                  const double* vec3, const double* xyzq, int64_t nbodies, double* out, double* out2);
+// kinds for op_expansion
+enum { OP_P2M = 0, OP_M2M = 1, OP_M2L = 2, OP_L2L = 3, OP_L2P = 4, OP_EVAL = 5, OP_DERIV = 6 };
+}  // namespace fmmb

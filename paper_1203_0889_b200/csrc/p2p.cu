@@ -1,0 +1,623 @@
+// p2p.cu — near-field P2P on sm_100a (reference: p2p non-mutual, kernels.cpp:181-192,
+// applied by KernelVisitor::p2p_pair, traversal.hpp:154-157) plus its acceleration extension.
+//
+// Work decomposition (replaces the QUARK task DAG): one CTA per work item =
+// (target leaf, target sub-range <= 128 bodies, contiguous chunk of its P2P source list).
+// Items are cost-sorted (n_t * sum n_s, descending) so the longest start first; lists whose
+// cost exceeds a per-SM share are split into source chunks whose partial sums are reduced in
+// a fixed order afterwards (deterministic, no atomics). Writes are target-owned.
+//
+// Inside a CTA the 128 threads form G = floor(128 / n_t) lane groups; thread (g, t) owns
+// target body t and every G-th source pair of each shared-memory tile. Source tiles hold up to
+// 32 list entries (1024 bodies) converted to coordinates relative to the TARGET leaf centre:
+// bodies are stored in HBM as FP32 offsets from their own leaf centre and shifted by the
+// FP64-computed centre difference, so FP32 only ever sees leaf-scale magnitudes. Tiles are
+// pair-interleaved {-x0,-x1,-y0,-y1},{-z0,-z1,q0,q1} so the inner loop runs on the packed
+// f32x2 pipe (FFMA2/FADD2/FMUL2) with one MUFU.RSQ per pair; r^2 == 0 pairs (self,
+// coincident; kernels.cpp:185-186) are removed by a select. Each tile's FP32 partial sums are
+// folded into FP64 per-target accumulators ("FP64-checked accumulation").
+#include <cub/cub.cuh>
+
+#include "context.cuh"
+
+namespace fmmb {
+namespace {
+
+constexpr int kThreads = 128;   // threads per P2P CTA (max target bodies per item)
+constexpr int kTileSegs = 32;   // list entries staged per tile
+constexpr int kTileBodies = 1024;
+
+struct P2PItem {
+  int32_t leaf, tb, te, lb, le;  // target leaf, target body range, list range [lb, le)
+  int32_t pbase;                 // partial-buffer base (in bodies) or -1 for a direct write
+  int32_t sb0;                   // body offset into the first list entry (always 0 here)
+  int32_t pad;
+};
+static_assert(sizeof(P2PItem) == 32, "P2PItem is 32 B");
+
+// Tile setup (warp 0): takes the next list entries whose bodies fit in TILE slots, starting
+// at (cursor, cur_off). A single source leaf larger than the tile (only possible for level-21
+// overflow leaves) is consumed TILE bodies at a time. Results: seg_off[0..nseg], seg_src,
+// seg_boff (body offset inside each entry), nxt[0] = next cursor, nxt[1] = next offset.
+template <int TILE>
+__device__ __forceinline__ void tile_setup(int tid, int32_t le, int32_t cursor, int32_t cur_off,
+                                           const int32_t* __restrict__ src_list, const int32_t* __restrict__ bb,
+                                           const int32_t* __restrict__ be, int32_t* seg_off, int32_t* seg_src,
+                                           int32_t* seg_boff, int32_t* nxt) {
+  if (tid >= 32) return;
+  const int32_t k = cursor + tid;
+  int32_t n = 0, s = -1, boff = 0;
+  if (k < le) {
+    s = src_list[k];
+    n = be[s] - bb[s];
+    if (tid == 0) {
+      boff = cur_off;
+      n -= cur_off;
+    }
+  }
+  int32_t incl = n;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (tid >= o) incl += v;
+  }
+  const bool fits = (k < le) && (incl <= TILE);
+  const unsigned m = __ballot_sync(0xffffffffu, fits);
+  if (m == 0) {  // the first entry alone overflows the tile: take TILE of its bodies
+    if (tid == 0) {
+      seg_off[0] = 0;
+      seg_off[1] = TILE;
+      seg_src[0] = s;
+      seg_boff[0] = boff;
+      nxt[0] = cursor;
+      nxt[1] = cur_off + TILE;
+      nxt[2] = 1;
+    }
+    return;
+  }
+  const int nseg = 32 - __clz(m);  // fits is a prefix of the lanes
+  if (tid < nseg) {
+    seg_off[tid + 1] = incl;
+    seg_src[tid] = s;
+    seg_boff[tid] = boff;
+  }
+  if (tid == 0) {
+    seg_off[0] = 0;
+    nxt[0] = cursor + nseg;
+    nxt[1] = 0;
+    nxt[2] = nseg;
+  }
+}
+
+// ------------------------------------------------------------------------ FP32 kernel ----
+__global__ void __launch_bounds__(kThreads, 6)
+k_p2p_fp32(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_list,
+           const int32_t* __restrict__ bb, const int32_t* __restrict__ be, const double4* __restrict__ cr,
+           const float4* __restrict__ bodyf, double* __restrict__ phi_out, double* __restrict__ acc_out,
+           double* __restrict__ partial, int with_acc) {
+  __shared__ float4 sA[kTileBodies / 2 + 1];
+  __shared__ float4 sB[kTileBodies / 2 + 1];
+  __shared__ int32_t seg_off[kTileSegs + 1];
+  __shared__ int32_t seg_src[kTileSegs];
+  __shared__ int32_t seg_boff[kTileSegs];
+  __shared__ int32_t nxt[3];
+  __shared__ double red[4][kThreads];
+
+  const P2PItem it = items[blockIdx.x];
+  const int tid = threadIdx.x;
+  const int nt = it.te - it.tb;
+  const int G = kThreads / nt;
+  const int g = tid / nt, t = tid - g * nt;
+  const bool active = g < G;
+  const double4 ct = cr[it.leaf];
+
+  float xt = 0.f, yt = 0.f, zt = 0.f;
+  if (active) {
+    const float4 b = bodyf[it.tb + t];
+    xt = b.x;
+    yt = b.y;
+    zt = b.z;
+  }
+  const float2 X = make_float2(xt, xt), Y = make_float2(yt, yt), Z = make_float2(zt, zt);
+  double phi_d = 0.0, ax_d = 0.0, ay_d = 0.0, az_d = 0.0;
+
+  int32_t cursor = it.lb, cur_off = 0;
+  while (cursor < it.le) {
+    tile_setup<kTileBodies>(tid, it.le, cursor, cur_off, src_list, bb, be, seg_off, seg_src, seg_boff, nxt);
+    __syncthreads();
+    const int32_t nseg = nxt[2];
+    const int32_t nb = seg_off[nseg];
+    // --- fill: warp w copies entries w, w+4, ...; sources shifted into the target leaf's
+    // frame (shift = c_s - c_t in FP64, rounded once), negated, pair-interleaved
+    {
+      const int w = tid >> 5, lane = tid & 31;
+      float* A = reinterpret_cast<float*>(sA);
+      float* B = reinterpret_cast<float*>(sB);
+      for (int k = w; k < nseg; k += kThreads / 32) {
+        const int32_t src = seg_src[k];
+        const int32_t base = bb[src] + seg_boff[k], n = seg_off[k + 1] - seg_off[k], o0 = seg_off[k];
+        const double4 cs = cr[src];
+        const float sx = static_cast<float>(cs.x - ct.x), sy = static_cast<float>(cs.y - ct.y),
+                    sz = static_cast<float>(cs.z - ct.z);
+        for (int j = lane; j < n; j += 32) {
+          const float4 b = bodyf[base + j];
+          const int p = o0 + j, pi = p >> 1, h = p & 1;
+          A[4 * pi + h] = -(b.x + sx);
+          A[4 * pi + 2 + h] = -(b.y + sy);
+          B[4 * pi + h] = -(b.z + sz);
+          B[4 * pi + 2 + h] = b.w;
+        }
+      }
+      if (tid == 0 && (nb & 1)) {  // pad to a whole pair with a zero charge
+        const int pi = nb >> 1;
+        A[4 * pi + 1] = 0.f;
+        A[4 * pi + 3] = 0.f;
+        B[4 * pi + 1] = 0.f;
+        B[4 * pi + 3] = 0.f;
+      }
+    }
+    __syncthreads();
+    // --- compute
+    if (active) {
+      const int npairs = (nb + 1) >> 1;
+      float2 ph = make_float2(0.f, 0.f), ax = ph, ay = ph, az = ph;
+#pragma unroll 4
+      for (int p = g; p < npairs; p += G) {
+        const float4 a = sA[p];
+        const float4 b = sB[p];
+        const float2 dx = __fadd2_rn(X, make_float2(a.x, a.y));
+        const float2 dy = __fadd2_rn(Y, make_float2(a.z, a.w));
+        const float2 dz = __fadd2_rn(Z, make_float2(b.x, b.y));
+        const float2 q = make_float2(b.z, b.w);
+        float2 r2 = __fmul2_rn(dx, dx);
+        r2 = __ffma2_rn(dy, dy, r2);
+        r2 = __ffma2_rn(dz, dz, r2);
+        float2 ri;
+        ri.x = r2.x > 0.f ? rsqrtf(r2.x) : 0.f;
+        ri.y = r2.y > 0.f ? rsqrtf(r2.y) : 0.f;
+        const float2 qr = __fmul2_rn(q, ri);
+        ph = __fadd2_rn(ph, qr);
+        if (with_acc) {
+          const float2 ri2 = __fmul2_rn(ri, ri);
+          const float2 qr3 = __fmul2_rn(qr, ri2);
+          ax = __ffma2_rn(dx, qr3, ax);
+          ay = __ffma2_rn(dy, qr3, ay);
+          az = __ffma2_rn(dz, qr3, az);
+        }
+      }
+      phi_d += static_cast<double>(ph.x) + static_cast<double>(ph.y);
+      ax_d += static_cast<double>(ax.x) + static_cast<double>(ax.y);
+      ay_d += static_cast<double>(ay.x) + static_cast<double>(ay.y);
+      az_d += static_cast<double>(az.x) + static_cast<double>(az.y);
+    }
+    cursor = nxt[0];
+    cur_off = nxt[1];
+    __syncthreads();
+  }
+  // --- reduce the G lane groups in fixed order and write (target-owned)
+  red[0][tid] = phi_d;
+  red[1][tid] = ax_d;
+  red[2][tid] = ay_d;
+  red[3][tid] = az_d;
+  __syncthreads();
+  if (tid < nt) {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int gg = 0; gg < G; ++gg)
+      for (int c = 0; c < 4; ++c) v[c] += red[c][gg * nt + tid];
+    if (it.pbase < 0) {
+      const int32_t i = it.tb + tid;
+      phi_out[i] = v[0];
+      if (with_acc) {
+        acc_out[3 * i] = v[1];
+        acc_out[3 * i + 1] = v[2];
+        acc_out[3 * i + 2] = v[3];
+      }
+    } else {
+      double* p = partial + 4 * ((int64_t)it.pbase + tid);
+      p[0] = v[0];
+      p[1] = v[1];
+      p[2] = v[2];
+      p[3] = v[3];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------ FP64 kernel ----
+// Parity mode: absolute FP64 coordinates and the reference's arithmetic
+// (dx = x_i - y_j, r2 = (dx*dx + dy*dy) + dz*dz, skip r2 == 0, phi += q / sqrt(r2)).
+__global__ void __launch_bounds__(kThreads, 4)
+k_p2p_fp64(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_list,
+           const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
+           const double4* __restrict__ bodies, double* __restrict__ phi_out, double* __restrict__ acc_out,
+           double* __restrict__ partial, int with_acc) {
+  constexpr int kTile = 512;
+  __shared__ double4 sS[kTile];
+  __shared__ int32_t seg_off[kTileSegs + 1];
+  __shared__ int32_t seg_src[kTileSegs];
+  __shared__ int32_t seg_boff[kTileSegs];
+  __shared__ int32_t nxt[3];
+  __shared__ double red[4][kThreads];
+
+  const P2PItem it = items[blockIdx.x];
+  const int tid = threadIdx.x;
+  const int nt = it.te - it.tb;
+  const int G = kThreads / nt;
+  const int g = tid / nt, t = tid - g * nt;
+  const bool active = g < G;
+  double4 bt = make_double4(0, 0, 0, 0);
+  if (active) bt = bodies[it.tb + t];
+  double phi_d = 0.0, ax_d = 0.0, ay_d = 0.0, az_d = 0.0;
+  int32_t cursor = it.lb, cur_off = 0;
+  while (cursor < it.le) {
+    tile_setup<kTile>(tid, it.le, cursor, cur_off, src_list, bb, be, seg_off, seg_src, seg_boff, nxt);
+    __syncthreads();
+    const int32_t nseg = nxt[2];
+    const int32_t nb = seg_off[nseg];
+    {
+      const int w = tid >> 5, lane = tid & 31;
+      for (int k = w; k < nseg; k += kThreads / 32) {
+        const int32_t src = seg_src[k];
+        const int32_t base = bb[src] + seg_boff[k], o0 = seg_off[k], n = seg_off[k + 1] - o0;
+        for (int j = lane; j < n; j += 32) sS[o0 + j] = bodies[base + j];
+      }
+    }
+    __syncthreads();
+    if (active) {
+      for (int j = g; j < nb; j += G) {
+        const double4 s = sS[j];
+        const double dx = bt.x - s.x, dy = bt.y - s.y, dz = bt.z - s.z;
+        const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+        if (r2 == 0.0) continue;
+        const double ri = 1.0 / sqrt(r2);
+        const double qr = s.w * ri;
+        phi_d += qr;
+        if (with_acc) {
+          const double qr3 = qr * ri * ri;
+          ax_d += dx * qr3;
+          ay_d += dy * qr3;
+          az_d += dz * qr3;
+        }
+      }
+    }
+    cursor = nxt[0];
+    cur_off = nxt[1];
+    __syncthreads();
+  }
+  red[0][tid] = phi_d;
+  red[1][tid] = ax_d;
+  red[2][tid] = ay_d;
+  red[3][tid] = az_d;
+  __syncthreads();
+  if (tid < nt) {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int gg = 0; gg < G; ++gg)
+      for (int c = 0; c < 4; ++c) v[c] += red[c][gg * nt + tid];
+    if (it.pbase < 0) {
+      const int32_t i = it.tb + tid;
+      phi_out[i] = v[0];
+      if (with_acc) {
+        acc_out[3 * i] = v[1];
+        acc_out[3 * i + 1] = v[2];
+        acc_out[3 * i + 2] = v[3];
+      }
+    } else {
+      double* p = partial + 4 * ((int64_t)it.pbase + tid);
+      p[0] = v[0];
+      p[1] = v[1];
+      p[2] = v[2];
+      p[3] = v[3];
+    }
+  }
+}
+
+// Split-list targets: sum the source-chunk partials in chunk order.
+__global__ void k_p2p_reduce(const int4* __restrict__ red, int64_t nred, const double* __restrict__ partial,
+                             double* __restrict__ phi_out, double* __restrict__ acc_out, int with_acc) {
+  const int64_t r = blockIdx.x;
+  if (r >= nred) return;
+  const int4 e = red[r];  // x = tb, y = te, z = pbase of chunk 0, w = nchunks
+  const int nt = e.y - e.x;
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k = 0; k < e.w; ++k) {
+      const double* p = partial + 4 * ((int64_t)e.z + (int64_t)k * nt + t);
+      for (int c = 0; c < 4; ++c) v[c] += p[c];
+    }
+    const int32_t i = e.x + t;
+    phi_out[i] = v[0];
+    if (with_acc) {
+      acc_out[3 * i] = v[1];
+      acc_out[3 * i + 1] = v[2];
+      acc_out[3 * i + 2] = v[3];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- work list build ----
+// Per target leaf (warp each): sum of source sizes, item count. Leaves are all cells with a
+// non-empty P2P list (every leaf has at least its self pair).
+__global__ void k_leaf_cost(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
+                            const int32_t* __restrict__ src, const int32_t* __restrict__ bb,
+                            const int32_t* __restrict__ be, uint64_t cmax, int64_t* __restrict__ sum_ns,
+                            int32_t* __restrict__ nitems, int32_t* __restrict__ nred, int32_t* __restrict__ npart) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nleaves) return;
+  const int32_t leaf = leaves[w];
+  const int64_t l0 = off[leaf], l1 = off[leaf + 1];
+  int64_t s = 0;
+  for (int64_t k = l0 + lane; k < l1; k += 32) s += be[src[k]] - bb[src[k]];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    const int64_t nt = be[leaf] - bb[leaf];
+    const int64_t cost = nt * s;
+    int64_t nsc = (cost + (int64_t)cmax - 1) / (int64_t)cmax;
+    if (nsc < 1) nsc = 1;
+    if (nsc > l1 - l0) nsc = l1 - l0;
+    if (l1 == l0) nsc = 0;
+    const int64_t ntc = (nt + kThreads - 1) / kThreads;
+    sum_ns[w] = s;
+    nitems[w] = static_cast<int32_t>(nsc * ntc);
+    nred[w] = nsc > 1 ? static_cast<int32_t>(ntc) : 0;
+    npart[w] = nsc > 1 ? static_cast<int32_t>(nsc * nt) : 0;
+  }
+}
+
+// Writes the items of one target leaf (warp each). Source chunks split the list where the
+// running source-body count crosses j * sum_ns / nsc.
+__global__ void k_write_items(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
+                              const int32_t* __restrict__ src, const int32_t* __restrict__ bb,
+                              const int32_t* __restrict__ be, const int64_t* __restrict__ sum_ns,
+                              const int32_t* __restrict__ nitems, const int32_t* __restrict__ item_off,
+                              const int32_t* __restrict__ red_off, const int32_t* __restrict__ part_off,
+                              P2PItem* __restrict__ items, uint64_t* __restrict__ costs, int4* __restrict__ red) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nleaves || nitems[w] == 0) return;
+  const int32_t leaf = leaves[w];
+  const int32_t tb = bb[leaf], te = be[leaf], nt = te - tb;
+  const int32_t ntc = (nt + kThreads - 1) / kThreads;
+  const int32_t nsc = nitems[w] / ntc;
+  const int64_t l0 = off[leaf], l1 = off[leaf + 1];
+  const int64_t S = sum_ns[w];
+  // chunk boundaries: bnd[j] = first list index whose prefix (exclusive) >= j*S/nsc
+  int64_t prev_b = l0;
+  int64_t prefix = 0;  // exclusive prefix at list index k
+  int32_t j = 1;
+  int32_t out = item_off[w];
+  const int32_t pb = nsc > 1 ? part_off[w] : -1;
+  auto emit = [&](int32_t chunk, int64_t lb, int64_t le, int64_t ns_chunk) {
+    if (lane != 0) return;
+    for (int32_t tc = 0; tc < ntc; ++tc) {
+      const int32_t t0 = tb + tc * kThreads;
+      const int32_t t1 = min(te, t0 + kThreads);
+      P2PItem itm;
+      itm.leaf = leaf;
+      itm.tb = t0;
+      itm.te = t1;
+      itm.lb = static_cast<int32_t>(lb);
+      itm.le = static_cast<int32_t>(le);
+      // partial layout per leaf: t-chunk regions of nsc * (t1-t0) bodies, source-chunk major
+      itm.pbase = pb < 0 ? -1 : pb + nsc * (t0 - tb) + chunk * (t1 - t0);
+      itm.sb0 = 0;
+      itm.pad = 0;
+      items[out] = itm;
+      costs[out] = static_cast<uint64_t>(t1 - t0) * static_cast<uint64_t>(ns_chunk);
+      ++out;
+    }
+  };
+  if (nsc == 1) {
+    emit(0, l0, l1, S);
+  } else {
+    int64_t chunk_start_prefix = 0;
+    for (int64_t base = l0; base < l1 && j < nsc; base += 32) {
+      const int64_t k = base + lane;
+      const int32_t n = k < l1 ? be[src[k]] - bb[src[k]] : 0;
+      int64_t incl = n;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int64_t excl = prefix + incl - n;
+      // walk boundaries that fall inside this 32-entry window
+      while (j < nsc) {
+        const int64_t target = (S * j) / nsc;
+        const bool hit = (k < l1) && (excl >= target) && (k > prev_b);
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (!m) break;
+        const int first = __ffs(m) - 1;
+        const int64_t kb = base + first;
+        const int64_t pre = __shfl_sync(0xffffffffu, excl, first);
+        emit(j - 1, prev_b, kb, pre - chunk_start_prefix);
+        chunk_start_prefix = pre;
+        prev_b = kb;
+        ++j;
+      }
+      prefix += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    // remaining chunks (degenerate boundaries collapse onto the list end)
+    while (j < nsc) {
+      emit(j - 1, prev_b, prev_b, 0);
+      ++j;
+    }
+    emit(nsc - 1, prev_b, l1, S - chunk_start_prefix);
+    if (lane == 0)
+      for (int32_t tc = 0; tc < ntc; ++tc) {
+        const int32_t t0 = tb + tc * kThreads;
+        red[red_off[w] + tc] = make_int4(t0, min(te, t0 + kThreads), pb + nsc * (t0 - tb), nsc);
+      }
+  }
+}
+
+__global__ void k_gather_items(const P2PItem* __restrict__ in, const int32_t* __restrict__ order, int64_t n,
+                               P2PItem* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[order[i]];
+}
+
+__global__ void k_iota(int32_t* __restrict__ v, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) v[i] = static_cast<int32_t>(i);
+}
+
+void exclusive_scan_i32(fmm_ctx* c, const int32_t* in, int32_t* out, int64_t n) {
+  size_t sb = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, in, out, (int)n, c->stream));
+  CK(cub::DeviceScan::ExclusiveSum(temp_storage(c, sb), sb, in, out, (int)n, c->stream));
+}
+
+}  // namespace
+
+void build_p2p_worklist(fmm_ctx* c) {
+  cudaStream_t s = c->stream;
+  const int64_t nl = c->nleaves;
+  const uint64_t total = static_cast<uint64_t>(c->p2p_body_pairs);
+  // Cost cap per item: an eighth of one SM's fair share, never below 64K pairs, so that a
+  // single heavy target (C3's halo leaf: 60.5 M pairs) is spread over many SMs.
+  uint64_t cmax = total / (148ull * 8ull);
+  if (cmax < 65536ull) cmax = 65536ull;
+
+  int64_t* sum_ns = c->scan_a.ensure(nl + 1);
+  int32_t* counts = c->i32_a.ensure(3 * (nl + 1));
+  int32_t* offs = c->i32_b.ensure(3 * (nl + 1));
+  int32_t *nitems = counts, *nred = counts + (nl + 1), *npart = counts + 2 * (nl + 1);
+  int32_t *item_off = offs, *red_off = offs + (nl + 1), *part_off = offs + 2 * (nl + 1);
+  CK(cudaMemsetAsync(counts, 0, sizeof(int32_t) * 3 * (nl + 1), s));
+  k_leaf_cost<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->leaves.p, nl, c->p2p_off.p, c->p2p_src.p, c->c_body_begin.p,
+                                                     c->c_body_end.p, cmax, sum_ns, nitems, nred, npart);
+  CK_LAUNCH("k_leaf_cost");
+  exclusive_scan_i32(c, nitems, item_off, nl + 1);
+  exclusive_scan_i32(c, nred, red_off, nl + 1);
+  exclusive_scan_i32(c, npart, part_off, nl + 1);
+  int32_t* h = nullptr;
+  CK(cudaMallocHost(&h, 4 * sizeof(int32_t)));
+  CK(cudaMemcpyAsync(&h[0], item_off + nl, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&h[1], red_off + nl, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&h[2], part_off + nl, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const int64_t nitem = h[0], nr = h[1], np = h[2];
+  CK(cudaFreeHost(h));
+  P2PItem* items_raw = reinterpret_cast<P2PItem*>(c->pairs_a.ensure(4 * (nitem + 1)));  // 32 B each
+  P2PItem* items = reinterpret_cast<P2PItem*>(c->p2p_items.ensure(2 * (nitem + 1)));
+  uint64_t* costs = c->keys_a.ensure(nitem + 1);
+  uint64_t* costs_sorted = c->keys_b.ensure(nitem + 1);
+  int4* red = c->p2p_reduce.ensure(nr + 1);
+  c->p2p_partial.ensure(4 * (np + 1));
+  k_write_items<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->leaves.p, nl, c->p2p_off.p, c->p2p_src.p, c->c_body_begin.p,
+                                                       c->c_body_end.p, sum_ns, nitems, item_off, red_off, part_off,
+                                                       items_raw, costs, red);
+  CK_LAUNCH("k_write_items");
+  // cost-sorted (descending, stable) work list: the longest items launch first
+  int32_t* ord_in = c->i32_c.ensure(2 * (nitem + 1));
+  int32_t* ord_out = ord_in + (nitem + 1);
+  k_iota<<<ceil_div(nitem, 256), 256, 0, s>>>(ord_in, nitem);
+  size_t sb = 0;
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, costs, costs_sorted, ord_in, ord_out, (int)nitem, 0, 48, s));
+  CK(cub::DeviceRadixSort::SortPairsDescending(temp_storage(c, sb), sb, costs, costs_sorted, ord_in, ord_out,
+                                               (int)nitem, 0, 48, s));
+  k_gather_items<<<ceil_div(nitem, 256), 256, 0, s>>>(items_raw, ord_out, nitem, items);
+  CK_LAUNCH("k_gather_items");
+  c->n_p2p_items = nitem;
+  c->n_p2p_reduce = nr;
+  c->kernel_launches += 6;
+}
+
+void run_p2p(fmm_ctx* c, cudaStream_t s) {
+  if (!c->have_lists) fail(FMM_ERR_STATE, "p2p: no interaction lists");
+  const int64_t n = c->N;
+  const int wa = c->cfg.with_acc ? 1 : 0;
+  double* phi = c->phi_p2p.ensure(n);
+  double* acc = c->acc_p2p.ensure(3 * n);
+  const P2PItem* items = reinterpret_cast<const P2PItem*>(c->p2p_items.p);
+  if (c->n_p2p_items > 0) {
+    if (c->cfg.precision == FMM_PREC_FP32_P2P) {
+      k_p2p_fp32<<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p,
+                                                              c->c_cr.p, c->bodyf.p, phi, acc, c->p2p_partial.p, wa);
+    } else {
+      k_p2p_fp64<<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p,
+                                                              c->bodies.p, phi, acc, c->p2p_partial.p, wa);
+    }
+    CK_LAUNCH("k_p2p");
+    c->kernel_launches += 1;
+  }
+  if (c->n_p2p_reduce > 0) {
+    k_p2p_reduce<<<(unsigned)c->n_p2p_reduce, 128, 0, s>>>(c->p2p_reduce.p, c->n_p2p_reduce, c->p2p_partial.p, phi,
+                                                          acc, wa);
+    CK_LAUNCH("k_p2p_reduce");
+    c->kernel_launches += 1;
+  }
+}
+
+}  // namespace fmmb
+
+namespace fmmb {
+namespace {
+// Operator-level P2P (kernels.cpp:181-192 + acc) over (target range, source range) pairs of one
+// body array; thread per target body. FP32 mode: coordinates relative to the target range's
+// first body, FP32 pair math, FP64 accumulation (the same arithmetic as k_p2p_fp32).
+__global__ void k_op_p2p(int64_t count, const int4* __restrict__ rng, const double4* __restrict__ b,
+                         int precision, double* __restrict__ phi, double* __restrict__ acc) {
+  const int64_t r = blockIdx.x;
+  if (r >= count) return;
+  const int4 g = rng[r];
+  for (int32_t i = g.x + threadIdx.x; i < g.y; i += blockDim.x) {
+    const double4 t = b[i];
+    double ph = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
+    for (int32_t j = g.z; j < g.w; ++j) {
+      const double4 s = b[j];
+      if (precision == FMM_PREC_FP64) {
+        const double dx = t.x - s.x, dy = t.y - s.y, dz = t.z - s.z;
+        const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+        if (r2 == 0.0) continue;
+        const double ri = 1.0 / sqrt(r2), qr = s.w * ri, qr3 = qr * ri * ri;
+        ph += qr;
+        ax += dx * qr3;
+        ay += dy * qr3;
+        az += dz * qr3;
+      } else {
+        const double4 o = b[g.x];
+        const float dx = static_cast<float>(t.x - o.x) - static_cast<float>(s.x - o.x);
+        const float dy = static_cast<float>(t.y - o.y) - static_cast<float>(s.y - o.y);
+        const float dz = static_cast<float>(t.z - o.z) - static_cast<float>(s.z - o.z);
+        const float r2 = dx * dx + dy * dy + dz * dz;
+        const float ri = r2 > 0.f ? rsqrtf(r2) : 0.f;
+        const float qr = static_cast<float>(s.w) * ri, qr3 = qr * ri * ri;
+        ph += qr;
+        ax += dx * qr3;
+        ay += dy * qr3;
+        az += dz * qr3;
+      }
+    }
+    phi[i] += ph;
+    if (acc) {
+      acc[3 * i] += ax;
+      acc[3 * i + 1] += ay;
+      acc[3 * i + 2] += az;
+    }
+  }
+}
+}  // namespace
+
+void op_p2p(int64_t count, const int32_t* ranges4, const double* xyzq, int64_t nbodies, int precision,
+            double* phi, double* acc) {
+  if (count <= 0 || nbodies <= 0) return;
+  int4* r = nullptr;
+  double4* b = nullptr;
+  double *p = nullptr, *a = nullptr;
+  CK(cudaMalloc(&r, count * sizeof(int4)));
+  CK(cudaMalloc(&b, nbodies * sizeof(double4)));
+  CK(cudaMalloc(&p, nbodies * sizeof(double)));
+  CK(cudaMalloc(&a, nbodies * 3 * sizeof(double)));
+  CK(cudaMemcpy(r, ranges4, count * sizeof(int4), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(b, xyzq, nbodies * sizeof(double4), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(p, phi, nbodies * sizeof(double), cudaMemcpyHostToDevice));
+  if (acc) CK(cudaMemcpy(a, acc, nbodies * 3 * sizeof(double), cudaMemcpyHostToDevice));
+  k_op_p2p<<<(unsigned)count, 64>>>(count, r, b, precision, p, acc ? a : nullptr);
+  CK_LAUNCH("op_p2p");
+  CK(cudaMemcpy(phi, p, nbodies * sizeof(double), cudaMemcpyDeviceToHost));
+  if (acc) CK(cudaMemcpy(acc, a, nbodies * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(r);
+  cudaFree(b);
+  cudaFree(p);
+  cudaFree(a);
+}
+}  // namespace fmmb

@@ -1,0 +1,287 @@
+// traverse.cu — dual tree traversal on the GPU emitting the reference's M2L / P2P lists
+// bit-exactly (reference: mac, traversal.cpp:8-13; split_target_side / process_pair,
+// traversal.hpp:49-94; dual_tree_traverse, traversal.hpp:118-133).
+//
+// The reference's emitted multiset is a pure function of (tree, theta, mutual) and is
+// independent of queue order and of the drain threshold Q (acceptance.cpp:99-123). The GPU
+// therefore replaces the FIFO queue by level-synchronous frontier expansion: every pair of
+// the frontier is examined by one thread (process_pair), emits an M2L or P2P pair or pushes
+// its child pairs to the next frontier. Output slots come from exclusive scans, so the
+// emission order is deterministic. The lists are then grouped into CSR by target with a
+// radix sort on (target, source), i.e. ascending sources within each target.
+// The MAC is evaluated with __dmul_rn/__dadd_rn/__dsqrt_rn: no FMA contraction, exactly
+// std::sqrt(3.0)*(rt+rs) < theta*sqrt((dx*dx+dy*dy)+dz*dz).
+#include <cub/cub.cuh>
+
+#include "context.cuh"
+
+namespace fmmb {
+namespace {
+
+constexpr double kSqrt3 = 1.7320508075688772;  // std::sqrt(3.0), correctly rounded
+
+__device__ __forceinline__ bool mac_exact(const double4 t, const double4 s, double theta) {
+  const double sum_r = __dmul_rn(kSqrt3, __dadd_rn(t.w, s.w));
+  const double dx = __dadd_rn(t.x, -s.x), dy = __dadd_rn(t.y, -s.y), dz = __dadd_rn(t.z, -s.z);
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  return sum_r < __dmul_rn(theta, __dsqrt_rn(d2));
+}
+
+// Outcome of process_pair: kind 0 = M2L, 1 = P2P, 2 = split target, 3 = split source,
+// 4 = mutual self split. nchild = number of pushed pairs.
+__device__ __forceinline__ void classify(const int2 pr, const double4* __restrict__ cr,
+                                         const int32_t* __restrict__ cc, double theta, int mutual,
+                                         int& kind, int& nchild) {
+  const double4 t = cr[pr.x], s = cr[pr.y];
+  const int tc = cc[pr.x], sc = cc[pr.y];
+  if (mac_exact(t, s, theta)) { kind = 0; nchild = 0; return; }
+  if (tc == 0 && sc == 0) { kind = 1; nchild = 0; return; }
+  if (mutual && pr.x == pr.y) { kind = 4; nchild = tc * (tc + 1) / 2; return; }
+  bool split_t;
+  if (tc == 0) split_t = false;            // traversal.hpp:53-57
+  else if (sc == 0) split_t = true;
+  else if (t.w != s.w) split_t = t.w > s.w;
+  else split_t = pr.x <= pr.y;
+  kind = split_t ? 2 : 3;
+  nchild = split_t ? tc : sc;
+}
+
+__global__ void k_classify(const int2* __restrict__ fr, int64_t n, const double4* __restrict__ cr,
+                           const int32_t* __restrict__ cc, double theta, int mutual,
+                           uint64_t* __restrict__ emit, int64_t* __restrict__ push) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int kind, nchild;
+  classify(fr[i], cr, cc, theta, mutual, kind, nchild);
+  emit[i] = kind == 0 ? 1ull : (kind == 1 ? (1ull << 32) : 0ull);
+  push[i] = nchild;
+}
+
+__global__ void k_expand(const int2* __restrict__ fr, int64_t n, const double4* __restrict__ cr,
+                         const int32_t* __restrict__ cc, const int32_t* __restrict__ cb, double theta,
+                         int mutual, const uint64_t* __restrict__ emit_off,
+                         const int64_t* __restrict__ push_off, int2* __restrict__ m2l, int64_t m2l_base,
+                         int2* __restrict__ p2p, int64_t p2p_base, int2* __restrict__ next) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int2 pr = fr[i];
+  int kind, nchild;
+  classify(pr, cr, cc, theta, mutual, kind, nchild);
+  const uint64_t eo = emit_off[i];
+  if (kind == 0) { m2l[m2l_base + (int64_t)(eo & 0xffffffffu)] = pr; return; }
+  if (kind == 1) { p2p[p2p_base + (int64_t)(eo >> 32)] = pr; return; }
+  int64_t o = push_off[i];
+  if (kind == 2) {
+    const int32_t b = cb[pr.x];
+    for (int k = 0; k < nchild; ++k) next[o + k] = make_int2(b + k, pr.y);
+  } else if (kind == 3) {
+    const int32_t b = cb[pr.y];
+    for (int k = 0; k < nchild; ++k) next[o + k] = make_int2(pr.x, b + k);
+  } else {
+    const int32_t b = cb[pr.x], m = cc[pr.x];
+    for (int a = 0; a < m; ++a)
+      for (int c = a; c < m; ++c) next[o++] = make_int2(b + a, b + c);
+  }
+}
+
+__global__ void k_pair_keys(const int2* __restrict__ pr, int64_t n, int sbits, uint64_t* __restrict__ keys) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = ((uint64_t)(uint32_t)pr[i].x << sbits) | (uint32_t)pr[i].y;
+}
+
+__global__ void k_csr_from_keys(const uint64_t* __restrict__ keys, int64_t n, int sbits, int64_t ncells,
+                                int64_t* __restrict__ off, int32_t* __restrict__ src) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i > n) return;
+  const uint64_t mask = (1ull << sbits) - 1;
+  const int64_t t = i < n ? (int64_t)(keys[i] >> sbits) : ncells;
+  const int64_t tp = i > 0 ? (int64_t)(keys[i - 1] >> sbits) : -1;
+  if (i < n) src[i] = (int32_t)(keys[i] & mask);
+  for (int64_t c = tp + 1; c <= t; ++c) off[c] = i;  // targets tp+1..t start at i
+}
+
+__global__ void k_p2p_body_pairs(const int64_t* __restrict__ off, const int32_t* __restrict__ src,
+                                 int64_t ncells, const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
+                                 unsigned long long* __restrict__ total) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long v = 0;
+  if (t < ncells) {
+    const int64_t nt = be[t] - bb[t];
+    for (int64_t k = off[t]; k < off[t + 1]; ++k) v += (unsigned long long)(nt * (be[src[k]] - bb[src[k]]));
+  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(total, v);
+}
+
+__global__ void k_flag_nonempty(const int64_t* __restrict__ off, int64_t ncells, int32_t* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < ncells) flag[i] = off[i + 1] > off[i];
+}
+
+int bits_for(uint64_t v) {
+  int b = 1;
+  while (b < 63 && (v >> b)) ++b;
+  return b;
+}
+
+template <class T>
+void grow_keep(fmm_ctx* c, DBuf<T>& buf, size_t used, size_t need) {
+  if (need <= buf.cap) return;
+  T* fresh = nullptr;
+  const size_t want = need + need / 2 + 1024;
+  CK(cudaMalloc(&fresh, want * sizeof(T)));
+  if (buf.p && used) CK(cudaMemcpyAsync(fresh, buf.p, used * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (buf.p) CK(cudaFree(buf.p));
+  buf.p = fresh;
+  buf.cap = want;
+}
+
+// Groups (target, source) pairs into CSR by target with ascending sources.
+void to_csr(fmm_ctx* c, const int2* d_pairs, int64_t n, DBuf<int64_t>& off, DBuf<int32_t>& src) {
+  cudaStream_t s = c->stream;
+  const int64_t nc = c->ncells;
+  off.ensure(nc + 1);
+  src.ensure(n > 0 ? n : 1);
+  if (n == 0) {
+    CK(cudaMemsetAsync(off.p, 0, sizeof(int64_t) * (nc + 1), s));
+    return;
+  }
+  const int sbits = bits_for(static_cast<uint64_t>(nc));
+  uint64_t* ka = c->keys_a.ensure(n);
+  uint64_t* kb = c->keys_b.ensure(n);
+  k_pair_keys<<<ceil_div(n, 256), 256, 0, s>>>(d_pairs, n, sbits, ka);
+  size_t sb = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, ka, kb, (int)n, 0, 2 * sbits, s));
+  CK(cub::DeviceRadixSort::SortKeys(temp_storage(c, sb), sb, ka, kb, (int)n, 0, 2 * sbits, s));
+  k_csr_from_keys<<<ceil_div(n + 1, 256), 256, 0, s>>>(kb, n, sbits, nc, off.p, src.p);
+  CK_LAUNCH("to_csr");
+  c->kernel_launches += 4;
+}
+
+}  // namespace
+
+void lists_from_pairs(fmm_ctx* c, const int2* d_m2l, int64_t n_m2l, const int2* d_p2p, int64_t n_p2p) {
+  cudaStream_t s = c->stream;
+  to_csr(c, d_m2l, n_m2l, c->m2l_off, c->m2l_src);
+  to_csr(c, d_p2p, n_p2p, c->p2p_off, c->p2p_src);
+  c->n_m2l = n_m2l;
+  c->n_p2p = n_p2p;
+  // body-pair count (P2P work) and the M2L target list
+  unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->d_counters.ensure(4));
+  CK(cudaMemsetAsync(tot, 0, sizeof(unsigned long long), s));
+  k_p2p_body_pairs<<<ceil_div(c->ncells, 256), 256, 0, s>>>(c->p2p_off.p, c->p2p_src.p, c->ncells,
+                                                            c->c_body_begin.p, c->c_body_end.p, tot);
+  int32_t* flag = c->i32_c.ensure(c->ncells);
+  k_flag_nonempty<<<ceil_div(c->ncells, 256), 256, 0, s>>>(c->m2l_off.p, c->ncells, flag);
+  CK_LAUNCH("k_flag_nonempty");
+  int32_t* targets = c->m2l_targets.ensure(c->ncells);
+  int64_t* nsel = c->d_counters.p + 1;
+  size_t sb = 0;
+  cub::CountingInputIterator<int32_t> it(0);
+  CK(cub::DeviceSelect::Flagged(nullptr, sb, it, flag, targets, nsel, (int)c->ncells, s));
+  CK(cub::DeviceSelect::Flagged(temp_storage(c, sb), sb, it, flag, targets, nsel, (int)c->ncells, s));
+  int64_t h[2];
+  CK(cudaMemcpyAsync(h, c->d_counters.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  c->p2p_body_pairs = h[0];
+  c->n_m2l_targets = h[1];
+  c->kernel_launches += 3;
+  c->have_lists = true;
+  build_p2p_worklist(c);
+}
+
+void traverse(fmm_ctx* c) {
+  if (!c->have_tree) fail(FMM_ERR_STATE, "traverse: no tree");
+  const double theta = c->cfg.theta;
+  if (!(theta > 0.0 && theta < 1.0)) fail(FMM_ERR_THETA, "theta must be in (0,1)");
+  cudaStream_t s = c->stream;
+  const int mutual = c->cfg.mutual ? 1 : 0;
+
+  int64_t nf = 1, nm = 0, np = 0;
+  int2 root = make_int2(0, 0);
+  c->pairs_a.ensure(1024);
+  c->pairs_b.ensure(1024);
+  c->pairs_c.ensure(1024);
+  DBuf<int2>* m2l = &c->pairs_b;
+  DBuf<int2>* p2p = &c->pairs_c;
+  DBuf<int2> front_b;  // second frontier buffer
+  DBuf<int2>* fa = &c->pairs_a;
+  DBuf<int2>* fb = &front_b;
+  fb->ensure(1024);
+  CK(cudaMemcpyAsync(fa->p, &root, sizeof(int2), cudaMemcpyHostToDevice, s));
+  int64_t* hcnt = nullptr;
+  CK(cudaMallocHost(&hcnt, 4 * sizeof(int64_t)));
+  while (nf > 0) {
+    uint64_t* emit = c->keys_a.ensure(nf + 1);
+    uint64_t* emit_off = c->keys_b.ensure(nf + 1);
+    int64_t* push = c->scan_a.ensure(2 * (nf + 1));
+    int64_t* push_off = push + (nf + 1);
+    k_classify<<<ceil_div(nf, 256), 256, 0, s>>>(fa->p, nf, c->c_cr.p, c->c_child_count.p, theta, mutual,
+                                                 emit, push);
+    CK_LAUNCH("k_classify");
+    CK(cudaMemsetAsync(emit + nf, 0, sizeof(uint64_t), s));
+    CK(cudaMemsetAsync(push + nf, 0, sizeof(int64_t), s));
+    size_t sb1 = 0, sb2 = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, sb1, emit, emit_off, (int)(nf + 1), s));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, sb2, push, push_off, (int)(nf + 1), s));
+    void* tmp = temp_storage(c, sb1 > sb2 ? sb1 : sb2);
+    CK(cub::DeviceScan::ExclusiveSum(tmp, sb1, emit, emit_off, (int)(nf + 1), s));
+    CK(cub::DeviceScan::ExclusiveSum(tmp, sb2, push, push_off, (int)(nf + 1), s));
+    uint64_t he = 0;
+    CK(cudaMemcpyAsync(&hcnt[0], emit_off + nf, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hcnt[1], push_off + nf, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    he = static_cast<uint64_t>(hcnt[0]);
+    const int64_t add_m = static_cast<int64_t>(he & 0xffffffffu), add_p = static_cast<int64_t>(he >> 32);
+    const int64_t nnext = hcnt[1];
+    grow_keep(c, *m2l, nm, nm + add_m);
+    grow_keep(c, *p2p, np, np + add_p);
+    fb->ensure(nnext > 0 ? nnext : 1);
+    k_expand<<<ceil_div(nf, 256), 256, 0, s>>>(fa->p, nf, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p,
+                                               theta, mutual, emit_off, push_off, m2l->p, nm, p2p->p, np, fb->p);
+    CK_LAUNCH("k_expand");
+    c->kernel_launches += 4;
+    nm += add_m;
+    np += add_p;
+    nf = nnext;
+    std::swap(fa, fb);
+  }
+  CK(cudaStreamSynchronize(s));
+  CK(cudaFreeHost(hcnt));
+  lists_from_pairs(c, m2l->p, nm, p2p->p, np);
+  CK(cudaStreamSynchronize(s));  // front_b is freed on return
+}
+
+}  // namespace fmmb
+
+namespace fmmb {
+namespace {
+__global__ void k_op_mac(int64_t count, const double* __restrict__ tc, const double* __restrict__ tr,
+                         const double* __restrict__ sc, const double* __restrict__ sr, double theta,
+                         int32_t* __restrict__ out) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  out[k] = mac_exact(make_double4(tc[3 * k], tc[3 * k + 1], tc[3 * k + 2], tr[k]),
+                     make_double4(sc[3 * k], sc[3 * k + 1], sc[3 * k + 2], sr[k]), theta) ? 1 : 0;
+}
+}  // namespace
+
+void op_mac(int64_t count, const double* tc3, const double* tr, const double* sc3, const double* sr,
+            double theta, int32_t* out) {
+  if (count <= 0) return;
+  double* d = nullptr;
+  int32_t* o = nullptr;
+  CK(cudaMalloc(&d, count * 8 * sizeof(double)));
+  CK(cudaMalloc(&o, count * sizeof(int32_t)));
+  CK(cudaMemcpy(d, tc3, count * 3 * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d + 3 * count, tr, count * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d + 4 * count, sc3, count * 3 * sizeof(double), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d + 7 * count, sr, count * sizeof(double), cudaMemcpyHostToDevice));
+  k_op_mac<<<ceil_div(count, 128), 128>>>(count, d, d + 3 * count, d + 4 * count, d + 7 * count, theta, o);
+  CK_LAUNCH("op_mac");
+  CK(cudaMemcpy(out, o, count * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  cudaFree(o);
+}
+}  // namespace fmmb

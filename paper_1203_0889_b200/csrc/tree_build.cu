@@ -1,0 +1,443 @@
+// tree_build.cu — bit-exact adaptive octree build on the GPU (reference: build_tree,
+// tree.cpp:52-119; compute_bounds, tree.cpp:10-23).
+//
+// Design: instead of the reference's per-cell BFS counting sort, every body descends the
+// octree once with the SAME recursively computed FP64 centres the reference uses
+// (octant_of, tree.cpp:45-48; child centre = parent + child_radius*(+-1), tree.cpp:102-103)
+// and records its 21-level path as a 63-bit key. One stable radix sort of (key, input
+// index) orders bodies by path; cells are then materialised level by level from key-digit
+// boundaries (binary searches inside each splitting cell's sorted range), which reproduces
+// the reference's BFS numbering (level-contiguous, children in octant order, empty octants
+// skipped). A second sort by (leaf, input index) restores the reference's within-leaf order
+// (stable counting sorts keep input order inside a leaf, tree.cpp:82-93).
+// All FP64 arithmetic uses explicit __dadd_rn/__dmul_rn so nothing is contracted to FMA.
+#include <cub/cub.cuh>
+
+#include "context.cuh"
+
+namespace fmmb {
+namespace {
+
+constexpr int kLevels = FMM_MAX_LEVEL;  // 21 levels -> 63 key bits
+constexpr double kMarginFactor = 1.0 + 1e-6;  // tree.cpp:21 (evaluated exactly at compile time)
+constexpr double kMinHalfSide = 0.5;          // tree.hpp:17
+
+__device__ __forceinline__ double dmin_ref(double a, double b) { return b < a ? b : a; }  // cwiseMin
+__device__ __forceinline__ double dmax_ref(double a, double b) { return a < b ? b : a; }  // cwiseMax
+
+// ---- compute_bounds: block partials then one finishing block ----------------------------
+__global__ void k_bounds_partial(const double4* __restrict__ xyzq, int64_t n, double* __restrict__ part) {
+  double lo[3] = {xyzq[0].x, xyzq[0].y, xyzq[0].z};
+  double hi[3] = {lo[0], lo[1], lo[2]};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double4 b = xyzq[i];
+    lo[0] = dmin_ref(lo[0], b.x); lo[1] = dmin_ref(lo[1], b.y); lo[2] = dmin_ref(lo[2], b.z);
+    hi[0] = dmax_ref(hi[0], b.x); hi[1] = dmax_ref(hi[1], b.y); hi[2] = dmax_ref(hi[2], b.z);
+  }
+  __shared__ double s[6][32];
+  for (int d = 0; d < 3; ++d) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[d] = dmin_ref(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+      hi[d] = dmax_ref(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+    }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0)
+    for (int d = 0; d < 3; ++d) { s[d][w] = lo[d]; s[3 + d][w] = hi[d]; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+    for (int k = 1; k < nw; ++k)
+      for (int d = 0; d < 3; ++d) {
+        s[d][0] = dmin_ref(s[d][0], s[d][k]);
+        s[3 + d][0] = dmax_ref(s[3 + d][0], s[3 + d][k]);
+      }
+    for (int d = 0; d < 6; ++d) part[blockIdx.x * 6 + d] = s[d][0];
+  }
+}
+
+// Finishes the reduction and evaluates the Domain formula of tree.cpp:19-21 exactly.
+__global__ void k_bounds_final(const double* __restrict__ part, int nparts, double* __restrict__ dom) {
+  if (threadIdx.x != 0) return;
+  double lo[3] = {part[0], part[1], part[2]}, hi[3] = {part[3], part[4], part[5]};
+  for (int k = 1; k < nparts; ++k)
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = dmin_ref(lo[d], part[6 * k + d]);
+      hi[d] = dmax_ref(hi[d], part[6 * k + 3 + d]);
+    }
+  for (int d = 0; d < 3; ++d) dom[d] = __dmul_rn(0.5, __dadd_rn(lo[d], hi[d]));
+  double ext = __dadd_rn(hi[0], -lo[0]);
+  ext = dmax_ref(ext, __dadd_rn(hi[1], -lo[1]));  // (hi - lo).maxCoeff()
+  ext = dmax_ref(ext, __dadd_rn(hi[2], -lo[2]));
+  const double extent_half = __dmul_rn(0.5, ext);
+  const double h = __dmul_rn(extent_half, kMarginFactor);
+  dom[3] = h < kMinHalfSide ? kMinHalfSide : h;  // std::max(h, kMinHalfSide)
+}
+
+// ---- per-body octant descent (octant_of with recursive centres) ------------------------
+__global__ void k_keys(const double4* __restrict__ xyzq, int64_t n, const double* __restrict__ dom,
+                       uint64_t* __restrict__ keys, int32_t* __restrict__ idx) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 b = xyzq[i];
+  double cx = dom[0], cy = dom[1], cz = dom[2], r = dom[3];
+  uint64_t key = 0;
+#pragma unroll 1
+  for (int l = 0; l < kLevels; ++l) {
+    const double cr = __dmul_rn(0.5, r);
+    const int ox = b.x >= cx, oy = b.y >= cy, oz = b.z >= cz;  // tree.cpp:45-48
+    key = (key << 3) | (uint64_t)(ox | (oy << 1) | (oz << 2));
+    cx = __dadd_rn(cx, ox ? cr : -cr);  // center + child_radius * (+-1), tree.cpp:102-103
+    cy = __dadd_rn(cy, oy ? cr : -cr);
+    cz = __dadd_rn(cz, oz ? cr : -cr);
+    r = cr;
+  }
+  keys[i] = key;
+  idx[i] = static_cast<int32_t>(i);
+}
+
+__device__ __forceinline__ int digit_at(uint64_t key, int child_level) {
+  return static_cast<int>((key >> (3 * (kLevels - child_level))) & 7u);
+}
+
+// First index in [lo, hi) whose digit at child_level is >= d (digits are sorted there).
+__device__ __forceinline__ int32_t lower_digit(const uint64_t* __restrict__ k, int32_t lo, int32_t hi,
+                                               int child_level, int d) {
+  while (lo < hi) {
+    const int32_t mid = lo + ((hi - lo) >> 1);
+    if (digit_at(k[mid], child_level) < d) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Children count of every cell of one level (0 when the cell is a leaf).
+__global__ void k_count_children(int32_t cbeg, int32_t cend, int level, int n_crit,
+                                 const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
+                                 const uint64_t* __restrict__ skeys, int32_t* __restrict__ nchild) {
+  const int32_t ci = cbeg + blockIdx.x * blockDim.x + threadIdx.x;
+  if (ci >= cend) return;
+  const int32_t b = bb[ci], e = be[ci];
+  int cnt = 0;
+  if (e - b > n_crit && level < kLevels) {  // tree.cpp:78
+    int32_t start = b;
+    for (int o = 0; o < 8; ++o) {
+      const int32_t stop = (o == 7) ? e : lower_digit(skeys, start, e, level + 1, o + 1);
+      cnt += stop > start;
+      start = stop;
+    }
+  }
+  nchild[ci - cbeg] = cnt;
+}
+
+// Materialises the children of one level; offsets = exclusive scan of nchild.
+__global__ void k_write_children(int32_t cbeg, int32_t cend, int level, int32_t next_begin,
+                                 const int32_t* __restrict__ nchild, const int32_t* __restrict__ offs,
+                                 const uint64_t* __restrict__ skeys, int32_t* __restrict__ c_level,
+                                 uint64_t* __restrict__ c_key, double4* __restrict__ c_cr,
+                                 int32_t* __restrict__ bb, int32_t* __restrict__ be,
+                                 int32_t* __restrict__ cb, int32_t* __restrict__ cc,
+                                 int32_t* __restrict__ par) {
+  const int32_t ci = cbeg + blockIdx.x * blockDim.x + threadIdx.x;
+  if (ci >= cend) return;
+  const int k = ci - cbeg;
+  if (nchild[k] == 0) return;
+  const int32_t b = bb[ci], e = be[ci];
+  const double4 pc = c_cr[ci];
+  const uint64_t pkey = c_key[ci];
+  const double cr = __dmul_rn(0.5, pc.w);
+  int32_t out = next_begin + offs[k];
+  cb[ci] = out;
+  cc[ci] = nchild[k];
+  int32_t start = b;
+  for (int o = 0; o < 8; ++o) {
+    const int32_t stop = (o == 7) ? e : lower_digit(skeys, start, e, level + 1, o + 1);
+    if (stop > start) {
+      c_level[out] = level + 1;
+      c_key[out] = (pkey << 3) | (uint64_t)o;
+      c_cr[out] = make_double4(__dadd_rn(pc.x, (o & 1) ? cr : -cr), __dadd_rn(pc.y, (o & 2) ? cr : -cr),
+                               __dadd_rn(pc.z, (o & 4) ? cr : -cr), cr);
+      bb[out] = start;
+      be[out] = stop;
+      cb[out] = 0;
+      cc[out] = 0;
+      par[out] = ci;
+      ++out;
+    }
+    start = stop;
+  }
+}
+
+__global__ void k_init_root(const double* __restrict__ dom, int32_t n, int32_t* c_level, uint64_t* c_key,
+                            double4* c_cr, int32_t* bb, int32_t* be, int32_t* cb, int32_t* cc, int32_t* par) {
+  c_level[0] = 0;
+  c_key[0] = 0;
+  c_cr[0] = make_double4(dom[0], dom[1], dom[2], dom[3]);
+  bb[0] = 0;
+  be[0] = n;
+  cb[0] = 0;
+  cc[0] = 0;
+  par[0] = -1;
+}
+
+// Leaf-of-body map (warp per leaf) and the (leaf begin, input index) composite key.
+__global__ void k_leaf_map(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __restrict__ bb,
+                           const int32_t* __restrict__ be, const int32_t* __restrict__ sidx,
+                           int32_t* __restrict__ leaf_of_body, uint64_t* __restrict__ ckey) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nleaves) return;
+  const int32_t leaf = leaves[w];
+  const int32_t b = bb[leaf], e = be[leaf];
+  for (int32_t i = b + lane; i < e; i += 32) {
+    leaf_of_body[i] = leaf;
+    if (ckey) ckey[i] = ((uint64_t)(uint32_t)b << 32) | (uint32_t)sidx[i];
+  }
+}
+
+__global__ void k_perm_from_ckey(const uint64_t* __restrict__ ckey, int64_t n, int32_t* __restrict__ perm) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) perm[i] = static_cast<int32_t>(ckey[i] & 0xffffffffu);
+}
+
+__global__ void k_gather(const double4* __restrict__ in, const int32_t* __restrict__ perm,
+                         const int32_t* __restrict__ leaf_of_body, const double4* __restrict__ c_cr,
+                         int64_t n, double4* __restrict__ bodies, float4* __restrict__ bodyf) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 b = in[perm[i]];
+  bodies[i] = b;
+  const double4 c = c_cr[leaf_of_body[i]];
+  bodyf[i] = make_float4(static_cast<float>(b.x - c.x), static_cast<float>(b.y - c.y),
+                         static_cast<float>(b.z - c.z), static_cast<float>(b.w));
+}
+
+__global__ void k_flag_leaves(const int32_t* __restrict__ cc, int64_t ncells, int32_t* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < ncells) flag[i] = cc[i] == 0;
+}
+
+template <class T>
+void grow_preserve(fmm_ctx* c, DBuf<T>& buf, size_t used, size_t need) {
+  if (need <= buf.cap) return;
+  T* old = buf.p;
+  size_t want = need * 2 + 1024;
+  T* fresh = nullptr;
+  CK(cudaMalloc(&fresh, want * sizeof(T)));
+  if (old && used) CK(cudaMemcpyAsync(fresh, old, used * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
+  if (old) {
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaFree(old));
+  }
+  buf.p = fresh;
+  buf.cap = want;
+}
+
+int bits_for(uint64_t v) {
+  int b = 1;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+
+}  // namespace
+
+void* temp_storage(fmm_ctx* c, size_t bytes) { return c->tmp.ensure(bytes > 0 ? bytes : 1); }
+
+void build_tree(fmm_ctx* c) {
+  if (!c->have_bodies) fail(FMM_ERR_STATE, "build_tree: no bodies set");
+  const int64_t n = c->N;
+  if (n <= 0) fail(FMM_ERR_EMPTY_INPUT, "empty input");
+  if (c->cfg.n_crit < 1) fail(FMM_ERR_NCRIT, "n_crit must be >= 1");
+  if (n >= (int64_t(1) << 31)) fail(FMM_ERR_UNSUPPORTED, "more than 2^31-1 bodies");
+  cudaStream_t s = c->stream;
+
+  // 1. compute_bounds
+  const int nparts = 592;  // 4 x 148 SMs
+  double* part = c->small.ensure(nparts * 6 + 8);
+  double* dom = part + nparts * 6;
+  k_bounds_partial<<<nparts, 256, 0, s>>>(c->xyzq_in.p, n, part);
+  k_bounds_final<<<1, 32, 0, s>>>(part, nparts, dom);
+  CK_LAUNCH("k_bounds");
+  double hdom[4];
+  CK(cudaMemcpyAsync(hdom, dom, sizeof(hdom), cudaMemcpyDeviceToHost, s));
+
+  // 2. keys by octant descent, 3. stable radix sort (key, index)
+  uint64_t* keys = c->keys_a.ensure(n);
+  int32_t* idx = c->idx_a.ensure(n);
+  k_keys<<<ceil_div(n, 256), 256, 0, s>>>(c->xyzq_in.p, n, dom, keys, idx);
+  CK_LAUNCH("k_keys");
+  uint64_t* skeys = c->keys_b.ensure(n);
+  int32_t* sidx = c->idx_b.ensure(n);
+  size_t tbytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, keys, skeys, idx, sidx, (int)n, 0, 3 * kLevels, s));
+  void* tmp = temp_storage(c, tbytes);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tbytes, keys, skeys, idx, sidx, (int)n, 0, 3 * kLevels, s));
+
+  c->center[0] = hdom[0];
+  c->center[1] = hdom[1];
+  c->center[2] = hdom[2];
+  c->half_side = hdom[3];
+
+  // 4. level-by-level cell materialisation
+  size_t cap = 1024;
+  auto ensure_cells = [&](size_t used, size_t need) {
+    grow_preserve(c, c->c_level, used, need);
+    grow_preserve(c, c->c_key, used, need);
+    grow_preserve(c, c->c_cr, used, need);
+    grow_preserve(c, c->c_body_begin, used, need);
+    grow_preserve(c, c->c_body_end, used, need);
+    grow_preserve(c, c->c_child_begin, used, need);
+    grow_preserve(c, c->c_child_count, used, need);
+    grow_preserve(c, c->c_parent, used, need);
+  };
+  ensure_cells(0, cap);
+  k_init_root<<<1, 1, 0, s>>>(dom, (int32_t)n, c->c_level.p, c->c_key.p, c->c_cr.p, c->c_body_begin.p,
+                              c->c_body_end.p, c->c_child_begin.p, c->c_child_count.p, c->c_parent.p);
+  CK_LAUNCH("k_init_root");
+  int64_t ncells = 1;
+  int level = 0;
+  for (int l = 0; l < FMM_MAX_LEVEL + 2; ++l) c->level_start[l] = 0;
+  c->level_start[0] = 0;
+  c->level_start[1] = 1;
+  int32_t* hbuf = nullptr;
+  CK(cudaMallocHost(&hbuf, 2 * sizeof(int32_t)));
+  while (true) {
+    const int32_t cb = c->level_start[level], ce = c->level_start[level + 1];
+    const int32_t m = ce - cb;
+    int32_t* nchild = c->i32_a.ensure(m + 1);
+    int32_t* offs = c->i32_b.ensure(m + 1);
+    k_count_children<<<ceil_div(m, 128), 128, 0, s>>>(cb, ce, level, c->cfg.n_crit, c->c_body_begin.p,
+                                                     c->c_body_end.p, skeys, nchild);
+    CK_LAUNCH("k_count_children");
+    size_t sb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, nchild, offs, m + 1, s));
+    CK(cudaMemsetAsync(nchild + m, 0, sizeof(int32_t), s));
+    CK(cub::DeviceScan::ExclusiveSum(temp_storage(c, sb), sb, nchild, offs, m + 1, s));
+    CK(cudaMemcpyAsync(hbuf, offs + m, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const int32_t nnew = hbuf[0];
+    if (nnew == 0) break;
+    ensure_cells(ncells, ncells + nnew);
+    k_write_children<<<ceil_div(m, 128), 128, 0, s>>>(cb, ce, level, ce, nchild, offs, skeys, c->c_level.p,
+                                                     c->c_key.p, c->c_cr.p, c->c_body_begin.p, c->c_body_end.p,
+                                                     c->c_child_begin.p, c->c_child_count.p, c->c_parent.p);
+    CK_LAUNCH("k_write_children");
+    ncells += nnew;
+    ++level;
+    c->level_start[level + 1] = static_cast<int32_t>(ncells);
+    if (ncells >= (int64_t(1) << 31) - 16) fail(FMM_ERR_UNSUPPORTED, "too many cells");
+  }
+  CK(cudaFreeHost(hbuf));
+  for (int l = level + 2; l < FMM_MAX_LEVEL + 2; ++l) c->level_start[l] = static_cast<int32_t>(ncells);
+  c->ncells = ncells;
+  c->depth = level;
+
+  // 5. leaves (ascending cell index)
+  int32_t* flag = c->i32_a.ensure(ncells);
+  k_flag_leaves<<<ceil_div(ncells, 256), 256, 0, s>>>(c->c_child_count.p, ncells, flag);
+  int32_t* leaves = c->leaves.ensure(ncells);
+  int64_t* nsel = c->d_counters.ensure(4);
+  {
+    size_t sb = 0;
+    cub::CountingInputIterator<int32_t> it(0);
+    CK(cub::DeviceSelect::Flagged(nullptr, sb, it, flag, leaves, nsel, (int)ncells, s));
+    CK(cub::DeviceSelect::Flagged(temp_storage(c, sb), sb, it, flag, leaves, nsel, (int)ncells, s));
+  }
+  int64_t hn = 0;
+  CK(cudaMemcpyAsync(&hn, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  c->nleaves = hn;
+
+  // 6. within-leaf input order: sort by (leaf body_begin << 32 | input index)
+  int32_t* leaf_of_body = c->leaf_of_body.ensure(n);
+  uint64_t* ckey = c->keys_a.ensure(n);  // keys no longer needed
+  k_leaf_map<<<ceil_div(c->nleaves * 32, 256), 256, 0, s>>>(leaves, c->nleaves, c->c_body_begin.p,
+                                                              c->c_body_end.p, sidx, leaf_of_body, ckey);
+  CK_LAUNCH("k_leaf_map");
+  uint64_t* ckey2 = c->keys_b.ensure(n);  // sorted keys no longer needed after leaf map
+  {
+    const int end_bit = 32 + bits_for(static_cast<uint64_t>(n));
+    size_t sb = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, ckey, ckey2, (int)n, 0, end_bit, s));
+    CK(cub::DeviceRadixSort::SortKeys(temp_storage(c, sb), sb, ckey, ckey2, (int)n, 0, end_bit, s));
+  }
+  int32_t* perm = c->perm.ensure(n);
+  k_perm_from_ckey<<<ceil_div(n, 256), 256, 0, s>>>(ckey2, n, perm);
+  CK_LAUNCH("k_perm_from_ckey");
+  c->kernel_launches += 8 + 2 * level;
+  c->have_tree = true;
+  gather_bodies(c);
+}
+
+void gather_bodies(fmm_ctx* c) {
+  cudaStream_t s = c->stream;
+  const int64_t n = c->N;
+  int32_t* leaf_of_body = c->leaf_of_body.ensure(n);
+  k_leaf_map<<<ceil_div(c->nleaves * 32, 256), 256, 0, s>>>(c->leaves.p, c->nleaves, c->c_body_begin.p,
+                                                              c->c_body_end.p, nullptr, leaf_of_body, nullptr);
+  k_gather<<<ceil_div(n, 256), 256, 0, s>>>(c->xyzq_in.p, c->perm.p, leaf_of_body, c->c_cr.p, n,
+                                            c->bodies.ensure(n), c->bodyf.ensure(n));
+  CK_LAUNCH("k_gather");
+  c->kernel_launches += 2;
+}
+
+}  // namespace fmmb
+
+// ---- single-operator entry points ---------------------------------------------------------
+namespace fmmb {
+namespace {
+// morton_key (tree.cpp:25-39): floor-based interleave (tests-only API of the reference).
+__global__ void k_morton(int64_t count, const double* __restrict__ p3, double cx, double cy, double cz,
+                         double half, int level, uint64_t* __restrict__ out) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const uint64_t cells = uint64_t(1) << level;
+  const double inv_cell = __ddiv_rn(static_cast<double>(cells), __dmul_rn(2.0, half));
+  const double c[3] = {cx, cy, cz};
+  uint64_t key = 0;
+  for (int axis = 0; axis < 3; ++axis) {
+    const double offset = __dadd_rn(p3[3 * k + axis], -__dadd_rn(c[axis], -half));
+    long long idx = static_cast<long long>(floor(__dmul_rn(offset, inv_cell)));
+    if (idx < 0) idx = 0;
+    if (idx > static_cast<long long>(cells) - 1) idx = static_cast<long long>(cells) - 1;
+    for (int bit = 0; bit < level; ++bit) key |= ((static_cast<uint64_t>(idx) >> bit) & 1u) << (3 * bit + axis);
+  }
+  out[k] = key;
+}
+}  // namespace
+
+void op_bounds(const double* xyzq, int64_t n, double* center3, double* half_side) {
+  if (n <= 0) fail(FMM_ERR_EMPTY_INPUT, "empty input");
+  double4* d = nullptr;
+  double* part = nullptr;
+  CK(cudaMalloc(&d, n * sizeof(double4)));
+  CK(cudaMalloc(&part, (592 * 6 + 8) * sizeof(double)));
+  CK(cudaMemcpy(d, xyzq, n * sizeof(double4), cudaMemcpyHostToDevice));
+  k_bounds_partial<<<592, 256>>>(d, n, part);
+  k_bounds_final<<<1, 32>>>(part, 592, part + 592 * 6);
+  CK_LAUNCH("op_bounds");
+  double h[4];
+  CK(cudaMemcpy(h, part + 592 * 6, sizeof(h), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  cudaFree(part);
+  center3[0] = h[0];
+  center3[1] = h[1];
+  center3[2] = h[2];
+  *half_side = h[3];
+}
+
+void op_morton(int64_t count, const double* p3, const double* center3, double half_side, int level,
+               uint64_t* out) {
+  if (level < 0 || level > FMM_MAX_LEVEL) fail(FMM_ERR_LEVEL_OVERFLOW, "level overflow");
+  if (count <= 0) return;
+  double* d = nullptr;
+  uint64_t* o = nullptr;
+  CK(cudaMalloc(&d, count * 3 * sizeof(double)));
+  CK(cudaMalloc(&o, count * sizeof(uint64_t)));
+  CK(cudaMemcpy(d, p3, count * 3 * sizeof(double), cudaMemcpyHostToDevice));
+  k_morton<<<ceil_div(count, 128), 128>>>(count, d, center3[0], center3[1], center3[2], half_side, level, o);
+  CK_LAUNCH("op_morton");
+  CK(cudaMemcpy(out, o, count * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  cudaFree(o);
+}
+}  // namespace fmmb
