@@ -100,6 +100,7 @@ int fmm_create(const fmm_config* cfg, fmm_ctx** out) {
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       CK(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
       for (int i = 0; i < EV_COUNT; ++i) CK(cudaEventCreate(&c->ev[i]));
+      CK(cudaMallocHost(&c->hpin, 64 * sizeof(int64_t)));
     } catch (...) {
       delete c;
       throw;
@@ -116,6 +117,7 @@ void fmm_destroy(fmm_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+  if (ctx->hpin) cudaFreeHost(ctx->hpin);
   delete ctx;
 }
 

@@ -74,6 +74,9 @@ struct fmm_ctx {
   fmmb::DBuf<int32_t> i32_a, i32_b, i32_c;
   fmmb::DBuf<int64_t> d_counters;
   fmmb::DBuf<double> small;
+  fmmb::DBuf<int2> pairs_d;         // second traversal frontier
+  fmmb::DBuf<int32_t> bnd;           // child boundaries of one level (9 per cell)
+  int64_t* hpin = nullptr;           // pinned host scratch (64 x int64)
 
   // state
   bool have_bodies = false, have_tree = false, have_lists = false, have_M = false,

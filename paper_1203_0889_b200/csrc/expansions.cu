@@ -122,7 +122,8 @@ k_p2m(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __rest
 }
 
 // ------------------------------------------------------------------------------ M2M ----
-// Warp per non-leaf cell of one level; children accumulated in order k = 0..count-1.
+// Warp per non-leaf cell of one level; children accumulated in order k = 0..count-1, each
+// child's multipole staged in shared memory with the power lines d^k/k! of its shift.
 template <int P>
 __global__ void __launch_bounds__(128)
 k_m2m(int32_t cbeg, int32_t cend, const int32_t* __restrict__ cb, const int32_t* __restrict__ cc,
@@ -130,6 +131,7 @@ k_m2m(int32_t cbeg, int32_t cend, const int32_t* __restrict__ cb, const int32_t*
   using T = MI<P>;
   constexpr int N = T::N;
   __shared__ double sD[4][3 * P];
+  __shared__ double sM[4][N];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t ci = cbeg + blockIdx.x * 4 + w;
   if (ci >= cend) return;
@@ -138,10 +140,24 @@ k_m2m(int32_t cbeg, int32_t cend, const int32_t* __restrict__ cb, const int32_t*
   const double4 pc = cr[ci];
   constexpr int KPL = (N + 31) / 32;
   double acc[KPL];
+  int ea[KPL], eb[KPL], ec[KPL];
 #pragma unroll
-  for (int k = 0; k < KPL; ++k) acc[k] = 0.0;
+  for (int k = 0; k < KPL; ++k) {
+    acc[k] = 0.0;
+    const int i = lane + 32 * k;
+    int n = 0;
+    if (i < N) {
+      while (n_coef(n + 1) <= i) ++n;
+      int r = i - n_coef(n), a = 0;
+      while (r >= n - a + 1) { r -= n - a + 1; ++a; }
+      ea[k] = a;
+      eb[k] = r;
+      ec[k] = n - a - r;
+    }
+  }
+  const int32_t c0 = cb[ci];
   for (int32_t ch = 0; ch < nch; ++ch) {
-    const int32_t child = cb[ci] + ch;
+    const int32_t child = c0 + ch;
     const double4 cc4 = cr[child];
     if (lane < 3) {
       const double d = lane == 0 ? cc4.x - pc.x : (lane == 1 ? cc4.y - pc.y : cc4.z - pc.z);
@@ -149,22 +165,19 @@ k_m2m(int32_t cbeg, int32_t cend, const int32_t* __restrict__ cb, const int32_t*
       L[0] = 1.0;
       for (int k = 1; k < P; ++k) L[k] = L[k - 1] * d / k;
     }
+    for (int i = lane; i < N; i += 32) sM[w][i] = M[(int64_t)child * N + i];
     __syncwarp();
-    const double* Mc = M + (int64_t)child * N;
 #pragma unroll
     for (int k = 0; k < KPL; ++k) {
       const int i = lane + 32 * k;
       if (i < N) {
-        int n = 0;
-        while (n_coef(n + 1) <= i) ++n;
-        int r = i - n_coef(n), a = 0;
-        while (r >= n - a + 1) { r -= n - a + 1; ++a; }
-        const int bb_ = r, cc_ = n - a - r;
+        const int a = ea[k], bb_ = eb[k], cc_ = ec[k];
         double s = 0.0;
         for (int ax = 0; ax <= a; ++ax)
-          for (int ay = 0; ay <= bb_; ++ay)
-            for (int az = 0; az <= cc_; ++az)
-              s += Mc[index_of(ax, ay, az)] * (sD[w][a - ax] * sD[w][P + bb_ - ay] * sD[w][2 * P + cc_ - az]);
+          for (int ay = 0; ay <= bb_; ++ay) {
+            const double xy = sD[w][a - ax] * sD[w][P + bb_ - ay];
+            for (int az = 0; az <= cc_; ++az) s += sM[w][index_of(ax, ay, az)] * (xy * sD[w][2 * P + cc_ - az]);
+          }
         acc[k] += s;
       }
     }
@@ -294,7 +307,8 @@ k_m2l(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* __re
 }
 
 // ------------------------------------------------------------------------------ L2L ----
-// Warp per cell of one level (>= 1): child_a += sum_d parent_{a+d} ((a+d)!/a!) d^d/d!.
+// Warp per cell of one level (>= 1): child_a += sum_d parent_{a+d} ((a+d)!/a!) d^d/d!,
+// parent local staged in shared memory.
 template <int P>
 __global__ void __launch_bounds__(128)
 k_l2l(int32_t cbeg, int32_t cend, const int32_t* __restrict__ par, const double4* __restrict__ cr,
@@ -302,7 +316,7 @@ k_l2l(int32_t cbeg, int32_t cend, const int32_t* __restrict__ par, const double4
   using T = MI<P>;
   constexpr int N = T::N;
   __shared__ double sD[4][3 * P];
-  __shared__ double sF[4][P];  // k! for k < P
+  __shared__ double sL[4][N];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t ci = cbeg + blockIdx.x * 4 + w;
   if (ci >= cend) return;
@@ -314,15 +328,12 @@ k_l2l(int32_t cbeg, int32_t cend, const int32_t* __restrict__ par, const double4
     Ld[0] = 1.0;
     for (int k = 1; k < P; ++k) Ld[k] = Ld[k - 1] * d / k;
   }
-  if (lane == 3) {
-    double f = 1.0;
-    for (int k = 0; k < P; ++k) {
-      if (k > 1) f *= k;
-      sF[w][k] = f;
-    }
-  }
+  for (int i = lane; i < N; i += 32) sL[w][i] = L[(int64_t)pi * N + i];
   __syncwarp();
-  const double* Lp = L + (int64_t)pi * N;
+  double fact[P];  // k! for k < P
+  fact[0] = 1.0;
+#pragma unroll
+  for (int k = 1; k < P; ++k) fact[k] = fact[k - 1] * k;
   double* Lc = L + (int64_t)ci * N;
   for (int i = lane; i < N; i += 32) {
     int n = 0;
@@ -331,13 +342,15 @@ k_l2l(int32_t cbeg, int32_t cend, const int32_t* __restrict__ par, const double4
     while (r >= n - a + 1) { r -= n - a + 1; ++a; }
     const int b = r, cz = n - a - r;
     double s = 0.0;
-    for (int dx = 0; dx + a + b + cz < P; ++dx)
-      for (int dy = 0; dx + dy + a + b + cz < P; ++dy)
-        for (int dz = 0; dx + dy + dz + a + b + cz < P; ++dz) {
-          // ((a+d)!/a!) = prod over axes of (a_k+d_k)!/a_k!
-          const double w_ = (sF[w][a + dx] / sF[w][a]) * (sF[w][b + dy] / sF[w][b]) * (sF[w][cz + dz] / sF[w][cz]);
-          s += Lp[index_of(a + dx, b + dy, cz + dz)] * w_ * (sD[w][dx] * sD[w][P + dy] * sD[w][2 * P + dz]);
+    for (int dx = 0; dx + n < P; ++dx)
+      for (int dy = 0; dx + dy + n < P; ++dy) {
+        const double wxy = (fact[a + dx] / fact[a]) * (fact[b + dy] / fact[b]);
+        const double pxy = sD[w][dx] * sD[w][P + dy];
+        for (int dz = 0; dx + dy + dz + n < P; ++dz) {
+          const double w_ = wxy * (fact[cz + dz] / fact[cz]);
+          s += sL[w][index_of(a + dx, b + dy, cz + dz)] * w_ * (pxy * sD[w][2 * P + dz]);
         }
+      }
     Lc[i] += s;
   }
 }

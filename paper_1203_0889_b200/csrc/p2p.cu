@@ -488,14 +488,12 @@ void build_p2p_worklist(fmm_ctx* c) {
   exclusive_scan_i32(c, nitems, item_off, nl + 1);
   exclusive_scan_i32(c, nred, red_off, nl + 1);
   exclusive_scan_i32(c, npart, part_off, nl + 1);
-  int32_t* h = nullptr;
-  CK(cudaMallocHost(&h, 4 * sizeof(int32_t)));
+  int32_t* h = reinterpret_cast<int32_t*>(c->hpin);
   CK(cudaMemcpyAsync(&h[0], item_off + nl, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&h[1], red_off + nl, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&h[2], part_off + nl, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const int64_t nitem = h[0], nr = h[1], np = h[2];
-  CK(cudaFreeHost(h));
   P2PItem* items_raw = reinterpret_cast<P2PItem*>(c->pairs_a.ensure(4 * (nitem + 1)));  // 32 B each
   P2PItem* items = reinterpret_cast<P2PItem*>(c->p2p_items.ensure(2 * (nitem + 1)));
   uint64_t* costs = c->keys_a.ensure(nitem + 1);

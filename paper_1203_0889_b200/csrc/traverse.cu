@@ -46,58 +46,73 @@ __device__ __forceinline__ void classify(const int2 pr, const double4* __restric
   nchild = split_t ? tc : sc;
 }
 
+struct Cnt {  // per-pair output counts; one exclusive scan gives all three offsets
+  long long m2l, p2p, push;
+};
+struct CntSum {
+  __host__ __device__ __forceinline__ Cnt operator()(const Cnt& a, const Cnt& b) const {
+    return Cnt{a.m2l + b.m2l, a.p2p + b.p2p, a.push + b.push};
+  }
+};
+
 __global__ void k_classify(const int2* __restrict__ fr, int64_t n, const double4* __restrict__ cr,
                            const int32_t* __restrict__ cc, double theta, int mutual,
-                           uint64_t* __restrict__ emit, int64_t* __restrict__ push) {
+                           uint8_t* __restrict__ kinds, Cnt* __restrict__ cnt) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i > n) return;
+  if (i == n) {  // trailing element: the exclusive scan's last entry is the total
+    cnt[i] = Cnt{0, 0, 0};
+    return;
+  }
   int kind, nchild;
   classify(fr[i], cr, cc, theta, mutual, kind, nchild);
-  emit[i] = kind == 0 ? 1ull : (kind == 1 ? (1ull << 32) : 0ull);
-  push[i] = nchild;
+  kinds[i] = static_cast<uint8_t>(kind);
+  cnt[i] = Cnt{kind == 0, kind == 1, nchild};
 }
 
-__global__ void k_expand(const int2* __restrict__ fr, int64_t n, const double4* __restrict__ cr,
-                         const int32_t* __restrict__ cc, const int32_t* __restrict__ cb, double theta,
-                         int mutual, const uint64_t* __restrict__ emit_off,
-                         const int64_t* __restrict__ push_off, int2* __restrict__ m2l, int64_t m2l_base,
+__global__ void k_expand(const int2* __restrict__ fr, int64_t n, const uint8_t* __restrict__ kinds,
+                         const int32_t* __restrict__ cc, const int32_t* __restrict__ cb,
+                         const Cnt* __restrict__ off, int2* __restrict__ m2l, int64_t m2l_base,
                          int2* __restrict__ p2p, int64_t p2p_base, int2* __restrict__ next) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int2 pr = fr[i];
-  int kind, nchild;
-  classify(pr, cr, cc, theta, mutual, kind, nchild);
-  const uint64_t eo = emit_off[i];
-  if (kind == 0) { m2l[m2l_base + (int64_t)(eo & 0xffffffffu)] = pr; return; }
-  if (kind == 1) { p2p[p2p_base + (int64_t)(eo >> 32)] = pr; return; }
-  int64_t o = push_off[i];
+  const int kind = kinds[i];
+  const Cnt o = off[i];
+  if (kind == 0) { m2l[m2l_base + o.m2l] = pr; return; }
+  if (kind == 1) { p2p[p2p_base + o.p2p] = pr; return; }
+  int64_t q = o.push;
   if (kind == 2) {
-    const int32_t b = cb[pr.x];
-    for (int k = 0; k < nchild; ++k) next[o + k] = make_int2(b + k, pr.y);
+    const int32_t b = cb[pr.x], m = cc[pr.x];
+    for (int k = 0; k < m; ++k) next[q + k] = make_int2(b + k, pr.y);
   } else if (kind == 3) {
-    const int32_t b = cb[pr.y];
-    for (int k = 0; k < nchild; ++k) next[o + k] = make_int2(pr.x, b + k);
+    const int32_t b = cb[pr.y], m = cc[pr.y];
+    for (int k = 0; k < m; ++k) next[q + k] = make_int2(pr.x, b + k);
   } else {
     const int32_t b = cb[pr.x], m = cc[pr.x];
     for (int a = 0; a < m; ++a)
-      for (int c = a; c < m; ++c) next[o++] = make_int2(b + a, b + c);
+      for (int c = a; c < m; ++c) next[q++] = make_int2(b + a, b + c);
   }
 }
 
-__global__ void k_pair_keys(const int2* __restrict__ pr, int64_t n, int sbits, uint64_t* __restrict__ keys) {
+__global__ void k_split_pairs(const int2* __restrict__ pr, int64_t n, uint32_t* __restrict__ t,
+                              int32_t* __restrict__ s) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) keys[i] = ((uint64_t)(uint32_t)pr[i].x << sbits) | (uint32_t)pr[i].y;
+  if (i < n) {
+    const int2 v = pr[i];
+    t[i] = static_cast<uint32_t>(v.x);
+    s[i] = v.y;
+  }
 }
 
-__global__ void k_csr_from_keys(const uint64_t* __restrict__ keys, int64_t n, int sbits, int64_t ncells,
-                                int64_t* __restrict__ off, int32_t* __restrict__ src) {
+// offsets from the target-sorted key array: targets tp+1..t start at i
+__global__ void k_csr_offsets(const uint32_t* __restrict__ t_sorted, int64_t n, int64_t ncells,
+                              int64_t* __restrict__ off) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i > n) return;
-  const uint64_t mask = (1ull << sbits) - 1;
-  const int64_t t = i < n ? (int64_t)(keys[i] >> sbits) : ncells;
-  const int64_t tp = i > 0 ? (int64_t)(keys[i - 1] >> sbits) : -1;
-  if (i < n) src[i] = (int32_t)(keys[i] & mask);
-  for (int64_t c = tp + 1; c <= t; ++c) off[c] = i;  // targets tp+1..t start at i
+  const int64_t t = i < n ? (int64_t)t_sorted[i] : ncells;
+  const int64_t tp = i > 0 ? (int64_t)t_sorted[i - 1] : -1;
+  for (int64_t c = tp + 1; c <= t; ++c) off[c] = i;
 }
 
 __global__ void k_p2p_body_pairs(const int64_t* __restrict__ off, const int32_t* __restrict__ src,
@@ -137,7 +152,8 @@ void grow_keep(fmm_ctx* c, DBuf<T>& buf, size_t used, size_t need) {
   buf.cap = want;
 }
 
-// Groups (target, source) pairs into CSR by target with ascending sources.
+// Groups (target, source) pairs into CSR by target: a stable radix sort on the target index
+// only (ceil(log2 ncells) bits), so sources keep the traversal's deterministic emission order.
 void to_csr(fmm_ctx* c, const int2* d_pairs, int64_t n, DBuf<int64_t>& off, DBuf<int32_t>& src) {
   cudaStream_t s = c->stream;
   const int64_t nc = c->ncells;
@@ -147,14 +163,15 @@ void to_csr(fmm_ctx* c, const int2* d_pairs, int64_t n, DBuf<int64_t>& off, DBuf
     CK(cudaMemsetAsync(off.p, 0, sizeof(int64_t) * (nc + 1), s));
     return;
   }
-  const int sbits = bits_for(static_cast<uint64_t>(nc));
-  uint64_t* ka = c->keys_a.ensure(n);
-  uint64_t* kb = c->keys_b.ensure(n);
-  k_pair_keys<<<ceil_div(n, 256), 256, 0, s>>>(d_pairs, n, sbits, ka);
+  const int tbits = bits_for(static_cast<uint64_t>(nc));
+  uint32_t* ta = reinterpret_cast<uint32_t*>(c->keys_a.ensure((n + 1) / 2 + 1));
+  uint32_t* tb = reinterpret_cast<uint32_t*>(c->keys_b.ensure((n + 1) / 2 + 1));
+  int32_t* sa = c->i32_c.ensure(n);
+  k_split_pairs<<<ceil_div(n, 256), 256, 0, s>>>(d_pairs, n, ta, sa);
   size_t sb = 0;
-  CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, ka, kb, (int)n, 0, 2 * sbits, s));
-  CK(cub::DeviceRadixSort::SortKeys(temp_storage(c, sb), sb, ka, kb, (int)n, 0, 2 * sbits, s));
-  k_csr_from_keys<<<ceil_div(n + 1, 256), 256, 0, s>>>(kb, n, sbits, nc, off.p, src.p);
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, sb, ta, tb, sa, src.p, (int)n, 0, tbits, s));
+  CK(cub::DeviceRadixSort::SortPairs(temp_storage(c, sb), sb, ta, tb, sa, src.p, (int)n, 0, tbits, s));
+  k_csr_offsets<<<ceil_div(n + 1, 256), 256, 0, s>>>(tb, n, nc, off.p);
   CK_LAUNCH("to_csr");
   c->kernel_launches += 4;
 }
@@ -181,8 +198,8 @@ void lists_from_pairs(fmm_ctx* c, const int2* d_m2l, int64_t n_m2l, const int2* 
   cub::CountingInputIterator<int32_t> it(0);
   CK(cub::DeviceSelect::Flagged(nullptr, sb, it, flag, targets, nsel, (int)c->ncells, s));
   CK(cub::DeviceSelect::Flagged(temp_storage(c, sb), sb, it, flag, targets, nsel, (int)c->ncells, s));
-  int64_t h[2];
-  CK(cudaMemcpyAsync(h, c->d_counters.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  int64_t* h = c->hpin;
+  CK(cudaMemcpyAsync(h, c->d_counters.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   c->p2p_body_pairs = h[0];
   c->n_m2l_targets = h[1];
@@ -199,58 +216,45 @@ void traverse(fmm_ctx* c) {
   const int mutual = c->cfg.mutual ? 1 : 0;
 
   int64_t nf = 1, nm = 0, np = 0;
-  int2 root = make_int2(0, 0);
-  c->pairs_a.ensure(1024);
-  c->pairs_b.ensure(1024);
-  c->pairs_c.ensure(1024);
+  const int2 root = make_int2(0, 0);
+  DBuf<int2>* fa = &c->pairs_a;
+  DBuf<int2>* fb = &c->pairs_d;
   DBuf<int2>* m2l = &c->pairs_b;
   DBuf<int2>* p2p = &c->pairs_c;
-  DBuf<int2> front_b;  // second frontier buffer
-  DBuf<int2>* fa = &c->pairs_a;
-  DBuf<int2>* fb = &front_b;
+  fa->ensure(1024);
   fb->ensure(1024);
+  m2l->ensure(1024);
+  p2p->ensure(1024);
   CK(cudaMemcpyAsync(fa->p, &root, sizeof(int2), cudaMemcpyHostToDevice, s));
-  int64_t* hcnt = nullptr;
-  CK(cudaMallocHost(&hcnt, 4 * sizeof(int64_t)));
+  Cnt* hcnt = reinterpret_cast<Cnt*>(c->hpin);
+  int launches = 0;
   while (nf > 0) {
-    uint64_t* emit = c->keys_a.ensure(nf + 1);
-    uint64_t* emit_off = c->keys_b.ensure(nf + 1);
-    int64_t* push = c->scan_a.ensure(2 * (nf + 1));
-    int64_t* push_off = push + (nf + 1);
-    k_classify<<<ceil_div(nf, 256), 256, 0, s>>>(fa->p, nf, c->c_cr.p, c->c_child_count.p, theta, mutual,
-                                                 emit, push);
+    Cnt* cnt = reinterpret_cast<Cnt*>(c->scan_a.ensure(3 * (nf + 1) * 2));
+    Cnt* off = cnt + (nf + 1);
+    uint8_t* kinds = reinterpret_cast<uint8_t*>(c->keys_a.ensure(nf / 8 + 2));
+    k_classify<<<ceil_div(nf + 1, 256), 256, 0, s>>>(fa->p, nf, c->c_cr.p, c->c_child_count.p, theta, mutual,
+                                                     kinds, cnt);
     CK_LAUNCH("k_classify");
-    CK(cudaMemsetAsync(emit + nf, 0, sizeof(uint64_t), s));
-    CK(cudaMemsetAsync(push + nf, 0, sizeof(int64_t), s));
-    size_t sb1 = 0, sb2 = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, sb1, emit, emit_off, (int)(nf + 1), s));
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, sb2, push, push_off, (int)(nf + 1), s));
-    void* tmp = temp_storage(c, sb1 > sb2 ? sb1 : sb2);
-    CK(cub::DeviceScan::ExclusiveSum(tmp, sb1, emit, emit_off, (int)(nf + 1), s));
-    CK(cub::DeviceScan::ExclusiveSum(tmp, sb2, push, push_off, (int)(nf + 1), s));
-    uint64_t he = 0;
-    CK(cudaMemcpyAsync(&hcnt[0], emit_off + nf, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&hcnt[1], push_off + nf, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    size_t sb = 0;
+    CK(cub::DeviceScan::ExclusiveScan(nullptr, sb, cnt, off, CntSum(), Cnt{0, 0, 0}, (int)(nf + 1), s));
+    CK(cub::DeviceScan::ExclusiveScan(temp_storage(c, sb), sb, cnt, off, CntSum(), Cnt{0, 0, 0}, (int)(nf + 1), s));
+    CK(cudaMemcpyAsync(hcnt, off + nf, sizeof(Cnt), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    he = static_cast<uint64_t>(hcnt[0]);
-    const int64_t add_m = static_cast<int64_t>(he & 0xffffffffu), add_p = static_cast<int64_t>(he >> 32);
-    const int64_t nnext = hcnt[1];
+    const int64_t add_m = hcnt->m2l, add_p = hcnt->p2p, nnext = hcnt->push;
     grow_keep(c, *m2l, nm, nm + add_m);
     grow_keep(c, *p2p, np, np + add_p);
     fb->ensure(nnext > 0 ? nnext : 1);
-    k_expand<<<ceil_div(nf, 256), 256, 0, s>>>(fa->p, nf, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p,
-                                               theta, mutual, emit_off, push_off, m2l->p, nm, p2p->p, np, fb->p);
+    k_expand<<<ceil_div(nf, 256), 256, 0, s>>>(fa->p, nf, kinds, c->c_child_count.p, c->c_child_begin.p, off,
+                                               m2l->p, nm, p2p->p, np, fb->p);
     CK_LAUNCH("k_expand");
-    c->kernel_launches += 4;
+    launches += 3;
     nm += add_m;
     np += add_p;
     nf = nnext;
     std::swap(fa, fb);
   }
-  CK(cudaStreamSynchronize(s));
-  CK(cudaFreeHost(hcnt));
+  c->kernel_launches += launches;
   lists_from_pairs(c, m2l->p, nm, p2p->p, np);
-  CK(cudaStreamSynchronize(s));  // front_b is freed on return
 }
 
 }  // namespace fmmb

@@ -56,15 +56,33 @@ __global__ void k_bounds_partial(const double4* __restrict__ xyzq, int64_t n, do
   }
 }
 
-// Finishes the reduction and evaluates the Domain formula of tree.cpp:19-21 exactly.
+// Finishes the reduction (one block) and evaluates the Domain formula of tree.cpp:19-21.
 __global__ void k_bounds_final(const double* __restrict__ part, int nparts, double* __restrict__ dom) {
-  if (threadIdx.x != 0) return;
+  __shared__ double s[6][256];
   double lo[3] = {part[0], part[1], part[2]}, hi[3] = {part[3], part[4], part[5]};
-  for (int k = 1; k < nparts; ++k)
+  for (int k = threadIdx.x; k < nparts; k += blockDim.x)
     for (int d = 0; d < 3; ++d) {
       lo[d] = dmin_ref(lo[d], part[6 * k + d]);
       hi[d] = dmax_ref(hi[d], part[6 * k + 3 + d]);
     }
+  for (int d = 0; d < 3; ++d) {
+    s[d][threadIdx.x] = lo[d];
+    s[3 + d][threadIdx.x] = hi[d];
+  }
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int d = 0; d < 3; ++d) {
+        s[d][threadIdx.x] = dmin_ref(s[d][threadIdx.x], s[d][threadIdx.x + o]);
+        s[3 + d][threadIdx.x] = dmax_ref(s[3 + d][threadIdx.x], s[3 + d][threadIdx.x + o]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = s[d][0];
+    hi[d] = s[3 + d][0];
+  }
   for (int d = 0; d < 3; ++d) dom[d] = __dmul_rn(0.5, __dadd_rn(lo[d], hi[d]));
   double ext = __dadd_rn(hi[0], -lo[0]);
   ext = dmax_ref(ext, __dadd_rn(hi[1], -lo[1]));  // (hi - lo).maxCoeff()
@@ -110,29 +128,31 @@ __device__ __forceinline__ int32_t lower_digit(const uint64_t* __restrict__ k, i
   return lo;
 }
 
-// Children count of every cell of one level (0 when the cell is a leaf).
+// Children of every cell of one level (warp per cell): lanes 1..7 binary-search the seven
+// octant boundaries in parallel; bnd[9*k + o] = first body of octant o (bnd[9*k+8] = end).
 __global__ void k_count_children(int32_t cbeg, int32_t cend, int level, int n_crit,
                                  const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
-                                 const uint64_t* __restrict__ skeys, int32_t* __restrict__ nchild) {
-  const int32_t ci = cbeg + blockIdx.x * blockDim.x + threadIdx.x;
+                                 const uint64_t* __restrict__ skeys, int32_t* __restrict__ nchild,
+                                 int32_t* __restrict__ bnd) {
+  const int32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int32_t ci = cbeg + k;
   if (ci >= cend) return;
   const int32_t b = bb[ci], e = be[ci];
-  int cnt = 0;
-  if (e - b > n_crit && level < kLevels) {  // tree.cpp:78
-    int32_t start = b;
-    for (int o = 0; o < 8; ++o) {
-      const int32_t stop = (o == 7) ? e : lower_digit(skeys, start, e, level + 1, o + 1);
-      cnt += stop > start;
-      start = stop;
-    }
-  }
-  nchild[ci - cbeg] = cnt;
+  const bool split = e - b > n_crit && level < kLevels;  // tree.cpp:78
+  int32_t pos = e;
+  if (split && lane >= 1 && lane <= 7) pos = lower_digit(skeys, b, e, level + 1, lane);
+  if (lane == 0) pos = b;
+  if (split && lane <= 8) bnd[9 * k + lane] = pos;
+  const int32_t nxt = __shfl_down_sync(0xffffffffu, pos, 1);
+  const unsigned nonempty = __ballot_sync(0xffffffffu, split && lane < 8 && nxt > pos);
+  if (lane == 0) nchild[k] = __popc(nonempty);
 }
 
-// Materialises the children of one level; offsets = exclusive scan of nchild.
+// Materialises the children of one level; offs = exclusive scan of nchild.
 __global__ void k_write_children(int32_t cbeg, int32_t cend, int level, int32_t next_begin,
                                  const int32_t* __restrict__ nchild, const int32_t* __restrict__ offs,
-                                 const uint64_t* __restrict__ skeys, int32_t* __restrict__ c_level,
+                                 const int32_t* __restrict__ bnd, int32_t* __restrict__ c_level,
                                  uint64_t* __restrict__ c_key, double4* __restrict__ c_cr,
                                  int32_t* __restrict__ bb, int32_t* __restrict__ be,
                                  int32_t* __restrict__ cb, int32_t* __restrict__ cc,
@@ -141,16 +161,14 @@ __global__ void k_write_children(int32_t cbeg, int32_t cend, int level, int32_t 
   if (ci >= cend) return;
   const int k = ci - cbeg;
   if (nchild[k] == 0) return;
-  const int32_t b = bb[ci], e = be[ci];
   const double4 pc = c_cr[ci];
   const uint64_t pkey = c_key[ci];
   const double cr = __dmul_rn(0.5, pc.w);
   int32_t out = next_begin + offs[k];
   cb[ci] = out;
   cc[ci] = nchild[k];
-  int32_t start = b;
   for (int o = 0; o < 8; ++o) {
-    const int32_t stop = (o == 7) ? e : lower_digit(skeys, start, e, level + 1, o + 1);
+    const int32_t start = bnd[9 * k + o], stop = bnd[9 * k + o + 1];
     if (stop > start) {
       c_level[out] = level + 1;
       c_key[out] = (pkey << 3) | (uint64_t)o;
@@ -163,7 +181,6 @@ __global__ void k_write_children(int32_t cbeg, int32_t cend, int level, int32_t 
       par[out] = ci;
       ++out;
     }
-    start = stop;
   }
 }
 
@@ -179,7 +196,8 @@ __global__ void k_init_root(const double* __restrict__ dom, int32_t n, int32_t* 
   par[0] = -1;
 }
 
-// Leaf-of-body map (warp per leaf) and the (leaf begin, input index) composite key.
+// Leaf-of-body map (warp per leaf) and, optionally, the (leaf begin, input index) composite
+// key of the global fallback sort.
 __global__ void k_leaf_map(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __restrict__ bb,
                            const int32_t* __restrict__ be, const int32_t* __restrict__ sidx,
                            int32_t* __restrict__ leaf_of_body, uint64_t* __restrict__ ckey) {
@@ -191,6 +209,35 @@ __global__ void k_leaf_map(const int32_t* __restrict__ leaves, int64_t nleaves, 
   for (int32_t i = b + lane; i < e; i += 32) {
     leaf_of_body[i] = leaf;
     if (ckey) ckey[i] = ((uint64_t)(uint32_t)b << 32) | (uint32_t)sidx[i];
+  }
+}
+
+// Within-leaf input order (tree.cpp:82-93 keeps input order inside every cell): rank sort of
+// the leaf's input indices (distinct), warp per leaf, leaves up to kRankMax bodies. Also writes
+// leaf_of_body. Larger leaves (level-21 overflow only) raise *big for the global fallback.
+constexpr int kRankMax = 1024;
+__global__ void __launch_bounds__(128)
+k_leaf_sort(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __restrict__ bb,
+            const int32_t* __restrict__ be, const int32_t* __restrict__ sidx, int32_t* __restrict__ perm,
+            int32_t* __restrict__ leaf_of_body, int32_t* __restrict__ big) {
+  __shared__ int32_t sv[4][kRankMax];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t wid = blockIdx.x * 4ll + w;
+  if (wid >= nleaves) return;
+  const int32_t leaf = leaves[wid];
+  const int32_t b = bb[leaf], e = be[leaf], n = e - b;
+  for (int32_t i = lane; i < n; i += 32) leaf_of_body[b + i] = leaf;
+  if (n > kRankMax) {
+    if (lane == 0) atomicExch(big, 1);
+    return;
+  }
+  for (int32_t i = lane; i < n; i += 32) sv[w][i] = sidx[b + i];
+  __syncwarp();
+  for (int32_t i = lane; i < n; i += 32) {
+    const int32_t v = sv[w][i];
+    int32_t r = 0;
+    for (int32_t j = 0; j < n; ++j) r += sv[w][j] < v;
+    perm[b + r] = v;
   }
 }
 
@@ -218,7 +265,7 @@ __global__ void k_flag_leaves(const int32_t* __restrict__ cc, int64_t ncells, in
 
 template <class T>
 void grow_preserve(fmm_ctx* c, DBuf<T>& buf, size_t used, size_t need) {
-  if (need <= buf.cap) return;
+  if (need <= buf.cap) return;  // steady state: no allocation
   T* old = buf.p;
   size_t want = need * 2 + 1024;
   T* fresh = nullptr;
@@ -249,16 +296,16 @@ void build_tree(fmm_ctx* c) {
   if (c->cfg.n_crit < 1) fail(FMM_ERR_NCRIT, "n_crit must be >= 1");
   if (n >= (int64_t(1) << 31)) fail(FMM_ERR_UNSUPPORTED, "more than 2^31-1 bodies");
   cudaStream_t s = c->stream;
+  int64_t* hp = c->hpin;
 
   // 1. compute_bounds
   const int nparts = 592;  // 4 x 148 SMs
   double* part = c->small.ensure(nparts * 6 + 8);
   double* dom = part + nparts * 6;
   k_bounds_partial<<<nparts, 256, 0, s>>>(c->xyzq_in.p, n, part);
-  k_bounds_final<<<1, 32, 0, s>>>(part, nparts, dom);
+  k_bounds_final<<<1, 256, 0, s>>>(part, nparts, dom);
   CK_LAUNCH("k_bounds");
-  double hdom[4];
-  CK(cudaMemcpyAsync(hdom, dom, sizeof(hdom), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hp + 32, dom, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
 
   // 2. keys by octant descent, 3. stable radix sort (key, index)
   uint64_t* keys = c->keys_a.ensure(n);
@@ -272,13 +319,7 @@ void build_tree(fmm_ctx* c) {
   void* tmp = temp_storage(c, tbytes);
   CK(cub::DeviceRadixSort::SortPairs(tmp, tbytes, keys, skeys, idx, sidx, (int)n, 0, 3 * kLevels, s));
 
-  c->center[0] = hdom[0];
-  c->center[1] = hdom[1];
-  c->center[2] = hdom[2];
-  c->half_side = hdom[3];
-
   // 4. level-by-level cell materialisation
-  size_t cap = 1024;
   auto ensure_cells = [&](size_t used, size_t need) {
     grow_preserve(c, c->c_level, used, need);
     grow_preserve(c, c->c_key, used, need);
@@ -289,47 +330,52 @@ void build_tree(fmm_ctx* c) {
     grow_preserve(c, c->c_child_count, used, need);
     grow_preserve(c, c->c_parent, used, need);
   };
-  ensure_cells(0, cap);
+  ensure_cells(0, 1024);
   k_init_root<<<1, 1, 0, s>>>(dom, (int32_t)n, c->c_level.p, c->c_key.p, c->c_cr.p, c->c_body_begin.p,
                               c->c_body_end.p, c->c_child_begin.p, c->c_child_count.p, c->c_parent.p);
   CK_LAUNCH("k_init_root");
   int64_t ncells = 1;
   int level = 0;
   for (int l = 0; l < FMM_MAX_LEVEL + 2; ++l) c->level_start[l] = 0;
-  c->level_start[0] = 0;
   c->level_start[1] = 1;
-  int32_t* hbuf = nullptr;
-  CK(cudaMallocHost(&hbuf, 2 * sizeof(int32_t)));
+  int launches = 4;
   while (true) {
     const int32_t cb = c->level_start[level], ce = c->level_start[level + 1];
     const int32_t m = ce - cb;
     int32_t* nchild = c->i32_a.ensure(m + 1);
     int32_t* offs = c->i32_b.ensure(m + 1);
-    k_count_children<<<ceil_div(m, 128), 128, 0, s>>>(cb, ce, level, c->cfg.n_crit, c->c_body_begin.p,
-                                                     c->c_body_end.p, skeys, nchild);
+    int32_t* bnd = c->bnd.ensure(9 * (size_t)m + 9);
+    k_count_children<<<ceil_div((int64_t)m * 32, 128), 128, 0, s>>>(cb, ce, level, c->cfg.n_crit, c->c_body_begin.p,
+                                                                    c->c_body_end.p, skeys, nchild, bnd);
     CK_LAUNCH("k_count_children");
     size_t sb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, nchild, offs, m + 1, s));
     CK(cudaMemsetAsync(nchild + m, 0, sizeof(int32_t), s));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, nchild, offs, m + 1, s));
     CK(cub::DeviceScan::ExclusiveSum(temp_storage(c, sb), sb, nchild, offs, m + 1, s));
-    CK(cudaMemcpyAsync(hbuf, offs + m, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hp, offs + m, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    const int32_t nnew = hbuf[0];
+    const int32_t nnew = static_cast<int32_t>(*reinterpret_cast<int32_t*>(hp));
+    launches += 2;
     if (nnew == 0) break;
     ensure_cells(ncells, ncells + nnew);
-    k_write_children<<<ceil_div(m, 128), 128, 0, s>>>(cb, ce, level, ce, nchild, offs, skeys, c->c_level.p,
+    k_write_children<<<ceil_div(m, 128), 128, 0, s>>>(cb, ce, level, ce, nchild, offs, bnd, c->c_level.p,
                                                      c->c_key.p, c->c_cr.p, c->c_body_begin.p, c->c_body_end.p,
                                                      c->c_child_begin.p, c->c_child_count.p, c->c_parent.p);
     CK_LAUNCH("k_write_children");
+    ++launches;
     ncells += nnew;
     ++level;
     c->level_start[level + 1] = static_cast<int32_t>(ncells);
     if (ncells >= (int64_t(1) << 31) - 16) fail(FMM_ERR_UNSUPPORTED, "too many cells");
   }
-  CK(cudaFreeHost(hbuf));
   for (int l = level + 2; l < FMM_MAX_LEVEL + 2; ++l) c->level_start[l] = static_cast<int32_t>(ncells);
   c->ncells = ncells;
   c->depth = level;
+  const double* hdom = reinterpret_cast<const double*>(hp + 32);
+  c->center[0] = hdom[0];
+  c->center[1] = hdom[1];
+  c->center[2] = hdom[2];
+  c->half_side = hdom[3];
 
   // 5. leaves (ascending cell index)
   int32_t* flag = c->i32_a.ensure(ncells);
@@ -342,30 +388,41 @@ void build_tree(fmm_ctx* c) {
     CK(cub::DeviceSelect::Flagged(nullptr, sb, it, flag, leaves, nsel, (int)ncells, s));
     CK(cub::DeviceSelect::Flagged(temp_storage(c, sb), sb, it, flag, leaves, nsel, (int)ncells, s));
   }
-  int64_t hn = 0;
-  CK(cudaMemcpyAsync(&hn, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  int32_t* big = reinterpret_cast<int32_t*>(nsel + 1);
+  CK(cudaMemsetAsync(big, 0, sizeof(int32_t), s));
+  CK(cudaMemcpyAsync(hp, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  c->nleaves = hn;
+  c->nleaves = hp[0];
 
-  // 6. within-leaf input order: sort by (leaf body_begin << 32 | input index)
+  // 6. within-leaf input order: rank sort per leaf; global (leaf, index) sort only when a
+  //    level-21 leaf exceeds kRankMax bodies
   int32_t* leaf_of_body = c->leaf_of_body.ensure(n);
-  uint64_t* ckey = c->keys_a.ensure(n);  // keys no longer needed
-  k_leaf_map<<<ceil_div(c->nleaves * 32, 256), 256, 0, s>>>(leaves, c->nleaves, c->c_body_begin.p,
-                                                              c->c_body_end.p, sidx, leaf_of_body, ckey);
-  CK_LAUNCH("k_leaf_map");
-  uint64_t* ckey2 = c->keys_b.ensure(n);  // sorted keys no longer needed after leaf map
-  {
+  int32_t* perm = c->perm.ensure(n);
+  k_leaf_sort<<<ceil_div(c->nleaves, 4), 128, 0, s>>>(leaves, c->nleaves, c->c_body_begin.p, c->c_body_end.p, sidx,
+                                                      perm, leaf_of_body, big);
+  CK_LAUNCH("k_leaf_sort");
+  CK(cudaMemcpyAsync(hp + 1, big, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  launches += 3;
+  if (*reinterpret_cast<int32_t*>(hp + 1)) {
+    uint64_t* ckey = c->keys_a.ensure(n);
+    k_leaf_map<<<ceil_div(c->nleaves * 32, 256), 256, 0, s>>>(leaves, c->nleaves, c->c_body_begin.p,
+                                                                c->c_body_end.p, sidx, leaf_of_body, ckey);
+    uint64_t* ckey2 = c->keys_b.ensure(n);  // sorted keys are no longer needed
     const int end_bit = 32 + bits_for(static_cast<uint64_t>(n));
     size_t sb = 0;
     CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, ckey, ckey2, (int)n, 0, end_bit, s));
     CK(cub::DeviceRadixSort::SortKeys(temp_storage(c, sb), sb, ckey, ckey2, (int)n, 0, end_bit, s));
+    k_perm_from_ckey<<<ceil_div(n, 256), 256, 0, s>>>(ckey2, n, perm);
+    CK_LAUNCH("k_perm_from_ckey");
+    launches += 3;
   }
-  int32_t* perm = c->perm.ensure(n);
-  k_perm_from_ckey<<<ceil_div(n, 256), 256, 0, s>>>(ckey2, n, perm);
-  CK_LAUNCH("k_perm_from_ckey");
-  c->kernel_launches += 8 + 2 * level;
+  c->kernel_launches += launches;
   c->have_tree = true;
-  gather_bodies(c);
+  k_gather<<<ceil_div(n, 256), 256, 0, s>>>(c->xyzq_in.p, perm, leaf_of_body, c->c_cr.p, n, c->bodies.ensure(n),
+                                            c->bodyf.ensure(n));
+  CK_LAUNCH("k_gather");
+  c->kernel_launches += 1;
 }
 
 void gather_bodies(fmm_ctx* c) {

@@ -1,0 +1,27 @@
+"""Runs `--warmup` + `--steps` FMM evaluations of a BASELINE config (for ncu launch lists /
+full captures of one step). Prints per-stage device times of the last step."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1203_0889_b200 as fb  # noqa: E402
+from bench import CONFIGS  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C2")
+ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--warmup", type=int, default=2)
+ap.add_argument("--precision", default="fp32")
+a = ap.parse_args()
+gen, n, p, n_crit, theta = CONFIGS[a.config]
+b = fb.generate_bodies(gen, n, 1)
+ctx = fb.Context(order=p, n_crit=n_crit, theta=theta, precision=a.precision)
+ctx.set_bodies(b)
+for _ in range(a.warmup + a.steps):
+    ctx.evaluate()
+t = ctx.stage_times()
+print({k: round(getattr(t, k), 3) for k, _ in t._fields_})
+info = ctx.tree_info()
+print("cells", info.ncells, "leaves", info.nleaves, "depth", info.depth, "m2l", info.n_m2l,
+      "p2p", info.n_p2p, "pairs", info.p2p_body_pairs)
