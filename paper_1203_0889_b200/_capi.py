@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libfmm_b200.so")
+LIB_PATH = os.environ.get("FMM_B200_LIB") or os.path.join(HERE, "lib", "libfmm_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "fmm_b200.h")
 
 FMM_MAX_ORDER = 10

@@ -75,6 +75,7 @@ struct fmm_ctx {
   fmmb::DBuf<int64_t> d_counters;
   fmmb::DBuf<double> small;
   fmmb::DBuf<int2> pairs_d;         // second traversal frontier
+  fmmb::DBuf<uint64_t> m2l_keys, p2p_keys;  // emitted (target << sbits | source)
   fmmb::DBuf<int32_t> bnd;           // child boundaries of one level (9 per cell)
   int64_t* hpin = nullptr;           // pinned host scratch (64 x int64)
 
@@ -95,6 +96,7 @@ void build_tree(fmm_ctx* c);
 void gather_bodies(fmm_ctx* c);  // bodies/bodyf/leaf_of_body from perm + tree
 // traverse.cu
 void traverse(fmm_ctx* c);
+void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p);  // lists from c->m2l_keys/p2p_keys
 void lists_from_pairs(fmm_ctx* c, const int2* d_m2l, int64_t n_m2l, const int2* d_p2p,
                       int64_t n_p2p);
 // p2p.cu

@@ -89,36 +89,43 @@ __device__ __forceinline__ void tile_setup(int tid, int32_t le, int32_t cursor, 
 }
 
 // ------------------------------------------------------------------------ FP32 kernel ----
-__global__ void __launch_bounds__(kThreads, 6)
+// Thread (g, t) owns the target pair (2t, 2t+1) of the item, packed in f32x2 lanes, and every
+// G-th source of each tile (G = 128 / ceil(n_t/2) lane groups). Sources are stored once as
+// float4 {-x, -y, -z, q} in the target leaf's frame; the packed ops take the source component
+// as a broadcast scalar operand, so one LDS.128 feeds two pair evaluations.
+#ifndef FMM_P2P_MIN_BLOCKS
+#define FMM_P2P_MIN_BLOCKS 6
+#endif
+template <bool kAcc>
+__global__ void __launch_bounds__(kThreads, FMM_P2P_MIN_BLOCKS)
 k_p2p_fp32(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_list,
            const int32_t* __restrict__ bb, const int32_t* __restrict__ be, const double4* __restrict__ cr,
            const float4* __restrict__ bodyf, double* __restrict__ phi_out, double* __restrict__ acc_out,
-           double* __restrict__ partial, int with_acc) {
-  __shared__ float4 sA[kTileBodies / 2 + 1];
-  __shared__ float4 sB[kTileBodies / 2 + 1];
+           double* __restrict__ partial) {
+  __shared__ __align__(16) float4 sS[kTileBodies];
   __shared__ int32_t seg_off[kTileSegs + 1];
   __shared__ int32_t seg_src[kTileSegs];
   __shared__ int32_t seg_boff[kTileSegs];
   __shared__ int32_t nxt[3];
-  __shared__ double red[4][kThreads];
 
   const P2PItem it = items[blockIdx.x];
   const int tid = threadIdx.x;
   const int nt = it.te - it.tb;
-  const int G = kThreads / nt;
-  const int g = tid / nt, t = tid - g * nt;
+  const int slots = (nt + 1) >> 1;
+  const int G = kThreads / slots;
+  const int g = tid / slots, t = tid - g * slots;
   const bool active = g < G;
   const double4 ct = cr[it.leaf];
 
-  float xt = 0.f, yt = 0.f, zt = 0.f;
+  float2 X = make_float2(0.f, 0.f), Y = X, Z = X;
   if (active) {
-    const float4 b = bodyf[it.tb + t];
-    xt = b.x;
-    yt = b.y;
-    zt = b.z;
+    const float4 b0 = bodyf[it.tb + 2 * t];
+    const float4 b1 = (2 * t + 1 < nt) ? bodyf[it.tb + 2 * t + 1] : b0;
+    X = make_float2(b0.x, b1.x);
+    Y = make_float2(b0.y, b1.y);
+    Z = make_float2(b0.z, b1.z);
   }
-  const float2 X = make_float2(xt, xt), Y = make_float2(yt, yt), Z = make_float2(zt, zt);
-  double phi_d = 0.0, ax_d = 0.0, ay_d = 0.0, az_d = 0.0;
+  double ph0 = 0.0, ph1 = 0.0, ax0 = 0.0, ax1 = 0.0, ay0 = 0.0, ay1 = 0.0, az0 = 0.0, az1 = 0.0;
 
   int32_t cursor = it.lb, cur_off = 0;
   while (cursor < it.le) {
@@ -126,12 +133,8 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_li
     __syncthreads();
     const int32_t nseg = nxt[2];
     const int32_t nb = seg_off[nseg];
-    // --- fill: warp w copies entries w, w+4, ...; sources shifted into the target leaf's
-    // frame (shift = c_s - c_t in FP64, rounded once), negated, pair-interleaved
-    {
+    {  // fill: warp w copies entries w, w+4, ...; shift = c_s - c_t in FP64, rounded once
       const int w = tid >> 5, lane = tid & 31;
-      float* A = reinterpret_cast<float*>(sA);
-      float* B = reinterpret_cast<float*>(sB);
       for (int k = w; k < nseg; k += kThreads / 32) {
         const int32_t src = seg_src[k];
         const int32_t base = bb[src] + seg_boff[k], n = seg_off[k + 1] - seg_off[k], o0 = seg_off[k];
@@ -140,73 +143,72 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_li
                     sz = static_cast<float>(cs.z - ct.z);
         for (int j = lane; j < n; j += 32) {
           const float4 b = bodyf[base + j];
-          const int p = o0 + j, pi = p >> 1, h = p & 1;
-          A[4 * pi + h] = -(b.x + sx);
-          A[4 * pi + 2 + h] = -(b.y + sy);
-          B[4 * pi + h] = -(b.z + sz);
-          B[4 * pi + 2 + h] = b.w;
+          sS[o0 + j] = make_float4(-(b.x + sx), -(b.y + sy), -(b.z + sz), b.w);
         }
-      }
-      if (tid == 0 && (nb & 1)) {  // pad to a whole pair with a zero charge
-        const int pi = nb >> 1;
-        A[4 * pi + 1] = 0.f;
-        A[4 * pi + 3] = 0.f;
-        B[4 * pi + 1] = 0.f;
-        B[4 * pi + 3] = 0.f;
       }
     }
     __syncthreads();
-    // --- compute
     if (active) {
-      const int npairs = (nb + 1) >> 1;
       float2 ph = make_float2(0.f, 0.f), ax = ph, ay = ph, az = ph;
 #pragma unroll 4
-      for (int p = g; p < npairs; p += G) {
-        const float4 a = sA[p];
-        const float4 b = sB[p];
-        const float2 dx = __fadd2_rn(X, make_float2(a.x, a.y));
-        const float2 dy = __fadd2_rn(Y, make_float2(a.z, a.w));
-        const float2 dz = __fadd2_rn(Z, make_float2(b.x, b.y));
-        const float2 q = make_float2(b.z, b.w);
+      for (int j = g; j < nb; j += G) {
+        const float4 sv = sS[j];
+        const float2 dx = __fadd2_rn(X, make_float2(sv.x, sv.x));
+        const float2 dy = __fadd2_rn(Y, make_float2(sv.y, sv.y));
+        const float2 dz = __fadd2_rn(Z, make_float2(sv.z, sv.z));
         float2 r2 = __fmul2_rn(dx, dx);
         r2 = __ffma2_rn(dy, dy, r2);
         r2 = __ffma2_rn(dz, dz, r2);
-        float2 ri;
+        float2 ri;  // r^2 == 0 (self / coincident) contributes nothing (kernels.cpp:185-186)
         ri.x = r2.x > 0.f ? rsqrtf(r2.x) : 0.f;
         ri.y = r2.y > 0.f ? rsqrtf(r2.y) : 0.f;
-        const float2 qr = __fmul2_rn(q, ri);
+        const float2 qr = __fmul2_rn(make_float2(sv.w, sv.w), ri);
         ph = __fadd2_rn(ph, qr);
-        if (with_acc) {
-          const float2 ri2 = __fmul2_rn(ri, ri);
-          const float2 qr3 = __fmul2_rn(qr, ri2);
+        if constexpr (kAcc) {
+          const float2 qr3 = __fmul2_rn(qr, __fmul2_rn(ri, ri));
           ax = __ffma2_rn(dx, qr3, ax);
           ay = __ffma2_rn(dy, qr3, ay);
           az = __ffma2_rn(dz, qr3, az);
         }
       }
-      phi_d += static_cast<double>(ph.x) + static_cast<double>(ph.y);
-      ax_d += static_cast<double>(ax.x) + static_cast<double>(ax.y);
-      ay_d += static_cast<double>(ay.x) + static_cast<double>(ay.y);
-      az_d += static_cast<double>(az.x) + static_cast<double>(az.y);
+      // fold this tile's FP32 partials into the FP64 accumulators
+      ph0 += ph.x;
+      ph1 += ph.y;
+      if constexpr (kAcc) {
+        ax0 += ax.x;
+        ax1 += ax.y;
+        ay0 += ay.x;
+        ay1 += ay.y;
+        az0 += az.x;
+        az1 += az.y;
+      }
     }
     cursor = nxt[0];
     cur_off = nxt[1];
     __syncthreads();
   }
-  // --- reduce the G lane groups in fixed order and write (target-owned)
-  red[0][tid] = phi_d;
-  red[1][tid] = ax_d;
-  red[2][tid] = ay_d;
-  red[3][tid] = az_d;
+  // reduce the G lane groups in fixed order (reusing the tile buffer) and write
+  double* red = reinterpret_cast<double*>(sS);  // [G][slots][2 targets][4]
+  if (active) {
+    double* r = red + 8 * (g * slots + t);
+    r[0] = ph0; r[1] = ax0; r[2] = ay0; r[3] = az0;
+    r[4] = ph1; r[5] = ax1; r[6] = ay1; r[7] = az1;
+  }
   __syncthreads();
   if (tid < nt) {
+    const int sl = tid >> 1, h = tid & 1;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int gg = 0; gg < G; ++gg)
-      for (int c = 0; c < 4; ++c) v[c] += red[c][gg * nt + tid];
+    for (int gg = 0; gg < G; ++gg) {
+      const double* r = red + 8 * (gg * slots + sl) + 4 * h;
+      v[0] += r[0];
+      v[1] += r[1];
+      v[2] += r[2];
+      v[3] += r[3];
+    }
     if (it.pbase < 0) {
       const int32_t i = it.tb + tid;
       phi_out[i] = v[0];
-      if (with_acc) {
+      if (kAcc) {
         acc_out[3 * i] = v[1];
         acc_out[3 * i + 1] = v[2];
         acc_out[3 * i + 2] = v[3];
@@ -528,8 +530,12 @@ void run_p2p(fmm_ctx* c, cudaStream_t s) {
   const P2PItem* items = reinterpret_cast<const P2PItem*>(c->p2p_items.p);
   if (c->n_p2p_items > 0) {
     if (c->cfg.precision == FMM_PREC_FP32_P2P) {
-      k_p2p_fp32<<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p,
-                                                              c->c_cr.p, c->bodyf.p, phi, acc, c->p2p_partial.p, wa);
+      if (wa)
+        k_p2p_fp32<true><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(
+            items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, c->bodyf.p, phi, acc, c->p2p_partial.p);
+      else
+        k_p2p_fp32<false><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(
+            items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, c->bodyf.p, phi, acc, c->p2p_partial.p);
     } else {
       k_p2p_fp64<<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p,
                                                               c->bodies.p, phi, acc, c->p2p_partial.p, wa);

@@ -46,72 +46,75 @@ __device__ __forceinline__ void classify(const int2 pr, const double4* __restric
   nchild = split_t ? tc : sc;
 }
 
-struct Cnt {  // per-pair output counts; one exclusive scan gives all three offsets
-  long long m2l, p2p, push;
-};
-struct CntSum {
-  __host__ __device__ __forceinline__ Cnt operator()(const Cnt& a, const Cnt& b) const {
-    return Cnt{a.m2l + b.m2l, a.p2p + b.p2p, a.push + b.push};
-  }
-};
-
-__global__ void k_classify(const int2* __restrict__ fr, int64_t n, const double4* __restrict__ cr,
-                           const int32_t* __restrict__ cc, double theta, int mutual,
-                           uint8_t* __restrict__ kinds, Cnt* __restrict__ cnt) {
+// One frontier step: every pair is classified (process_pair) and its outputs are placed with
+// warp-aggregated atomics. The emission order is therefore not deterministic, but the lists
+// are canonicalised afterwards by a radix sort on (target, source), so everything downstream
+// (CSR order, summation order, results) is deterministic.
+__global__ void __launch_bounds__(256)
+k_step(const int2* __restrict__ fr, int64_t n, const double4* __restrict__ cr, const int32_t* __restrict__ cc,
+       const int32_t* __restrict__ cb, double theta, int mutual, int sbits, uint64_t* __restrict__ m2l_keys,
+       uint64_t* __restrict__ p2p_keys, int2* __restrict__ next, unsigned long long* __restrict__ ctr) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i > n) return;
-  if (i == n) {  // trailing element: the exclusive scan's last entry is the total
-    cnt[i] = Cnt{0, 0, 0};
-    return;
-  }
-  int kind, nchild;
-  classify(fr[i], cr, cc, theta, mutual, kind, nchild);
-  kinds[i] = static_cast<uint8_t>(kind);
-  cnt[i] = Cnt{kind == 0, kind == 1, nchild};
-}
-
-__global__ void k_expand(const int2* __restrict__ fr, int64_t n, const uint8_t* __restrict__ kinds,
-                         const int32_t* __restrict__ cc, const int32_t* __restrict__ cb,
-                         const Cnt* __restrict__ off, int2* __restrict__ m2l, int64_t m2l_base,
-                         int2* __restrict__ p2p, int64_t p2p_base, int2* __restrict__ next) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int2 pr = fr[i];
-  const int kind = kinds[i];
-  const Cnt o = off[i];
-  if (kind == 0) { m2l[m2l_base + o.m2l] = pr; return; }
-  if (kind == 1) { p2p[p2p_base + o.p2p] = pr; return; }
-  int64_t q = o.push;
-  if (kind == 2) {
-    const int32_t b = cb[pr.x], m = cc[pr.x];
-    for (int k = 0; k < m; ++k) next[q + k] = make_int2(b + k, pr.y);
-  } else if (kind == 3) {
-    const int32_t b = cb[pr.y], m = cc[pr.y];
-    for (int k = 0; k < m; ++k) next[q + k] = make_int2(pr.x, b + k);
-  } else {
-    const int32_t b = cb[pr.x], m = cc[pr.x];
-    for (int a = 0; a < m; ++a)
-      for (int c = a; c < m; ++c) next[q++] = make_int2(b + a, b + c);
-  }
-}
-
-__global__ void k_split_pairs(const int2* __restrict__ pr, int64_t n, uint32_t* __restrict__ t,
-                              int32_t* __restrict__ s) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int kind = -1, nchild = 0;
+  int2 pr = make_int2(0, 0);
   if (i < n) {
-    const int2 v = pr[i];
-    t[i] = static_cast<uint32_t>(v.x);
-    s[i] = v.y;
+    pr = fr[i];
+    classify(pr, cr, cc, theta, mutual, kind, nchild);
+  }
+  const unsigned bm = __ballot_sync(0xffffffffu, kind == 0);
+  const unsigned bp = __ballot_sync(0xffffffffu, kind == 1);
+  int incl = nchild;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long base_m = 0, base_p = 0, base_c = 0;
+  if (lane == 0) {
+    if (bm) base_m = atomicAdd(&ctr[0], (unsigned long long)__popc(bm));
+    if (bp) base_p = atomicAdd(&ctr[1], (unsigned long long)__popc(bp));
+    if (wtot) base_c = atomicAdd(&ctr[2], (unsigned long long)wtot);
+  }
+  base_m = __shfl_sync(0xffffffffu, base_m, 0);
+  base_p = __shfl_sync(0xffffffffu, base_p, 0);
+  base_c = __shfl_sync(0xffffffffu, base_c, 0);
+  const unsigned lt = (1u << lane) - 1u;
+  const uint64_t key = ((uint64_t)(uint32_t)pr.x << sbits) | (uint32_t)pr.y;
+  if (kind == 0) {
+    m2l_keys[base_m + __popc(bm & lt)] = key;
+  } else if (kind == 1) {
+    p2p_keys[base_p + __popc(bp & lt)] = key;
+  } else if (kind >= 2) {
+    int64_t q = (int64_t)base_c + incl - nchild;
+    if (kind == 2) {
+      const int32_t b = cb[pr.x];
+      for (int k = 0; k < nchild; ++k) next[q + k] = make_int2(b + k, pr.y);
+    } else if (kind == 3) {
+      const int32_t b = cb[pr.y];
+      for (int k = 0; k < nchild; ++k) next[q + k] = make_int2(pr.x, b + k);
+    } else {
+      const int32_t b = cb[pr.x], m = cc[pr.x];
+      for (int a = 0; a < m; ++a)
+        for (int c = a; c < m; ++c) next[q++] = make_int2(b + a, b + c);
+    }
   }
 }
 
-// offsets from the target-sorted key array: targets tp+1..t start at i
-__global__ void k_csr_offsets(const uint32_t* __restrict__ t_sorted, int64_t n, int64_t ncells,
-                              int64_t* __restrict__ off) {
+__global__ void k_pair_keys(const int2* __restrict__ pr, int64_t n, int sbits, uint64_t* __restrict__ keys) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = ((uint64_t)(uint32_t)pr[i].x << sbits) | (uint32_t)pr[i].y;
+}
+
+// CSR from sorted (target, source) keys: sources, and offsets (targets tp+1..t start at i)
+__global__ void k_csr_from_keys(const uint64_t* __restrict__ keys, int64_t n, int sbits, int64_t ncells,
+                                int64_t* __restrict__ off, int32_t* __restrict__ src) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i > n) return;
-  const int64_t t = i < n ? (int64_t)t_sorted[i] : ncells;
-  const int64_t tp = i > 0 ? (int64_t)t_sorted[i - 1] : -1;
+  const uint64_t mask = (1ull << sbits) - 1;
+  const int64_t t = i < n ? (int64_t)(keys[i] >> sbits) : ncells;
+  const int64_t tp = i > 0 ? (int64_t)(keys[i - 1] >> sbits) : -1;
+  if (i < n) src[i] = (int32_t)(keys[i] & mask);
   for (int64_t c = tp + 1; c <= t; ++c) off[c] = i;
 }
 
@@ -152,9 +155,9 @@ void grow_keep(fmm_ctx* c, DBuf<T>& buf, size_t used, size_t need) {
   buf.cap = want;
 }
 
-// Groups (target, source) pairs into CSR by target: a stable radix sort on the target index
-// only (ceil(log2 ncells) bits), so sources keep the traversal's deterministic emission order.
-void to_csr(fmm_ctx* c, const int2* d_pairs, int64_t n, DBuf<int64_t>& off, DBuf<int32_t>& src) {
+// Sorts packed (target, source) keys (2 * ceil(log2 ncells) bits) and splits them into CSR by
+// target with ascending sources: the canonical form of the emitted multiset.
+void keys_to_csr(fmm_ctx* c, uint64_t* keys, int64_t n, DBuf<int64_t>& off, DBuf<int32_t>& src) {
   cudaStream_t s = c->stream;
   const int64_t nc = c->ncells;
   off.ensure(nc + 1);
@@ -163,25 +166,32 @@ void to_csr(fmm_ctx* c, const int2* d_pairs, int64_t n, DBuf<int64_t>& off, DBuf
     CK(cudaMemsetAsync(off.p, 0, sizeof(int64_t) * (nc + 1), s));
     return;
   }
-  const int tbits = bits_for(static_cast<uint64_t>(nc));
-  uint32_t* ta = reinterpret_cast<uint32_t*>(c->keys_a.ensure((n + 1) / 2 + 1));
-  uint32_t* tb = reinterpret_cast<uint32_t*>(c->keys_b.ensure((n + 1) / 2 + 1));
-  int32_t* sa = c->i32_c.ensure(n);
-  k_split_pairs<<<ceil_div(n, 256), 256, 0, s>>>(d_pairs, n, ta, sa);
+  const int sbits = bits_for(static_cast<uint64_t>(nc));
+  uint64_t* kb = c->keys_b.ensure(n);
   size_t sb = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, sb, ta, tb, sa, src.p, (int)n, 0, tbits, s));
-  CK(cub::DeviceRadixSort::SortPairs(temp_storage(c, sb), sb, ta, tb, sa, src.p, (int)n, 0, tbits, s));
-  k_csr_offsets<<<ceil_div(n + 1, 256), 256, 0, s>>>(tb, n, nc, off.p);
-  CK_LAUNCH("to_csr");
-  c->kernel_launches += 4;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys, kb, (int)n, 0, 2 * sbits, s));
+  CK(cub::DeviceRadixSort::SortKeys(temp_storage(c, sb), sb, keys, kb, (int)n, 0, 2 * sbits, s));
+  k_csr_from_keys<<<ceil_div(n + 1, 256), 256, 0, s>>>(kb, n, sbits, nc, off.p, src.p);
+  CK_LAUNCH("keys_to_csr");
+  c->kernel_launches += 3;
 }
 
 }  // namespace
 
 void lists_from_pairs(fmm_ctx* c, const int2* d_m2l, int64_t n_m2l, const int2* d_p2p, int64_t n_p2p) {
+  const int sbits = bits_for(static_cast<uint64_t>(c->ncells));
+  uint64_t* mk = c->m2l_keys.ensure(n_m2l + 1);
+  uint64_t* pk = c->p2p_keys.ensure(n_p2p + 1);
+  if (n_m2l) k_pair_keys<<<ceil_div(n_m2l, 256), 256, 0, c->stream>>>(d_m2l, n_m2l, sbits, mk);
+  if (n_p2p) k_pair_keys<<<ceil_div(n_p2p, 256), 256, 0, c->stream>>>(d_p2p, n_p2p, sbits, pk);
+  CK_LAUNCH("k_pair_keys");
+  finish_lists(c, n_m2l, n_p2p);
+}
+
+void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
   cudaStream_t s = c->stream;
-  to_csr(c, d_m2l, n_m2l, c->m2l_off, c->m2l_src);
-  to_csr(c, d_p2p, n_p2p, c->p2p_off, c->p2p_src);
+  keys_to_csr(c, c->m2l_keys.p, n_m2l, c->m2l_off, c->m2l_src);
+  keys_to_csr(c, c->p2p_keys.p, n_p2p, c->p2p_off, c->p2p_src);
   c->n_m2l = n_m2l;
   c->n_p2p = n_p2p;
   // body-pair count (P2P work) and the M2L target list
@@ -214,47 +224,39 @@ void traverse(fmm_ctx* c) {
   if (!(theta > 0.0 && theta < 1.0)) fail(FMM_ERR_THETA, "theta must be in (0,1)");
   cudaStream_t s = c->stream;
   const int mutual = c->cfg.mutual ? 1 : 0;
+  const int fan = mutual ? 36 : 8;  // max pairs pushed per pair
+  const int sbits = bits_for(static_cast<uint64_t>(c->ncells));
 
   int64_t nf = 1, nm = 0, np = 0;
   const int2 root = make_int2(0, 0);
   DBuf<int2>* fa = &c->pairs_a;
   DBuf<int2>* fb = &c->pairs_d;
-  DBuf<int2>* m2l = &c->pairs_b;
-  DBuf<int2>* p2p = &c->pairs_c;
   fa->ensure(1024);
-  fb->ensure(1024);
-  m2l->ensure(1024);
-  p2p->ensure(1024);
   CK(cudaMemcpyAsync(fa->p, &root, sizeof(int2), cudaMemcpyHostToDevice, s));
-  Cnt* hcnt = reinterpret_cast<Cnt*>(c->hpin);
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(c->d_counters.ensure(8)) + 4;
+  unsigned long long* h = reinterpret_cast<unsigned long long*>(c->hpin);
   int launches = 0;
   while (nf > 0) {
-    Cnt* cnt = reinterpret_cast<Cnt*>(c->scan_a.ensure(3 * (nf + 1) * 2));
-    Cnt* off = cnt + (nf + 1);
-    uint8_t* kinds = reinterpret_cast<uint8_t*>(c->keys_a.ensure(nf / 8 + 2));
-    k_classify<<<ceil_div(nf + 1, 256), 256, 0, s>>>(fa->p, nf, c->c_cr.p, c->c_child_count.p, theta, mutual,
-                                                     kinds, cnt);
-    CK_LAUNCH("k_classify");
-    size_t sb = 0;
-    CK(cub::DeviceScan::ExclusiveScan(nullptr, sb, cnt, off, CntSum(), Cnt{0, 0, 0}, (int)(nf + 1), s));
-    CK(cub::DeviceScan::ExclusiveScan(temp_storage(c, sb), sb, cnt, off, CntSum(), Cnt{0, 0, 0}, (int)(nf + 1), s));
-    CK(cudaMemcpyAsync(hcnt, off + nf, sizeof(Cnt), cudaMemcpyDeviceToHost, s));
+    grow_keep(c, c->m2l_keys, nm, nm + nf);
+    grow_keep(c, c->p2p_keys, np, np + nf);
+    fb->ensure(fan * nf);
+    h[0] = nm;
+    h[1] = np;
+    h[2] = 0;
+    CK(cudaMemcpyAsync(ctr, h, 3 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+    k_step<<<ceil_div(nf, 256), 256, 0, s>>>(fa->p, nf, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
+                                             mutual, sbits, c->m2l_keys.p, c->p2p_keys.p, fb->p, ctr);
+    CK_LAUNCH("k_step");
+    CK(cudaMemcpyAsync(h + 4, ctr, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    const int64_t add_m = hcnt->m2l, add_p = hcnt->p2p, nnext = hcnt->push;
-    grow_keep(c, *m2l, nm, nm + add_m);
-    grow_keep(c, *p2p, np, np + add_p);
-    fb->ensure(nnext > 0 ? nnext : 1);
-    k_expand<<<ceil_div(nf, 256), 256, 0, s>>>(fa->p, nf, kinds, c->c_child_count.p, c->c_child_begin.p, off,
-                                               m2l->p, nm, p2p->p, np, fb->p);
-    CK_LAUNCH("k_expand");
-    launches += 3;
-    nm += add_m;
-    np += add_p;
-    nf = nnext;
+    ++launches;
+    nm = static_cast<int64_t>(h[4]);
+    np = static_cast<int64_t>(h[5]);
+    nf = static_cast<int64_t>(h[6]);
     std::swap(fa, fb);
   }
   c->kernel_launches += launches;
-  lists_from_pairs(c, m2l->p, nm, p2p->p, np);
+  finish_lists(c, nm, np);
 }
 
 }  // namespace fmmb

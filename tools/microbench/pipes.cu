@@ -85,6 +85,30 @@ __global__ void k_dfma(double* out, double a, double b) {
   if (s == 12345.) out[0] = s;
 }
 
+// mixed: FFMA2 chains interleaved with scalar FFMA chains (heavy + lite pipes?)
+__global__ void k_mixed(float* out, const float* ab) {
+  float2 x[CHAINS], c2[CHAINS];
+  float y[CHAINS], c1[CHAINS];
+  const float2 b2 = make_float2(ab[0], ab[1]);
+  const float b1 = ab[2];
+  for (int i = 0; i < CHAINS; ++i) {
+    x[i] = make_float2(threadIdx.x * 1e-3f + i, i);
+    c2[i] = make_float2(ab[4 + i], ab[5 + i]);
+    y[i] = threadIdx.x * 2e-3f + i;
+    c1[i] = ab[4 + i];
+  }
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < CHAINS; ++i) {
+      x[i] = __ffma2_rn(x[i], c2[i], b2);
+      y[i] = __fmaf_rn(y[i], c1[i], b1);
+    }
+  }
+  float s = 0;
+  for (int i = 0; i < CHAINS; ++i) s += x[i].x + x[i].y + y[i];
+  if (s == 12345.f) out[0] = s;
+}
+
 template <class F>
 float time_it(F f, int reps = 5) {
   cudaEvent_t e0, e1;
@@ -133,6 +157,8 @@ int main() {
   report("ffma2", ms, double(ITERS) * CHAINS * 2);
   ms = time_it([&] { k_ffma2_reg<<<blocks, threads>>>(d, d); });
   report("ffma2_reg", ms, double(ITERS) * CHAINS * 2);
+  ms = time_it([&] { k_mixed<<<blocks, threads>>>(d, d); });
+  report("ffma2+ffma", ms, double(ITERS) * CHAINS * 3);
   ms = time_it([&] { k_rsq<<<blocks, threads>>>(d, 1.f); });
   report("mufu_rsq", ms, double(ITERS) * CHAINS);
   ms = time_it([&] { k_dfma<<<blocks, threads>>>((double*)d, 0.999, 1e-4); });
