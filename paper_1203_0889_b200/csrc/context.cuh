@@ -58,6 +58,7 @@ struct fmm_ctx {
   int64_t n_p2p_items = 0;
   fmmb::DBuf<double> p2p_partial;   // [slot][target body][4] (phi, ax, ay, az)
   fmmb::DBuf<int4> p2p_reduce;      // target leaf, first slot, n slots, body begin
+  fmmb::DBuf<int4> p2p_ent;         // per P2P list entry: {body_begin, count, shift.xy} + {shift.z,...}
   int64_t n_p2p_reduce = 0;
 
   // expansions and outputs

@@ -25,7 +25,10 @@ namespace {
 
 constexpr int kThreads = 128;   // threads per P2P CTA (max target bodies per item)
 constexpr int kTileSegs = 32;   // list entries staged per tile
-constexpr int kTileBodies = 1024;
+#ifndef FMM_P2P_TILE
+#define FMM_P2P_TILE 1024
+#endif
+constexpr int kTileBodies = FMM_P2P_TILE;
 
 struct P2PItem {
   int32_t leaf, tb, te, lb, le;  // target leaf, target body range, list range [lb, le)
@@ -90,32 +93,189 @@ __device__ __forceinline__ void tile_setup(int tid, int32_t le, int32_t cursor, 
 
 // ------------------------------------------------------------------------ FP32 kernel ----
 // Thread (g, t) owns the target pair (2t, 2t+1) of the item, packed in f32x2 lanes, and every
-// G-th source of each tile (G = 128 / ceil(n_t/2) lane groups). Sources are stored once as
-// float4 {-x, -y, -z, q} in the target leaf's frame; the packed ops take the source component
-// as a broadcast scalar operand, so one LDS.128 feeds two pair evaluations.
+// G-th source of each tile (G = 128 / ceil(n_t/2) lane groups). Sources are staged as float4
+// {-x, -y, -z, q} in the target leaf's frame; the packed ops take the source component as a
+// broadcast scalar operand, so one LDS.128 feeds two pair evaluations.
+//
+// Tiles are software-pipelined: while tile k is computed from one shared buffer, tile k+1's
+// raw bodies stream into the other buffer with cp.async (no registers), and warp 0 resolves
+// tile k+2's list entries. After the compute, each thread converts the bodies it copied in
+// place (shift into the target frame, negate), and one barrier per tile publishes them.
+struct P2PEnt {  // one P2P list entry (target-specific): source bodies and FP32 frame shift
+  int32_t bb, n;
+  float sx, sy, sz;
+  int32_t pad[3];
+};
+static_assert(sizeof(P2PEnt) == 32, "P2PEnt is 32 B");
+
+struct TileTab {
+  int32_t off[kTileSegs + 1];
+  int32_t bb[kTileSegs];
+  float sh[kTileSegs][3];
+  int32_t nseg, next, next_off;
+};
+
+// warp 0: take the list entries from (cursor, cur_off) that fit in one tile
+__device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cursor, int32_t cur_off,
+                                               const P2PEnt* __restrict__ ent, TileTab& tt) {
+  const int32_t k = cursor + lane;
+  int32_t n = 0, b = 0;
+  float sx = 0.f, sy = 0.f, sz = 0.f;
+  if (k < le) {
+    const int4 e0 = reinterpret_cast<const int4*>(ent)[2 * k];
+    const float z = reinterpret_cast<const float*>(ent)[8 * k + 4];
+    b = e0.x;
+    n = e0.y;
+    sx = __int_as_float(e0.z);
+    sy = __int_as_float(e0.w);
+    sz = z;
+    if (lane == 0) {
+      b += cur_off;
+      n -= cur_off;
+    }
+  }
+  int32_t incl = n;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const bool fits = (k < le) && (incl <= kTileBodies);
+  const unsigned m = __ballot_sync(0xffffffffu, fits);
+  int nseg;
+  if (m == 0) {  // one (level-21 overflow) leaf larger than the tile: take kTileBodies of it
+    nseg = 1;
+    incl = kTileBodies;
+  } else {
+    nseg = 32 - __clz(m);  // fits is a prefix of the lanes
+  }
+  if (lane < nseg) {
+    tt.off[lane + 1] = incl;
+    tt.bb[lane] = b;
+    tt.sh[lane][0] = sx;
+    tt.sh[lane][1] = sy;
+    tt.sh[lane][2] = sz;
+  }
+  if (lane == 0) {
+    tt.off[0] = 0;
+    tt.nseg = nseg;
+    tt.next = m == 0 ? cursor : cursor + nseg;
+    tt.next_off = m == 0 ? cur_off + kTileBodies : 0;
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// all threads: issue the raw copies of one tile (warp w copies segments w, w+4, ...)
+__device__ __forceinline__ void tile_issue(int tid, const TileTab& tt, const float4* __restrict__ bodyf,
+                                           float4* buf) {
+  const int w = tid >> 5, lane = tid & 31;
+  for (int k = w; k < tt.nseg; k += kThreads / 32) {
+    const int32_t base = tt.bb[k], o0 = tt.off[k], n = tt.off[k + 1] - o0;
+    for (int j = lane; j < n; j += 32) cp_async16(&buf[o0 + j], &bodyf[base + j]);
+  }
+}
+
+// all threads: convert the bodies this thread copied (same mapping as tile_issue)
+__device__ __forceinline__ void tile_convert(int tid, const TileTab& tt, float4* buf) {
+  const int w = tid >> 5, lane = tid & 31;
+  for (int k = w; k < tt.nseg; k += kThreads / 32) {
+    const int32_t o0 = tt.off[k], n = tt.off[k + 1] - o0;
+    const float sx = tt.sh[k][0], sy = tt.sh[k][1], sz = tt.sh[k][2];
+    for (int j = lane; j < n; j += 32) {
+      const float4 b = buf[o0 + j];
+      buf[o0 + j] = make_float4(-b.x - sx, -b.y - sy, -b.z - sz, b.w);
+    }
+  }
+}
+
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// One source against the thread's two targets: 13 FP32-pipe lane-ops per pair (3 dx, 3 r^2,
+// q/r, phi, 1/r^2, q/r^3, 3 acc) and one MUFU.RSQ (XU pipe: 16/clk/SM, so a second MUFU per
+// pair would make the XU the bottleneck); r^2 == 0 pairs (self, coincident;
+// kernels.cpp:185-186) are predicated off.
+template <bool kAcc>
+__device__ __forceinline__ void pair_body(const float4 sv, const float2 X, const float2 Y, const float2 Z, float2& ph,
+                                          float2& ax, float2& ay, float2& az) {
+  const float2 dx = __fadd2_rn(X, make_float2(sv.x, sv.x));
+  const float2 dy = __fadd2_rn(Y, make_float2(sv.y, sv.y));
+  const float2 dz = __fadd2_rn(Z, make_float2(sv.z, sv.z));
+  float2 r2 = __fmul2_rn(dx, dx);
+  r2 = __ffma2_rn(dy, dy, r2);
+  r2 = __ffma2_rn(dz, dz, r2);
+  float2 ri = make_float2(0.f, 0.f);
+  if (r2.x > 0.f) ri.x = rsqrt_approx(r2.x);
+  if (r2.y > 0.f) ri.y = rsqrt_approx(r2.y);
+  const float2 qr = __fmul2_rn(make_float2(sv.w, sv.w), ri);
+  ph = __fadd2_rn(ph, qr);
+  if constexpr (kAcc) {
+    const float2 qr3 = __fmul2_rn(qr, __fmul2_rn(ri, ri));
+    ax = __ffma2_rn(dx, qr3, ax);
+    ay = __ffma2_rn(dy, qr3, ay);
+    az = __ffma2_rn(dz, qr3, az);
+  }
+}
+
+template <bool kAcc>
+__device__ __forceinline__ void tile_compute(const float4* __restrict__ buf, int nb, int g, int G, float2 X,
+                                             float2 Y, float2 Z, double& ph0, double& ph1, double& ax0,
+                                             double& ax1, double& ay0, double& ay1, double& az0, double& az1) {
+  float2 ph = make_float2(0.f, 0.f), ax = ph, ay = ph, az = ph;
+  // group g takes a contiguous chunk of the tile: unit stride, immediate-offset LDS and one
+  // pointer bump per 4 independent sources (ILP, no per-source address arithmetic)
+  const int chunk = ((nb + G - 1) / G) | 1;  // odd: the groups of a warp hit distinct banks
+  const float4* p = buf + g * chunk;
+  const float4* const end = buf + min(nb, (g + 1) * chunk);
+#ifndef FMM_P2P_UNROLL
+#define FMM_P2P_UNROLL 8
+#endif
+  constexpr int U = FMM_P2P_UNROLL;
+  for (; p + (U - 1) < end; p += U) {
+    float4 sv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) sv[u] = p[u];
+#pragma unroll
+    for (int u = 0; u < U; ++u) pair_body<kAcc>(sv[u], X, Y, Z, ph, ax, ay, az);
+  }
+  for (; p < end; ++p) pair_body<kAcc>(*p, X, Y, Z, ph, ax, ay, az);
+  // fold this tile's FP32 partials into the FP64 accumulators
+  ph0 += ph.x;
+  ph1 += ph.y;
+  if constexpr (kAcc) {
+    ax0 += ax.x;
+    ax1 += ax.y;
+    ay0 += ay.x;
+    ay1 += ay.y;
+    az0 += az.x;
+    az1 += az.y;
+  }
+}
+
 #ifndef FMM_P2P_MIN_BLOCKS
 #define FMM_P2P_MIN_BLOCKS 6
 #endif
 template <bool kAcc>
 __global__ void __launch_bounds__(kThreads, FMM_P2P_MIN_BLOCKS)
-k_p2p_fp32(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_list,
-           const int32_t* __restrict__ bb, const int32_t* __restrict__ be, const double4* __restrict__ cr,
-           const float4* __restrict__ bodyf, double* __restrict__ phi_out, double* __restrict__ acc_out,
-           double* __restrict__ partial) {
-  __shared__ __align__(16) float4 sS[kTileBodies];
-  __shared__ int32_t seg_off[kTileSegs + 1];
-  __shared__ int32_t seg_src[kTileSegs];
-  __shared__ int32_t seg_boff[kTileSegs];
-  __shared__ int32_t nxt[3];
+k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, const float4* __restrict__ bodyf,
+           double* __restrict__ phi_out, double* __restrict__ acc_out, double* __restrict__ partial) {
+  __shared__ __align__(16) float4 sS[2][kTileBodies];
+  __shared__ TileTab tabs[3];  // ring: tile k computes from tabs[k%3] while k+2 is resolved
 
   const P2PItem it = items[blockIdx.x];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int nt = it.te - it.tb;
   const int slots = (nt + 1) >> 1;
   const int G = kThreads / slots;
   const int g = tid / slots, t = tid - g * slots;
   const bool active = g < G;
-  const double4 ct = cr[it.leaf];
 
   float2 X = make_float2(0.f, 0.f), Y = X, Z = X;
   if (active) {
@@ -127,65 +287,35 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_li
   }
   double ph0 = 0.0, ph1 = 0.0, ax0 = 0.0, ax1 = 0.0, ay0 = 0.0, ay1 = 0.0, az0 = 0.0, az1 = 0.0;
 
-  int32_t cursor = it.lb, cur_off = 0;
-  while (cursor < it.le) {
-    tile_setup<kTileBodies>(tid, it.le, cursor, cur_off, src_list, bb, be, seg_off, seg_src, seg_boff, nxt);
-    __syncthreads();
-    const int32_t nseg = nxt[2];
-    const int32_t nb = seg_off[nseg];
-    {  // fill: warp w copies entries w, w+4, ...; shift = c_s - c_t in FP64, rounded once
-      const int w = tid >> 5, lane = tid & 31;
-      for (int k = w; k < nseg; k += kThreads / 32) {
-        const int32_t src = seg_src[k];
-        const int32_t base = bb[src] + seg_boff[k], n = seg_off[k + 1] - seg_off[k], o0 = seg_off[k];
-        const double4 cs = cr[src];
-        const float sx = static_cast<float>(cs.x - ct.x), sy = static_cast<float>(cs.y - ct.y),
-                    sz = static_cast<float>(cs.z - ct.z);
-        for (int j = lane; j < n; j += 32) {
-          const float4 b = bodyf[base + j];
-          sS[o0 + j] = make_float4(-(b.x + sx), -(b.y + sy), -(b.z + sz), b.w);
-        }
-      }
+  // prologue: tile 0 staged and converted, tile 1 resolved
+  if (tid < 32) tile_setup_ent(lane, it.le, it.lb, 0, ent, tabs[0]);
+  __syncthreads();
+  bool have = it.lb < it.le;
+  if (have) {
+    tile_issue(tid, tabs[0], bodyf, sS[0]);
+    cp_async_wait_all();
+    tile_convert(tid, tabs[0], sS[0]);
+    if (tid < 32 && tabs[0].next < it.le) tile_setup_ent(lane, it.le, tabs[0].next, tabs[0].next_off, ent, tabs[1]);
+  }
+  __syncthreads();
+  int k3 = 0, k2 = 0;  // tile index mod 3 (tables) and mod 2 (buffers)
+  while (have) {
+    const TileTab& tc = tabs[k3];
+    const int n1 = k3 == 2 ? 0 : k3 + 1, n2 = n1 == 2 ? 0 : n1 + 1;
+    const TileTab& tn = tabs[n1];
+    const bool more = tc.next < it.le;
+    const int nb = tc.off[tc.nseg];
+    if (more) tile_issue(tid, tn, bodyf, sS[k2 ^ 1]);
+    if (active) tile_compute<kAcc>(sS[k2], nb, g, G, X, Y, Z, ph0, ph1, ax0, ax1, ay0, ay1, az0, az1);
+    if (more) {
+      cp_async_wait_all();
+      tile_convert(tid, tn, sS[k2 ^ 1]);
+      if (tid < 32 && tn.next < it.le) tile_setup_ent(lane, it.le, tn.next, tn.next_off, ent, tabs[n2]);
     }
-    __syncthreads();
-    if (active) {
-      float2 ph = make_float2(0.f, 0.f), ax = ph, ay = ph, az = ph;
-#pragma unroll 4
-      for (int j = g; j < nb; j += G) {
-        const float4 sv = sS[j];
-        const float2 dx = __fadd2_rn(X, make_float2(sv.x, sv.x));
-        const float2 dy = __fadd2_rn(Y, make_float2(sv.y, sv.y));
-        const float2 dz = __fadd2_rn(Z, make_float2(sv.z, sv.z));
-        float2 r2 = __fmul2_rn(dx, dx);
-        r2 = __ffma2_rn(dy, dy, r2);
-        r2 = __ffma2_rn(dz, dz, r2);
-        float2 ri;  // r^2 == 0 (self / coincident) contributes nothing (kernels.cpp:185-186)
-        ri.x = r2.x > 0.f ? rsqrtf(r2.x) : 0.f;
-        ri.y = r2.y > 0.f ? rsqrtf(r2.y) : 0.f;
-        const float2 qr = __fmul2_rn(make_float2(sv.w, sv.w), ri);
-        ph = __fadd2_rn(ph, qr);
-        if constexpr (kAcc) {
-          const float2 qr3 = __fmul2_rn(qr, __fmul2_rn(ri, ri));
-          ax = __ffma2_rn(dx, qr3, ax);
-          ay = __ffma2_rn(dy, qr3, ay);
-          az = __ffma2_rn(dz, qr3, az);
-        }
-      }
-      // fold this tile's FP32 partials into the FP64 accumulators
-      ph0 += ph.x;
-      ph1 += ph.y;
-      if constexpr (kAcc) {
-        ax0 += ax.x;
-        ax1 += ax.y;
-        ay0 += ay.x;
-        ay1 += ay.y;
-        az0 += az.x;
-        az1 += az.y;
-      }
-    }
-    cursor = nxt[0];
-    cur_off = nxt[1];
-    __syncthreads();
+    __syncthreads();  // tile k+1 published, tile k+2 resolved; everyone is done with tile k
+    have = more;
+    k3 = n1;
+    k2 ^= 1;
   }
   // reduce the G lane groups in fixed order (reusing the tile buffer) and write
   double* red = reinterpret_cast<double*>(sS);  // [G][slots][2 targets][4]
@@ -220,6 +350,31 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_li
       p[2] = v[2];
       p[3] = v[3];
     }
+  }
+}
+
+// Resolves every P2P list entry of every target leaf into {source body range, FP32 shift of
+// the source leaf centre into the target leaf's frame} (computed in FP64, rounded once).
+__global__ void k_p2p_entries(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
+                              const int32_t* __restrict__ src, const int32_t* __restrict__ bb,
+                              const int32_t* __restrict__ be, const double4* __restrict__ cr,
+                              P2PEnt* __restrict__ ent) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nleaves) return;
+  const int32_t leaf = leaves[w];
+  const double4 ct = cr[leaf];
+  for (int64_t k = off[leaf] + lane; k < off[leaf + 1]; k += 32) {
+    const int32_t s = src[k];
+    const double4 cs = cr[s];
+    P2PEnt e;
+    e.bb = bb[s];
+    e.n = be[s] - bb[s];
+    e.sx = static_cast<float>(cs.x - ct.x);
+    e.sy = static_cast<float>(cs.y - ct.y);
+    e.sz = static_cast<float>(cs.z - ct.z);
+    e.pad[0] = e.pad[1] = e.pad[2] = 0;
+    ent[k] = e;
   }
 }
 
@@ -506,6 +661,13 @@ void build_p2p_worklist(fmm_ctx* c) {
                                                        c->c_body_end.p, sum_ns, nitems, item_off, red_off, part_off,
                                                        items_raw, costs, red);
   CK_LAUNCH("k_write_items");
+  if (c->cfg.precision == FMM_PREC_FP32_P2P) {
+    P2PEnt* ent = reinterpret_cast<P2PEnt*>(c->p2p_ent.ensure(2 * (c->n_p2p + 1)));
+    k_p2p_entries<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->leaves.p, nl, c->p2p_off.p, c->p2p_src.p,
+                                                         c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, ent);
+    CK_LAUNCH("k_p2p_entries");
+    c->kernel_launches += 1;
+  }
   // cost-sorted (descending, stable) work list: the longest items launch first
   int32_t* ord_in = c->i32_c.ensure(2 * (nitem + 1));
   int32_t* ord_out = ord_in + (nitem + 1);
@@ -530,12 +692,13 @@ void run_p2p(fmm_ctx* c, cudaStream_t s) {
   const P2PItem* items = reinterpret_cast<const P2PItem*>(c->p2p_items.p);
   if (c->n_p2p_items > 0) {
     if (c->cfg.precision == FMM_PREC_FP32_P2P) {
+      const P2PEnt* ent = reinterpret_cast<const P2PEnt*>(c->p2p_ent.p);
       if (wa)
-        k_p2p_fp32<true><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(
-            items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, c->bodyf.p, phi, acc, c->p2p_partial.p);
+        k_p2p_fp32<true><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, ent, c->bodyf.p, phi, acc,
+                                                                       c->p2p_partial.p);
       else
-        k_p2p_fp32<false><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(
-            items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, c->bodyf.p, phi, acc, c->p2p_partial.p);
+        k_p2p_fp32<false><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, ent, c->bodyf.p, phi, acc,
+                                                                        c->p2p_partial.p);
     } else {
       k_p2p_fp64<<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p,
                                                               c->bodies.p, phi, acc, c->p2p_partial.p, wa);
