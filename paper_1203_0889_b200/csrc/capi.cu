@@ -101,6 +101,7 @@ int fmm_create(const fmm_config* cfg, fmm_ctx** out) {
       CK(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
       for (int i = 0; i < EV_COUNT; ++i) CK(cudaEventCreate(&c->ev[i]));
       CK(cudaMallocHost(&c->hpin, 64 * sizeof(int64_t)));
+      c->d_counters.ensure(32);
     } catch (...) {
       delete c;
       throw;

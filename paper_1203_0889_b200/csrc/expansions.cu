@@ -89,71 +89,55 @@ k_p2m(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __rest
 }
 
 // ------------------------------------------------------------------------------ M2M ----
-// Warp per non-leaf cell of one level; children accumulated in order k = 0..count-1, each
-// child's multipole staged in shared memory with the power lines d^k/k! of its shift.
+// One CTA per cell of one level; warp k translates child k (staged multipole + power lines
+// d^k/k! of its shift) into a shared-memory partial, and the partials are summed in child
+// order k = 0..count-1 (the reference's accumulation order, traversal.cpp:44-47).
 template <int P>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
 k_m2m(int32_t cbeg, int32_t cend, const int32_t* __restrict__ cb, const int32_t* __restrict__ cc,
       const double4* __restrict__ cr, double* __restrict__ M) {
   using T = MI<P>;
   constexpr int N = T::N;
-  __shared__ double sD[4][3 * P];
-  __shared__ double sM[4][N];
+  __shared__ double sD[8][3 * P];
+  __shared__ double sM[8][N];
+  __shared__ double part[8][N];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t ci = cbeg + blockIdx.x * 4 + w;
+  const int32_t ci = cbeg + blockIdx.x;
   if (ci >= cend) return;
   const int32_t nch = cc[ci];
-  if (nch == 0) return;
-  const double4 pc = cr[ci];
-  constexpr int KPL = (N + 31) / 32;
-  double acc[KPL];
-  int ea[KPL], eb[KPL], ec[KPL];
-#pragma unroll
-  for (int k = 0; k < KPL; ++k) {
-    acc[k] = 0.0;
-    const int i = lane + 32 * k;
-    int n = 0;
-    if (i < N) {
-      while (n_coef(n + 1) <= i) ++n;
-      int r = i - n_coef(n), a = 0;
-      while (r >= n - a + 1) { r -= n - a + 1; ++a; }
-      ea[k] = a;
-      eb[k] = r;
-      ec[k] = n - a - r;
-    }
-  }
-  const int32_t c0 = cb[ci];
-  for (int32_t ch = 0; ch < nch; ++ch) {
-    const int32_t child = c0 + ch;
-    const double4 cc4 = cr[child];
+  if (nch == 0) return;  // uniform over the CTA
+  if (w < nch) {
+    const double4 pc = cr[ci];
+    const int32_t child = cb[ci] + w;
+    const double4 c4 = cr[child];
     if (lane < 3) {
-      const double d = lane == 0 ? cc4.x - pc.x : (lane == 1 ? cc4.y - pc.y : cc4.z - pc.z);
+      const double d = lane == 0 ? c4.x - pc.x : (lane == 1 ? c4.y - pc.y : c4.z - pc.z);
       double* L = sD[w] + lane * P;
       L[0] = 1.0;
       for (int k = 1; k < P; ++k) L[k] = L[k - 1] * d / k;
     }
     for (int i = lane; i < N; i += 32) sM[w][i] = M[(int64_t)child * N + i];
     __syncwarp();
-#pragma unroll
-    for (int k = 0; k < KPL; ++k) {
-      const int i = lane + 32 * k;
-      if (i < N) {
-        const int a = ea[k], bb_ = eb[k], cc_ = ec[k];
-        double s = 0.0;
-        for (int ax = 0; ax <= a; ++ax)
-          for (int ay = 0; ay <= bb_; ++ay) {
-            const double xy = sD[w][a - ax] * sD[w][P + bb_ - ay];
-            for (int az = 0; az <= cc_; ++az) s += sM[w][index_of(ax, ay, az)] * (xy * sD[w][2 * P + cc_ - az]);
-          }
-        acc[k] += s;
-      }
+    for (int i = lane; i < N; i += 32) {
+      int n = 0;
+      while (n_coef(n + 1) <= i) ++n;
+      int r = i - n_coef(n), a = 0;
+      while (r >= n - a + 1) { r -= n - a + 1; ++a; }
+      const int bb_ = r, cc_ = n - a - r;
+      double s = 0.0;
+      for (int ax = 0; ax <= a; ++ax)
+        for (int ay = 0; ay <= bb_; ++ay) {
+          const double xy = sD[w][a - ax] * sD[w][P + bb_ - ay];
+          for (int az = 0; az <= cc_; ++az) s += sM[w][index_of(ax, ay, az)] * (xy * sD[w][2 * P + cc_ - az]);
+        }
+      part[w][i] = s;
     }
-    __syncwarp();
   }
-#pragma unroll
-  for (int k = 0; k < KPL; ++k) {
-    const int i = lane + 32 * k;
-    if (i < N) M[(int64_t)ci * N + i] = acc[k];
+  __syncthreads();
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < nch; ++k) s += part[k][i];
+    M[(int64_t)ci * N + i] = s;
   }
 }
 
@@ -272,7 +256,7 @@ struct Upward {
     for (int l = c->depth - 1; l >= 0; --l) {
       const int32_t b = c->level_start[l], e = c->level_start[l + 1];
       if (e <= b) continue;
-      k_m2m<P><<<ceil_div(e - b, 4), 128, 0, s>>>(b, e, c->c_child_begin.p, c->c_child_count.p, c->c_cr.p, M);
+      k_m2m<P><<<e - b, 256, 0, s>>>(b, e, c->c_child_begin.p, c->c_child_count.p, c->c_cr.p, M);
       CK_LAUNCH("k_m2m");
       ++launches;
     }

@@ -492,31 +492,45 @@ __global__ void k_p2p_reduce(const int4* __restrict__ red, int64_t nred, const d
 // ---------------------------------------------------------------- work list build ----
 // Per target leaf (warp each): sum of source sizes, item count. Leaves are all cells with a
 // non-empty P2P list (every leaf has at least its self pair).
-__global__ void k_leaf_cost(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
-                            const int32_t* __restrict__ src, const int32_t* __restrict__ bb,
-                            const int32_t* __restrict__ be, uint64_t cmax, int64_t* __restrict__ sum_ns,
-                            int32_t* __restrict__ nitems, int32_t* __restrict__ nred, int32_t* __restrict__ npart) {
+__global__ void k_leaf_sum(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
+                           const int32_t* __restrict__ src, const int32_t* __restrict__ bb,
+                           const int32_t* __restrict__ be, int64_t* __restrict__ sum_ns,
+                           unsigned long long* __restrict__ total) {
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= nleaves) return;
   const int32_t leaf = leaves[w];
   const int64_t l0 = off[leaf], l1 = off[leaf + 1];
   int64_t s = 0;
-  for (int64_t k = l0 + lane; k < l1; k += 32) s += be[src[k]] - bb[src[k]];
+  for (int64_t k = l0 + lane; k < l1; k += 32) {
+    const int32_t q = src[k];
+    s += be[q] - bb[q];
+  }
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) {
-    const int64_t nt = be[leaf] - bb[leaf];
-    const int64_t cost = nt * s;
-    int64_t nsc = (cost + (int64_t)cmax - 1) / (int64_t)cmax;
-    if (nsc < 1) nsc = 1;
-    if (nsc > l1 - l0) nsc = l1 - l0;
-    if (l1 == l0) nsc = 0;
-    const int64_t ntc = (nt + kThreads - 1) / kThreads;
     sum_ns[w] = s;
-    nitems[w] = static_cast<int32_t>(nsc * ntc);
-    nred[w] = nsc > 1 ? static_cast<int32_t>(ntc) : 0;
-    npart[w] = nsc > 1 ? static_cast<int32_t>(nsc * nt) : 0;
+    atomicAdd(total, static_cast<unsigned long long>(s) * static_cast<unsigned long long>(be[leaf] - bb[leaf]));
   }
+}
+
+__global__ void k_leaf_cost(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
+                            const int32_t* __restrict__ bb, const int32_t* __restrict__ be, uint64_t cmax,
+                            const int64_t* __restrict__ sum_ns, int32_t* __restrict__ nitems,
+                            int32_t* __restrict__ nred, int32_t* __restrict__ npart) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= nleaves) return;
+  const int32_t leaf = leaves[w];
+  const int64_t l0 = off[leaf], l1 = off[leaf + 1];
+  const int64_t nt = be[leaf] - bb[leaf];
+  const int64_t cost = nt * sum_ns[w];
+  int64_t nsc = (cost + (int64_t)cmax - 1) / (int64_t)cmax;
+  if (nsc < 1) nsc = 1;
+  if (nsc > l1 - l0) nsc = l1 - l0;
+  if (l1 == l0) nsc = 0;
+  const int64_t ntc = (nt + kThreads - 1) / kThreads;
+  nitems[w] = static_cast<int32_t>(nsc * ntc);
+  nred[w] = nsc > 1 ? static_cast<int32_t>(ntc) : 0;
+  npart[w] = nsc > 1 ? static_cast<int32_t>(nsc * nt) : 0;
 }
 
 // Writes the items of one target leaf (warp each). Source chunks split the list where the
@@ -627,20 +641,28 @@ void exclusive_scan_i32(fmm_ctx* c, const int32_t* in, int32_t* out, int64_t n) 
 void build_p2p_worklist(fmm_ctx* c) {
   cudaStream_t s = c->stream;
   const int64_t nl = c->nleaves;
+  int64_t* sum_ns = c->scan_a.ensure(nl + 1);
+  unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->d_counters.ensure(16)) + 12;
+  CK(cudaMemsetAsync(tot, 0, sizeof(unsigned long long), s));
+  k_leaf_sum<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->leaves.p, nl, c->p2p_off.p, c->p2p_src.p, c->c_body_begin.p,
+                                                    c->c_body_end.p, sum_ns, tot);
+  CK_LAUNCH("k_leaf_sum");
+  CK(cudaMemcpyAsync(c->hpin + 16, tot, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  c->p2p_body_pairs = c->hpin[16];
   const uint64_t total = static_cast<uint64_t>(c->p2p_body_pairs);
   // Cost cap per item: an eighth of one SM's fair share, never below 64K pairs, so that a
   // single heavy target (C3's halo leaf: 60.5 M pairs) is spread over many SMs.
   uint64_t cmax = total / (148ull * 8ull);
   if (cmax < 65536ull) cmax = 65536ull;
 
-  int64_t* sum_ns = c->scan_a.ensure(nl + 1);
   int32_t* counts = c->i32_a.ensure(3 * (nl + 1));
   int32_t* offs = c->i32_b.ensure(3 * (nl + 1));
   int32_t *nitems = counts, *nred = counts + (nl + 1), *npart = counts + 2 * (nl + 1);
   int32_t *item_off = offs, *red_off = offs + (nl + 1), *part_off = offs + 2 * (nl + 1);
   CK(cudaMemsetAsync(counts, 0, sizeof(int32_t) * 3 * (nl + 1), s));
-  k_leaf_cost<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->leaves.p, nl, c->p2p_off.p, c->p2p_src.p, c->c_body_begin.p,
-                                                     c->c_body_end.p, cmax, sum_ns, nitems, nred, npart);
+  k_leaf_cost<<<ceil_div(nl, 256), 256, 0, s>>>(c->leaves.p, nl, c->p2p_off.p, c->c_body_begin.p, c->c_body_end.p,
+                                                cmax, sum_ns, nitems, nred, npart);
   CK_LAUNCH("k_leaf_cost");
   exclusive_scan_i32(c, nitems, item_off, nl + 1);
   exclusive_scan_i32(c, nred, red_off, nl + 1);

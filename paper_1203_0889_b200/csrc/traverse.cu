@@ -27,14 +27,27 @@ __device__ __forceinline__ bool mac_exact(const double4 t, const double4 s, doub
   return sum_r < __dmul_rn(theta, __dsqrt_rn(d2));
 }
 
+// Same decision without the FP64 square root whenever it is unambiguous: both sides are
+// compared squared with a 1e-12 relative guard band (the rounding of sqrt and of the products
+// is below 1e-15), and only pairs inside the band take the exact path above.
+__device__ __forceinline__ bool mac_fast(const double4 t, const double4 s, double theta, double theta2) {
+  const double sum_r = __dmul_rn(kSqrt3, __dadd_rn(t.w, s.w));
+  const double dx = __dadd_rn(t.x, -s.x), dy = __dadd_rn(t.y, -s.y), dz = __dadd_rn(t.z, -s.z);
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  const double a2 = sum_r * sum_r, q = theta2 * d2;
+  if (a2 < q * (1.0 - 1e-12)) return true;
+  if (a2 > q * (1.0 + 1e-12)) return false;
+  return sum_r < __dmul_rn(theta, __dsqrt_rn(d2));
+}
+
 // Outcome of process_pair: kind 0 = M2L, 1 = P2P, 2 = split target, 3 = split source,
 // 4 = mutual self split. nchild = number of pushed pairs.
 __device__ __forceinline__ void classify(const int2 pr, const double4* __restrict__ cr,
-                                         const int32_t* __restrict__ cc, double theta, int mutual,
-                                         int& kind, int& nchild) {
+                                         const int32_t* __restrict__ cc, double theta, double theta2,
+                                         int mutual, int& kind, int& nchild) {
   const double4 t = cr[pr.x], s = cr[pr.y];
   const int tc = cc[pr.x], sc = cc[pr.y];
-  if (mac_exact(t, s, theta)) { kind = 0; nchild = 0; return; }
+  if (mac_fast(t, s, theta, theta2)) { kind = 0; nchild = 0; return; }
   if (tc == 0 && sc == 0) { kind = 1; nchild = 0; return; }
   if (mutual && pr.x == pr.y) { kind = 4; nchild = tc * (tc + 1) / 2; return; }
   bool split_t;
@@ -50,17 +63,19 @@ __device__ __forceinline__ void classify(const int2 pr, const double4* __restric
 // warp-aggregated atomics. The emission order is therefore not deterministic, but the lists
 // are canonicalised afterwards by a radix sort on (target, source), so everything downstream
 // (CSR order, summation order, results) is deterministic.
+template <class KeyT>
 __global__ void __launch_bounds__(256)
 k_step(const int2* __restrict__ fr, int64_t n, const double4* __restrict__ cr, const int32_t* __restrict__ cc,
-       const int32_t* __restrict__ cb, double theta, int mutual, int sbits, uint64_t* __restrict__ m2l_keys,
-       uint64_t* __restrict__ p2p_keys, int2* __restrict__ next, unsigned long long* __restrict__ ctr) {
+       const int32_t* __restrict__ cb, double theta, double theta2, int mutual, int sbits,
+       KeyT* __restrict__ m2l_keys, KeyT* __restrict__ p2p_keys, int2* __restrict__ next,
+       unsigned long long* __restrict__ ctr) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   int kind = -1, nchild = 0;
   int2 pr = make_int2(0, 0);
   if (i < n) {
     pr = fr[i];
-    classify(pr, cr, cc, theta, mutual, kind, nchild);
+    classify(pr, cr, cc, theta, theta2, mutual, kind, nchild);
   }
   const unsigned bm = __ballot_sync(0xffffffffu, kind == 0);
   const unsigned bp = __ballot_sync(0xffffffffu, kind == 1);
@@ -80,7 +95,7 @@ k_step(const int2* __restrict__ fr, int64_t n, const double4* __restrict__ cr, c
   base_p = __shfl_sync(0xffffffffu, base_p, 0);
   base_c = __shfl_sync(0xffffffffu, base_c, 0);
   const unsigned lt = (1u << lane) - 1u;
-  const uint64_t key = ((uint64_t)(uint32_t)pr.x << sbits) | (uint32_t)pr.y;
+  const KeyT key = static_cast<KeyT>(((uint64_t)(uint32_t)pr.x << sbits) | (uint32_t)pr.y);
   if (kind == 0) {
     m2l_keys[base_m + __popc(bm & lt)] = key;
   } else if (kind == 1) {
@@ -101,13 +116,15 @@ k_step(const int2* __restrict__ fr, int64_t n, const double4* __restrict__ cr, c
   }
 }
 
-__global__ void k_pair_keys(const int2* __restrict__ pr, int64_t n, int sbits, uint64_t* __restrict__ keys) {
+template <class KeyT>
+__global__ void k_pair_keys(const int2* __restrict__ pr, int64_t n, int sbits, KeyT* __restrict__ keys) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) keys[i] = ((uint64_t)(uint32_t)pr[i].x << sbits) | (uint32_t)pr[i].y;
+  if (i < n) keys[i] = static_cast<KeyT>(((uint64_t)(uint32_t)pr[i].x << sbits) | (uint32_t)pr[i].y);
 }
 
 // CSR from sorted (target, source) keys: sources, and offsets (targets tp+1..t start at i)
-__global__ void k_csr_from_keys(const uint64_t* __restrict__ keys, int64_t n, int sbits, int64_t ncells,
+template <class KeyT>
+__global__ void k_csr_from_keys(const KeyT* __restrict__ keys, int64_t n, int sbits, int64_t ncells,
                                 int64_t* __restrict__ off, int32_t* __restrict__ src) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i > n) return;
@@ -116,19 +133,6 @@ __global__ void k_csr_from_keys(const uint64_t* __restrict__ keys, int64_t n, in
   const int64_t tp = i > 0 ? (int64_t)(keys[i - 1] >> sbits) : -1;
   if (i < n) src[i] = (int32_t)(keys[i] & mask);
   for (int64_t c = tp + 1; c <= t; ++c) off[c] = i;
-}
-
-__global__ void k_p2p_body_pairs(const int64_t* __restrict__ off, const int32_t* __restrict__ src,
-                                 int64_t ncells, const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
-                                 unsigned long long* __restrict__ total) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  unsigned long long v = 0;
-  if (t < ncells) {
-    const int64_t nt = be[t] - bb[t];
-    for (int64_t k = off[t]; k < off[t + 1]; ++k) v += (unsigned long long)(nt * (be[src[k]] - bb[src[k]]));
-  }
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0 && v) atomicAdd(total, v);
 }
 
 __global__ void k_flag_nonempty(const int64_t* __restrict__ off, int64_t ncells, int32_t* __restrict__ flag) {
@@ -157,7 +161,11 @@ void grow_keep(fmm_ctx* c, DBuf<T>& buf, size_t used, size_t need) {
 
 // Sorts packed (target, source) keys (2 * ceil(log2 ncells) bits) and splits them into CSR by
 // target with ascending sources: the canonical form of the emitted multiset.
-void keys_to_csr(fmm_ctx* c, uint64_t* keys, int64_t n, DBuf<int64_t>& off, DBuf<int32_t>& src) {
+// Keys are 32-bit when 2 * ceil(log2 ncells) <= 32 (half the sort traffic), else 64-bit.
+inline bool small_keys(int64_t ncells) { return 2 * bits_for(static_cast<uint64_t>(ncells)) <= 32; }
+
+template <class KeyT>
+void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int32_t>& src) {
   cudaStream_t s = c->stream;
   const int64_t nc = c->ncells;
   off.ensure(nc + 1);
@@ -167,7 +175,7 @@ void keys_to_csr(fmm_ctx* c, uint64_t* keys, int64_t n, DBuf<int64_t>& off, DBuf
     return;
   }
   const int sbits = bits_for(static_cast<uint64_t>(nc));
-  uint64_t* kb = c->keys_b.ensure(n);
+  KeyT* kb = reinterpret_cast<KeyT*>(c->keys_b.ensure(n));
   size_t sb = 0;
   CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys, kb, (int)n, 0, 2 * sbits, s));
   CK(cub::DeviceRadixSort::SortKeys(temp_storage(c, sb), sb, keys, kb, (int)n, 0, 2 * sbits, s));
@@ -182,23 +190,29 @@ void lists_from_pairs(fmm_ctx* c, const int2* d_m2l, int64_t n_m2l, const int2* 
   const int sbits = bits_for(static_cast<uint64_t>(c->ncells));
   uint64_t* mk = c->m2l_keys.ensure(n_m2l + 1);
   uint64_t* pk = c->p2p_keys.ensure(n_p2p + 1);
-  if (n_m2l) k_pair_keys<<<ceil_div(n_m2l, 256), 256, 0, c->stream>>>(d_m2l, n_m2l, sbits, mk);
-  if (n_p2p) k_pair_keys<<<ceil_div(n_p2p, 256), 256, 0, c->stream>>>(d_p2p, n_p2p, sbits, pk);
+  if (small_keys(c->ncells)) {
+    if (n_m2l) k_pair_keys<<<ceil_div(n_m2l, 256), 256, 0, c->stream>>>(d_m2l, n_m2l, sbits, (uint32_t*)mk);
+    if (n_p2p) k_pair_keys<<<ceil_div(n_p2p, 256), 256, 0, c->stream>>>(d_p2p, n_p2p, sbits, (uint32_t*)pk);
+  } else {
+    if (n_m2l) k_pair_keys<<<ceil_div(n_m2l, 256), 256, 0, c->stream>>>(d_m2l, n_m2l, sbits, mk);
+    if (n_p2p) k_pair_keys<<<ceil_div(n_p2p, 256), 256, 0, c->stream>>>(d_p2p, n_p2p, sbits, pk);
+  }
   CK_LAUNCH("k_pair_keys");
   finish_lists(c, n_m2l, n_p2p);
 }
 
 void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
   cudaStream_t s = c->stream;
-  keys_to_csr(c, c->m2l_keys.p, n_m2l, c->m2l_off, c->m2l_src);
-  keys_to_csr(c, c->p2p_keys.p, n_p2p, c->p2p_off, c->p2p_src);
+  if (small_keys(c->ncells)) {
+    keys_to_csr(c, reinterpret_cast<uint32_t*>(c->m2l_keys.p), n_m2l, c->m2l_off, c->m2l_src);
+    keys_to_csr(c, reinterpret_cast<uint32_t*>(c->p2p_keys.p), n_p2p, c->p2p_off, c->p2p_src);
+  } else {
+    keys_to_csr(c, c->m2l_keys.p, n_m2l, c->m2l_off, c->m2l_src);
+    keys_to_csr(c, c->p2p_keys.p, n_p2p, c->p2p_off, c->p2p_src);
+  }
   c->n_m2l = n_m2l;
   c->n_p2p = n_p2p;
-  // body-pair count (P2P work) and the M2L target list
-  unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->d_counters.ensure(4));
-  CK(cudaMemsetAsync(tot, 0, sizeof(unsigned long long), s));
-  k_p2p_body_pairs<<<ceil_div(c->ncells, 256), 256, 0, s>>>(c->p2p_off.p, c->p2p_src.p, c->ncells,
-                                                            c->c_body_begin.p, c->c_body_end.p, tot);
+  // the M2L target list (cells with a non-empty list)
   int32_t* flag = c->i32_c.ensure(c->ncells);
   k_flag_nonempty<<<ceil_div(c->ncells, 256), 256, 0, s>>>(c->m2l_off.p, c->ncells, flag);
   CK_LAUNCH("k_flag_nonempty");
@@ -209,10 +223,9 @@ void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
   CK(cub::DeviceSelect::Flagged(nullptr, sb, it, flag, targets, nsel, (int)c->ncells, s));
   CK(cub::DeviceSelect::Flagged(temp_storage(c, sb), sb, it, flag, targets, nsel, (int)c->ncells, s));
   int64_t* h = c->hpin;
-  CK(cudaMemcpyAsync(h, c->d_counters.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  c->p2p_body_pairs = h[0];
-  c->n_m2l_targets = h[1];
+  c->n_m2l_targets = h[0];
   c->kernel_launches += 3;
   c->have_lists = true;
   build_p2p_worklist(c);
@@ -226,6 +239,7 @@ void traverse(fmm_ctx* c) {
   const int mutual = c->cfg.mutual ? 1 : 0;
   const int fan = mutual ? 36 : 8;  // max pairs pushed per pair
   const int sbits = bits_for(static_cast<uint64_t>(c->ncells));
+  const bool small = small_keys(c->ncells);
 
   int64_t nf = 1, nm = 0, np = 0;
   const int2 root = make_int2(0, 0);
@@ -244,8 +258,13 @@ void traverse(fmm_ctx* c) {
     h[1] = np;
     h[2] = 0;
     CK(cudaMemcpyAsync(ctr, h, 3 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
-    k_step<<<ceil_div(nf, 256), 256, 0, s>>>(fa->p, nf, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
-                                             mutual, sbits, c->m2l_keys.p, c->p2p_keys.p, fb->p, ctr);
+    if (small)
+      k_step<<<ceil_div(nf, 256), 256, 0, s>>>(fa->p, nf, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
+                                               theta * theta, mutual, sbits, (uint32_t*)c->m2l_keys.p,
+                                               (uint32_t*)c->p2p_keys.p, fb->p, ctr);
+    else
+      k_step<<<ceil_div(nf, 256), 256, 0, s>>>(fa->p, nf, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
+                                               theta * theta, mutual, sbits, c->m2l_keys.p, c->p2p_keys.p, fb->p, ctr);
     CK_LAUNCH("k_step");
     CK(cudaMemcpyAsync(h + 4, ctr, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
