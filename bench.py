@@ -69,7 +69,7 @@ class ClockSampler:
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
         except Exception:
@@ -161,14 +161,15 @@ def cpu_reference_sample(gen, n_full, p, n_crit, theta, n_sample, steps=1, warmu
             "sample": f"N={n} bodies of the same distribution (p={p}, n_crit={n_crit}, theta={theta}), "
                       f"reference scheduler with {threads} workers + master, {len(times)} step(s), "
                       f"{inter} interactions/step",
-            "config": {"workload": f"reference CPU FMM sample N={n}", "n_bodies": n, "order": p,
-                       "n_crit": n_crit, "theta": theta}}
+            "config": {"workload": f"C{gen}: same distribution/p/n_crit/theta as the GPU arm; reference CPU "
+                                   f"FMM timed on a bounded N={n} sample (interactions/s)",
+                       "n_bodies": n, "order": p, "n_crit": n_crit, "theta": theta}}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C2", choices=list(CONFIGS))

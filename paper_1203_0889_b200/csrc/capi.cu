@@ -272,20 +272,14 @@ int fmm_get_results(fmm_ctx* c, double* phi, double* acc, int order) {
       CK(cudaStreamSynchronize(c->stream));
       return;
     }
-    std::vector<double> p(n), a(acc ? 3 * n : 0);
-    std::vector<int32_t> perm(n);
-    CK(cudaMemcpyAsync(p.data(), c->phi.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(perm.data(), c->perm.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
-    if (acc) {
-      if (!c->cfg.with_acc) fail(FMM_ERR_STATE, "acceleration was not requested (with_acc = 0)");
-      CK(cudaMemcpyAsync(a.data(), c->acc.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    }
+    // input order: scatter through the permutation on the device, then one copy each
+    double* dphi = c->phi_in.ensure(n);
+    double* dacc = acc ? c->acc_in.ensure(3 * n) : nullptr;
+    if (acc && !c->cfg.with_acc) fail(FMM_ERR_STATE, "acceleration was not requested (with_acc = 0)");
+    fmmb::unpermute_results(c, dphi, dacc);
+    if (phi) CK(cudaMemcpyAsync(phi, dphi, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (acc) CK(cudaMemcpyAsync(acc, dacc, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    for (int64_t i = 0; i < n; ++i) {
-      if (phi) phi[perm[i]] = p[i];
-      if (acc)
-        for (int d = 0; d < 3; ++d) acc[3 * (int64_t)perm[i] + d] = a[3 * i + d];
-    }
   });
 }
 

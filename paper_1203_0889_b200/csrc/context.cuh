@@ -65,6 +65,7 @@ struct fmm_ctx {
   fmmb::DBuf<double> M, L;
   fmmb::DBuf<double> phi, acc;
   fmmb::DBuf<double> phi_p2p, acc_p2p;  // near-field part (tree order)
+  fmmb::DBuf<double> phi_in, acc_in;    // outputs scattered back to input order
 
   // scratch
   fmmb::DBuf<unsigned char> tmp;
@@ -94,6 +95,7 @@ namespace fmmb {
 
 // tree_build.cu
 void build_tree(fmm_ctx* c);
+void unpermute_results(fmm_ctx* c, double* phi_in, double* acc_in);  // tree -> input order
 void gather_bodies(fmm_ctx* c);  // bodies/bodyf/leaf_of_body from perm + tree
 // traverse.cu
 void traverse(fmm_ctx* c);

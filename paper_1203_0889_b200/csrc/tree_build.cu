@@ -425,6 +425,26 @@ void build_tree(fmm_ctx* c) {
   c->kernel_launches += 1;
 }
 
+namespace {
+__global__ void k_unpermute(const int32_t* __restrict__ perm, int64_t n, const double* __restrict__ phi,
+                            const double* __restrict__ acc, double* __restrict__ phi_in, double* __restrict__ acc_in) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t j = perm[i];
+  phi_in[j] = phi[i];
+  if (acc_in) {
+    acc_in[3 * j] = acc[3 * i];
+    acc_in[3 * j + 1] = acc[3 * i + 1];
+    acc_in[3 * j + 2] = acc[3 * i + 2];
+  }
+}
+}  // namespace
+
+void unpermute_results(fmm_ctx* c, double* phi_in, double* acc_in) {
+  k_unpermute<<<ceil_div(c->N, 256), 256, 0, c->stream>>>(c->perm.p, c->N, c->phi.p, c->acc.p, phi_in, acc_in);
+  CK_LAUNCH("k_unpermute");
+}
+
 void gather_bodies(fmm_ctx* c) {
   cudaStream_t s = c->stream;
   const int64_t n = c->N;
