@@ -1,85 +1,74 @@
 // m2l.cu — the FP64 M2L kernel (reference: m2l, kernels.cpp:98-111, applied over the M2L list
 // by KernelVisitor::m2l_pair, traversal.hpp:143-152). See expansions.cu for the conventions.
+#include <algorithm>
+
 #include "expansions.cuh"
 
 namespace fmmb {
 namespace {
 
-// ------------------------------------------------------------------------------ M2L ----
+// --------------------------------------------------------------- shared-memory M2L (p >= 7) ----
+// Lane = source, warp = target (grid-stride over targets; a fixed pool of warps). The lane's
+// Dt row (N doubles) lives in shared memory (odd stride: conflict-free), its source multipole is
+// read through L1, and the per-lane partial Lambda is accumulated in register blocks of kBlk
+// coefficients that round-trip through an L2-resident scratch row per (warp slot, lane). The
+// 32 partial rows are reduced once per target. Shared-memory bound (~1 LDS per term): the
+// register kernel below covers p <= 6.
 template <int P>
-struct M2LCfg {
+struct BigCfg {
   static constexpr int N = MI<P>::N;
   static constexpr int S = odd_stride(N);
-  static constexpr int kWarps = (P <= 6) ? 4 : 2;
-  // Lambda in registers when it fits; otherwise blocks of kBlk coefficients in shared memory
-  static constexpr bool kRegs = N <= 56;
-  static constexpr int kBlk = kRegs ? N : 40;
+  static constexpr int kWarps = 4;
+  static constexpr int kBlk = 32;
+  static constexpr int kBlocks = (N + kBlk - 1) / kBlk;
 };
 
 template <int P>
-__global__ void __launch_bounds__(32 * M2LCfg<P>::kWarps)
-k_m2l(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* __restrict__ off,
-      const int32_t* __restrict__ src, const double4* __restrict__ cr, const double* __restrict__ M,
-      double* __restrict__ L) {
+__global__ void __launch_bounds__(32 * BigCfg<P>::kWarps)
+k_m2l_big(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* __restrict__ off,
+          const int32_t* __restrict__ src, const double4* __restrict__ cr, const double* __restrict__ M,
+          const double* __restrict__ zero_row, double* __restrict__ L, double* __restrict__ scratch) {
   using T = MI<P>;
-  using C = M2LCfg<P>;
+  using C = BigCfg<P>;
   constexpr int N = C::N, S = C::S;
   extern __shared__ double smem[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* sD = smem + (size_t)w * 32 * S * (C::kRegs ? 1 : 2);  // Dt rows (+ Lambda rows)
-  double* myD = sD + lane * S;
-  double* myLam = sD + 32 * S + lane * S;  // only when !kRegs
-  const int64_t wid = blockIdx.x * (int64_t)C::kWarps + w;
-  if (wid >= ntargets) return;
-  const int32_t t = targets[wid];
-  const double4 ct = cr[t];
-  const int64_t l0 = off[t], l1 = off[t + 1];
-
-  double lam[C::kBlk];
-  if constexpr (C::kRegs) {
-#pragma unroll
-    for (int i = 0; i < N; ++i) lam[i] = 0.0;
-  } else {
-    for (int i = 0; i < N; ++i) myLam[i] = 0.0;
-  }
-  for (int64_t base = l0; base < l1; base += 32) {
-    const int64_t k = base + lane;
-    const bool valid = k < l1;
-    const int32_t s = valid ? src[k] : t;
-    double rx = 1.0, ry = 0.0, rz = 0.0;
-    if (valid) {
-      const double4 cs = cr[s];
-      rx = cs.x - ct.x;  // R = source centre - target centre (traversal.hpp:146)
-      ry = cs.y - ct.y;
-      rz = cs.z - ct.z;
-    }
-    derivs_row<P, true>(rx, ry, rz, myD);
-    const double* Ms = M + (int64_t)s * N;
-    const double mscale = valid ? 1.0 : 0.0;
-    if constexpr (C::kRegs) {
-      static_for<N>([&](auto IA) {
-        constexpr int ia = decltype(IA)::value;
-        constexpr int aa = T::ea(ia), ab = T::eb(ia), ac = T::ec(ia), da = T::deg(ia);
-        const double m = __ldg(Ms + ia) * mscale;
-        static_for<N>([&](auto IB) {
-          constexpr int ib = decltype(IB)::value;
-          if constexpr (da + T::deg(ib) <= P - 1) {
-            constexpr int ig = index_of(aa + T::ea(ib), ab + T::eb(ib), ac + T::ec(ib));
-            lam[ib] = fma(m, myD[ig], lam[ib]);
-          }
-        });
-      });
-    } else {
-      // beta blocks of kBlk coefficients; Lambda block round-trips through shared memory
-      static_for<(N + C::kBlk - 1) / C::kBlk>([&](auto BI) {
+  double* myD = smem + (size_t)w * 32 * S + lane * S;
+  const int64_t slot = blockIdx.x * (int64_t)C::kWarps + w;
+  const int64_t nslots = (int64_t)gridDim.x * C::kWarps;
+  double* part = scratch + (slot * 32 + lane) * (int64_t)N;  // this lane's partial Lambda row
+  double* rows = scratch + slot * 32 * (int64_t)N;           // the warp's 32 rows
+  for (int64_t wid = slot; wid < ntargets; wid += nslots) {
+    const int32_t t = targets[wid];
+    const double4 ct = cr[t];
+    const int64_t l0 = off[t], l1 = off[t + 1];
+    for (int i = 0; i < N; ++i) part[i] = 0.0;
+    for (int64_t base = l0; base < l1; base += 32) {
+      const int64_t k = base + lane;
+      const bool valid = k < l1;
+      const int32_t s = valid ? src[k] : t;
+      double rx = 1.0, ry = 0.0, rz = 0.0;
+      if (valid) {
+        const double4 cs = cr[s];
+        rx = cs.x - ct.x;  // R = source centre - target centre (traversal.hpp:146)
+        ry = cs.y - ct.y;
+        rz = cs.z - ct.z;
+      }
+      derivs_row<P, true>(rx, ry, rz, myD);
+      const double* Ms = valid ? M + (int64_t)s * N : zero_row;
+      static_for<C::kBlocks>([&](auto BI) {
         constexpr int b0 = decltype(BI)::value * C::kBlk;
         constexpr int b1 = (b0 + C::kBlk < N) ? b0 + C::kBlk : N;
-        static_for<b1 - b0>([&](auto J) { lam[decltype(J)::value] = myLam[b0 + decltype(J)::value]; });
+        double lam[b1 - b0];
+#pragma unroll
+        for (int j = 0; j < b1 - b0; ++j) lam[j] = part[b0 + j];
         static_for<N>([&](auto IA) {
           constexpr int ia = decltype(IA)::value;
           constexpr int aa = T::ea(ia), ab = T::eb(ia), ac = T::ec(ia), da = T::deg(ia);
           if constexpr (da + T::deg(b0) <= P - 1) {
-            const double m = __ldg(Ms + ia) * mscale;
+            // keep the multipole loads from being hoisted en masse (register pressure)
+            if constexpr (ia % 8 == 0) __syncwarp();
+            const double m = __ldg(Ms + ia);
             static_for<b1 - b0>([&](auto J) {
               constexpr int ib = b0 + decltype(J)::value;
               if constexpr (da + T::deg(ib) <= P - 1) {
@@ -89,35 +78,27 @@ k_m2l(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* __re
             });
           }
         });
-        static_for<b1 - b0>([&](auto J) { myLam[b0 + decltype(J)::value] = lam[decltype(J)::value]; });
+#pragma unroll
+        for (int j = 0; j < b1 - b0; ++j) part[b0 + j] = lam[j];
       });
     }
-  }
-  // warp reduction of the per-lane partials, then L_b += (-1)^{|b|}/b! * Lambda_b
-  __syncwarp();
-  if constexpr (C::kRegs) {
-#pragma unroll
-    for (int i = 0; i < N; ++i) myD[i] = lam[i];
-  } else {
-    for (int i = 0; i < N; ++i) myD[i] = myLam[i];
-  }
-  __syncwarp();
-  double* Lt = L + (int64_t)t * N;
-  for (int i = lane; i < N; i += 32) {
-    double s = 0.0;
-    for (int j = 0; j < 32; ++j) s += sD[j * S + i];
-    int n = 0;
-    while (n_coef(n + 1) <= i) ++n;
-    // 1/b! for coefficient i
-    int r = i - n_coef(n), a = 0;
-    while (r >= n - a + 1) { r -= n - a + 1; ++a; }
-    const int bexp = r, cexp = n - a - r;
-    double f = 1.0;
-    for (int q = 2; q <= a; ++q) f *= q;
-    for (int q = 2; q <= bexp; ++q) f *= q;
-    for (int q = 2; q <= cexp; ++q) f *= q;
-    const double sgn = (n & 1) ? -1.0 : 1.0;
-    Lt[i] += sgn * s / f;
+    __syncwarp();
+    double* Lt = L + (int64_t)t * N;
+    for (int i = lane; i < N; i += 32) {
+      double acc = 0.0;
+      for (int j = 0; j < 32; ++j) acc += rows[(int64_t)j * N + i];
+      int n = 0;
+      while (n_coef(n + 1) <= i) ++n;
+      int r = i - n_coef(n), a = 0;
+      while (r >= n - a + 1) { r -= n - a + 1; ++a; }
+      const int bexp = r, cexp = n - a - r;
+      double f = 1.0;
+      for (int q = 2; q <= a; ++q) f *= q;
+      for (int q = 2; q <= bexp; ++q) f *= q;
+      for (int q = 2; q <= cexp; ++q) f *= q;
+      Lt[i] += ((n & 1) ? -acc : acc) / f;
+    }
+    __syncwarp();
   }
 }
 
@@ -283,18 +264,28 @@ struct M2L {
       c->kernel_launches += 1;
       return;
     }
-    using C = M2LCfg<P>;
-    const size_t smem = sizeof(double) * C::kWarps * 32 * C::S * (C::kRegs ? 1 : 2);
+    using C = BigCfg<P>;
+    const size_t smem = sizeof(double) * C::kWarps * 32 * C::S;
     static bool attr_set = false;
     if (!attr_set) {
-      CK(cudaFuncSetAttribute(k_m2l<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CK(cudaFuncSetAttribute(k_m2l_big<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attr_set = true;
     }
     if (c->n_m2l_targets == 0) return;
-    k_m2l<P><<<ceil_div(c->n_m2l_targets, C::kWarps), 32 * C::kWarps, smem, s>>>(
-        c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p, c->m2l_src.p, c->c_cr.p, c->M.p, c->L.p);
-    CK_LAUNCH("k_m2l");
-    c->kernel_launches += 1;
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_big<P>, 32 * C::kWarps, smem));
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->cfg.device));
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(per_sm, 1),
+                                                               (c->n_m2l_targets + C::kWarps - 1) / C::kWarps));
+    double* scratch = c->m2l_scratch.ensure((size_t)grid * C::kWarps * 32 * C::N + C::N);
+    double* zero_row = scratch + (size_t)grid * C::kWarps * 32 * C::N;
+    CK(cudaMemsetAsync(zero_row, 0, sizeof(double) * C::N, s));
+    k_m2l_big<P><<<(unsigned)grid, 32 * C::kWarps, smem, s>>>(c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p,
+                                                              c->m2l_src.p, c->c_cr.p, c->M.p, zero_row, c->L.p,
+                                                              scratch);
+    CK_LAUNCH("k_m2l_big");
+    c->kernel_launches += 2;
   }
 };
 
