@@ -166,6 +166,35 @@ int fmm_op_morton_key(int64_t count, const double* p3, const double* center3,
 int fmm_op_mac(int64_t count, const double* tcenter3, const double* tradius,
                const double* scenter3, const double* sradius, double theta, int32_t* out);
 
+/* ---- multi-GPU sharding ----------------------------------------------
+ * One process per GPU, every rank holds all bodies. After fmm_set_partition(rank, world) the
+ * traversal also splits the target leaves into `world` contiguous body (Morton) ranges balanced
+ * by cost, and a sharded step is:
+ *   fmm_build_tree; fmm_traverse; fmm_upward_local(send);
+ *   <all-gather: recv[world * chunk] <- send[chunk]  (NCCL, caller side; chunk = shard.chunk_doubles)>
+ *   fmm_upward_finish(recv); fmm_m2l; fmm_p2p; fmm_downward;
+ * after which the potentials/accelerations of bodies [shard.body_begin, shard.body_end) (tree
+ * order) are final on this rank. send/recv are device pointers on the context's device. */
+typedef struct {
+  int32_t rank, world;
+  int64_t body_begin, body_end;   /* own bodies, tree order */
+  int64_t own_leaves, own_cells;  /* leaves / cells whose multipoles this rank computes */
+  int64_t chunk_doubles;          /* all-gather chunk per rank (doubles) */
+} fmm_shard_info;
+
+int fmm_set_partition(fmm_ctx* ctx, int rank, int world);
+int fmm_get_shard_info(fmm_ctx* ctx, fmm_shard_info* info);
+int fmm_upward_local(fmm_ctx* ctx, double* d_send);
+int fmm_upward_finish(fmm_ctx* ctx, const double* d_recv);
+/* Run subsequent stages on `stream` (a cudaStream_t; NULL restores the context's own stream),
+ * e.g. the stream an NCCL collective is issued on. */
+int fmm_set_stream(fmm_ctx* ctx, void* stream);
+/* Host-only (no GPU): the partition plan the traversal uses. cell_cost holds each leaf's cost
+ * (ignored for non-leaves). bounds[world+1] (body indices), owner[ncells] (rank or -1). */
+int fmm_plan_partition(int64_t ncells, const int32_t* body_begin, const int32_t* body_end,
+                       const int32_t* child_count, const double* cell_cost, int world,
+                       int64_t* bounds, int32_t* owner);
+
 /* ---- synthetic BASELINE inputs (host-side generator) ----------------- */
 /* config: 1..5 = BASELINE configs C1..C5 distributions; writes N x {x,y,z,q}. */
 int fmm_generate_bodies(int config, int64_t n, uint64_t seed, double* xyzq);

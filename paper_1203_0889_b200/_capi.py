@@ -62,6 +62,12 @@ class StageTimes(C.Structure):
                 ("m2l_launches", C.c_int32), ("kernel_launches", C.c_int32)]
 
 
+class ShardInfo(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("body_begin", C.c_int64),
+                ("body_end", C.c_int64), ("own_leaves", C.c_int64), ("own_cells", C.c_int64),
+                ("chunk_doubles", C.c_int64)]
+
+
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
 _u64p = C.POINTER(C.c_uint64)
@@ -109,6 +115,12 @@ SIGNATURES = {
     "fmm_op_morton_key": (C.c_int, [C.c_int64, _dp, _dp, C.c_double, C.c_int, _u64p]),
     "fmm_op_mac": (C.c_int, [C.c_int64, _dp, _dp, _dp, _dp, C.c_double, _i32p]),
     "fmm_generate_bodies": (C.c_int, [C.c_int, C.c_int64, C.c_uint64, _dp]),
+    "fmm_set_partition": (C.c_int, [_vp, C.c_int, C.c_int]),
+    "fmm_get_shard_info": (C.c_int, [_vp, C.POINTER(ShardInfo)]),
+    "fmm_upward_local": (C.c_int, [_vp, _vp]),
+    "fmm_upward_finish": (C.c_int, [_vp, _vp]),
+    "fmm_set_stream": (C.c_int, [_vp, _vp]),
+    "fmm_plan_partition": (C.c_int, [C.c_int64, _i32p, _i32p, _i32p, _dp, C.c_int, _i64p, _i32p]),
 }
 
 _lib = None

@@ -116,6 +116,7 @@ void fmm_destroy(fmm_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  if (ctx->own_stream) ctx->stream = ctx->own_stream;
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
   if (ctx->hpin) cudaFreeHost(ctx->hpin);
@@ -216,6 +217,7 @@ int fmm_downward(fmm_ctx* c) {
 int fmm_evaluate(fmm_ctx* c) {
   if (!c) return FMM_ERR_ARG;
   return guard(c, [&] {
+    if (c->world > 1) fail(FMM_ERR_STATE, "evaluate: sharded contexts run the staged sequence (see fmm_b200.h)");
     set_device(c);
     c->kernel_launches = 0;
     CK(cudaEventRecord(c->ev[EV_BUILD0], c->stream));
@@ -441,6 +443,9 @@ int fmm_load_tree(fmm_ctx* c, int64_t ncells, const int32_t* level, const uint64
     up(c->perm.ensure(c->N), p32.data(), c->N * 4);
     c->ncells = ncells;
     c->nleaves = static_cast<int64_t>(leaves.size());
+    c->wl = c->leaves.p;
+    c->nwl = c->nleaves;
+    c->shard_planned = false;
     c->depth = depth;
     c->center[0] = center3[0];
     c->center[1] = center3[1];
@@ -491,6 +496,75 @@ int fmm_reset_accumulators(fmm_ctx* c) {
     CK(cudaMemsetAsync(c->acc_p2p.ensure(3 * c->N), 0, 3 * c->N * sizeof(double), c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->have_L = true;
+  });
+}
+
+// ---------------------------------------------------------------------- sharding -------
+int fmm_set_partition(fmm_ctx* c, int rank, int world) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (world < 1 || rank < 0 || rank >= world) fail(FMM_ERR_ARG, "bad rank/world");
+    c->rank = rank;
+    c->world = world;
+    c->shard_planned = false;
+    c->have_lists = c->have_M = c->have_L = c->have_out = false;
+  });
+}
+
+int fmm_get_shard_info(fmm_ctx* c, fmm_shard_info* info) {
+  if (!c || !info) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_lists) fail(FMM_ERR_STATE, "shard info: run the traversal first");
+    info->rank = c->rank;
+    info->world = c->world;
+    info->body_begin = c->shard_b0;
+    info->body_end = c->shard_b1;
+    info->own_leaves = c->nwl;
+    info->own_cells = c->world > 1 ? c->rank_cells_off[c->rank + 1] - c->rank_cells_off[c->rank] : c->ncells;
+    info->chunk_doubles = c->world > 1 ? c->chunk_cells * c->ncoef : 0;
+  });
+}
+
+int fmm_upward_local(fmm_ctx* c, double* d_send) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (c->world == 1) fail(FMM_ERR_STATE, "upward_local: no partition (use fmm_upward)");
+    if (!c->shard_planned) fail(FMM_ERR_STATE, "upward_local: run the traversal first");
+    set_device(c);
+    CK(cudaMemsetAsync(c->M.ensure((size_t)c->ncells * c->ncoef), 0, sizeof(double) * c->ncells * c->ncoef,
+                       c->stream));
+    fmmb::run_upward(c, c->stream, 1);
+    fmmb::shard_pack(c, d_send, c->stream);
+  });
+}
+
+int fmm_upward_finish(fmm_ctx* c, const double* d_recv) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (c->world == 1 || !c->shard_planned) fail(FMM_ERR_STATE, "upward_finish: no sharded upward pass");
+    set_device(c);
+    fmmb::shard_unpack(c, d_recv, c->stream);
+    fmmb::run_upward(c, c->stream, 2);
+    c->have_M = true;
+  });
+}
+
+int fmm_set_stream(fmm_ctx* c, void* stream) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    set_device(c);
+    if (!c->own_stream) c->own_stream = c->stream;
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+  });
+}
+
+int fmm_plan_partition(int64_t ncells, const int32_t* body_begin, const int32_t* body_end,
+                       const int32_t* child_count, const double* cell_cost, int world, int64_t* bounds,
+                       int32_t* owner) {
+  return guard(nullptr, [&] {
+    if (ncells <= 0 || world < 1 || !body_begin || !body_end || !child_count || !cell_cost || !bounds || !owner)
+      fail(FMM_ERR_ARG, "bad partition arguments");
+    fmmb::plan_partition_host(ncells, body_begin, body_end, child_count, cell_cost, world, bounds, owner);
   });
 }
 

@@ -25,6 +25,7 @@ struct fmm_ctx {
   int ncoef = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t stream2 = nullptr;  // concurrent stream (P2P alongside the expansion chain)
+  cudaStream_t own_stream = nullptr;  // the context's stream while a caller stream is set
   std::string err;
 
   // bodies
@@ -82,6 +83,18 @@ struct fmm_ctx {
   fmmb::DBuf<int32_t> bnd;           // child boundaries of one level (9 per cell)
   int64_t* hpin = nullptr;           // pinned host scratch (64 x int64)
 
+  // sharding: target leaves split by contiguous body (Morton) range
+  int rank = 0, world = 1;
+  int64_t shard_b0 = 0, shard_b1 = 0;      // own body range [b0, b1) in tree order
+  const int32_t* wl = nullptr;             // work leaves: all leaves, or the rank's own leaves
+  int64_t nwl = 0;
+  fmmb::DBuf<int32_t> own_leaves;
+  fmmb::DBuf<int32_t> owner;               // per cell: owning rank, -1 = straddles ranks
+  fmmb::DBuf<int32_t> rank_cells;          // cells owned by each rank, concatenated
+  std::vector<int64_t> rank_cells_off;     // world + 1 offsets into rank_cells
+  int64_t chunk_cells = 0;                 // max cells owned by a rank (exchange chunk)
+  bool shard_planned = false;
+
   // state
   bool have_bodies = false, have_tree = false, have_lists = false, have_M = false,
        have_L = false, have_out = false;
@@ -103,11 +116,17 @@ void traverse(fmm_ctx* c);
 void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p);  // lists from c->m2l_keys/p2p_keys
 void lists_from_pairs(fmm_ctx* c, const int2* d_m2l, int64_t n_m2l, const int2* d_p2p,
                       int64_t n_p2p);
+// shard.cu
+void plan_shards(fmm_ctx* c);      // after the lists: partition, own leaves, owners
+void shard_pack(fmm_ctx* c, double* d_send, cudaStream_t s);
+void shard_unpack(fmm_ctx* c, const double* d_recv, cudaStream_t s);
+void plan_partition_host(int64_t ncells, const int32_t* bb, const int32_t* be, const int32_t* cc,
+                         const double* cell_cost, int world, int64_t* bounds, int32_t* owner);
 // p2p.cu
 void build_p2p_worklist(fmm_ctx* c);
 void run_p2p(fmm_ctx* c, cudaStream_t s);
 // expansions.cu
-void run_upward(fmm_ctx* c, cudaStream_t s);
+void run_upward(fmm_ctx* c, cudaStream_t s, int mode = 0);  // 0 all, 1 own cells, 2 shared cells
 void run_m2l(fmm_ctx* c, cudaStream_t s);
 void run_downward(fmm_ctx* c, cudaStream_t s);  // L2L + L2P + combine with P2P part
 

@@ -95,7 +95,7 @@ k_p2m(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __rest
 template <int P>
 __global__ void __launch_bounds__(256)
 k_m2m(int32_t cbeg, int32_t cend, const int32_t* __restrict__ cb, const int32_t* __restrict__ cc,
-      const double4* __restrict__ cr, double* __restrict__ M) {
+      const double4* __restrict__ cr, double* __restrict__ M, const int32_t* __restrict__ owner, int32_t want) {
   using T = MI<P>;
   constexpr int N = T::N;
   __shared__ double sD[8][3 * P];
@@ -106,6 +106,7 @@ k_m2m(int32_t cbeg, int32_t cend, const int32_t* __restrict__ cb, const int32_t*
   if (ci >= cend) return;
   const int32_t nch = cc[ci];
   if (nch == 0) return;  // uniform over the CTA
+  if (owner && owner[ci] != want) return;  // sharded: only this rank's (or the shared) cells
   if (w < nch) {
     const double4 pc = cr[ci];
     const int32_t child = cb[ci] + w;
@@ -246,17 +247,23 @@ k_l2p(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __rest
 // --------------------------------------------------------------------- launchers ------
 template <int P>
 struct Upward {
-  static void run(fmm_ctx* c, cudaStream_t s) {
+  // mode 0: every cell; 1: P2P leaves + M2M of this rank's cells; 2: M2M of shared cells only
+  static void run(fmm_ctx* c, cudaStream_t s, int mode) {
     const int N = MI<P>::N;
     double* M = c->M.ensure((size_t)c->ncells * N);
-    k_p2m<P><<<ceil_div(c->nleaves, 4), 128, 0, s>>>(c->leaves.p, c->nleaves, c->c_body_begin.p, c->c_body_end.p,
-                                                     c->c_cr.p, c->bodies.p, M);
-    CK_LAUNCH("k_p2m");
-    int launches = 1;
+    int launches = 0;
+    if (mode != 2 && c->nwl > 0) {
+      k_p2m<P><<<ceil_div(c->nwl, 4), 128, 0, s>>>(c->wl, c->nwl, c->c_body_begin.p, c->c_body_end.p, c->c_cr.p,
+                                                   c->bodies.p, M);
+      CK_LAUNCH("k_p2m");
+      ++launches;
+    }
+    const int32_t* owner = mode == 0 ? nullptr : c->owner.p;
+    const int32_t want = mode == 1 ? c->rank : -1;
     for (int l = c->depth - 1; l >= 0; --l) {
       const int32_t b = c->level_start[l], e = c->level_start[l + 1];
       if (e <= b) continue;
-      k_m2m<P><<<e - b, 256, 0, s>>>(b, e, c->c_child_begin.p, c->c_child_count.p, c->c_cr.p, M);
+      k_m2m<P><<<e - b, 256, 0, s>>>(b, e, c->c_child_begin.p, c->c_child_count.p, c->c_cr.p, M, owner, want);
       CK_LAUNCH("k_m2m");
       ++launches;
     }
@@ -277,7 +284,8 @@ struct Downward {
       ++launches;
     }
     (void)N;
-    k_l2p<P><<<ceil_div(c->nleaves, 4), 128, 0, s>>>(c->leaves.p, c->nleaves, c->c_body_begin.p, c->c_body_end.p,
+    if (c->nwl > 0)
+    k_l2p<P><<<ceil_div(c->nwl, 4), 128, 0, s>>>(c->wl, c->nwl, c->c_body_begin.p, c->c_body_end.p,
                                                      c->c_cr.p, c->bodies.p, c->L.p, c->phi_p2p.p, c->acc_p2p.p,
                                                      c->phi.ensure(c->N), c->acc.ensure(3 * c->N),
                                                      c->cfg.with_acc ? 1 : 0);
@@ -288,9 +296,10 @@ struct Downward {
 
 }  // namespace
 
-void run_upward(fmm_ctx* c, cudaStream_t s) {
+void run_upward(fmm_ctx* c, cudaStream_t s, int mode) {
   if (!c->have_tree) fail(FMM_ERR_STATE, "upward: no tree");
-  dispatch_order<Upward>(c->cfg.order, c, s);
+  if (mode != 0 && !c->shard_planned) fail(FMM_ERR_STATE, "sharded upward before the partition (run traverse)");
+  dispatch_order<Upward>(c->cfg.order, c, s, mode);
   c->have_M = true;
 }
 

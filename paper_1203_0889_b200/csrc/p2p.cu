@@ -640,11 +640,11 @@ void exclusive_scan_i32(fmm_ctx* c, const int32_t* in, int32_t* out, int64_t n) 
 
 void build_p2p_worklist(fmm_ctx* c) {
   cudaStream_t s = c->stream;
-  const int64_t nl = c->nleaves;
+  const int64_t nl = c->nwl;
   int64_t* sum_ns = c->scan_a.ensure(nl + 1);
   unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->d_counters.ensure(16)) + 12;
   CK(cudaMemsetAsync(tot, 0, sizeof(unsigned long long), s));
-  k_leaf_sum<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->leaves.p, nl, c->p2p_off.p, c->p2p_src.p, c->c_body_begin.p,
+  k_leaf_sum<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->wl, nl, c->p2p_off.p, c->p2p_src.p, c->c_body_begin.p,
                                                     c->c_body_end.p, sum_ns, tot);
   CK_LAUNCH("k_leaf_sum");
   CK(cudaMemcpyAsync(c->hpin + 16, tot, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -661,7 +661,7 @@ void build_p2p_worklist(fmm_ctx* c) {
   int32_t *nitems = counts, *nred = counts + (nl + 1), *npart = counts + 2 * (nl + 1);
   int32_t *item_off = offs, *red_off = offs + (nl + 1), *part_off = offs + 2 * (nl + 1);
   CK(cudaMemsetAsync(counts, 0, sizeof(int32_t) * 3 * (nl + 1), s));
-  k_leaf_cost<<<ceil_div(nl, 256), 256, 0, s>>>(c->leaves.p, nl, c->p2p_off.p, c->c_body_begin.p, c->c_body_end.p,
+  k_leaf_cost<<<ceil_div(nl, 256), 256, 0, s>>>(c->wl, nl, c->p2p_off.p, c->c_body_begin.p, c->c_body_end.p,
                                                 cmax, sum_ns, nitems, nred, npart);
   CK_LAUNCH("k_leaf_cost");
   exclusive_scan_i32(c, nitems, item_off, nl + 1);
@@ -679,13 +679,13 @@ void build_p2p_worklist(fmm_ctx* c) {
   uint64_t* costs_sorted = c->keys_b.ensure(nitem + 1);
   int4* red = c->p2p_reduce.ensure(nr + 1);
   c->p2p_partial.ensure(4 * (np + 1));
-  k_write_items<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->leaves.p, nl, c->p2p_off.p, c->p2p_src.p, c->c_body_begin.p,
+  k_write_items<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->wl, nl, c->p2p_off.p, c->p2p_src.p, c->c_body_begin.p,
                                                        c->c_body_end.p, sum_ns, nitems, item_off, red_off, part_off,
                                                        items_raw, costs, red);
   CK_LAUNCH("k_write_items");
   if (c->cfg.precision == FMM_PREC_FP32_P2P) {
     P2PEnt* ent = reinterpret_cast<P2PEnt*>(c->p2p_ent.ensure(2 * (c->n_p2p + 1)));
-    k_p2p_entries<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->leaves.p, nl, c->p2p_off.p, c->p2p_src.p,
+    k_p2p_entries<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->wl, nl, c->p2p_off.p, c->p2p_src.p,
                                                          c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, ent);
     CK_LAUNCH("k_p2p_entries");
     c->kernel_launches += 1;

@@ -135,9 +135,11 @@ __global__ void k_csr_from_keys(const KeyT* __restrict__ keys, int64_t n, int sb
   for (int64_t c = tp + 1; c <= t; ++c) off[c] = i;
 }
 
-__global__ void k_flag_nonempty(const int64_t* __restrict__ off, int64_t ncells, int32_t* __restrict__ flag) {
+// cells with a non-empty M2L list whose body range meets [b0, b1) (the rank's targets)
+__global__ void k_flag_nonempty(const int64_t* __restrict__ off, int64_t ncells, const int32_t* __restrict__ bb,
+                                const int32_t* __restrict__ be, int64_t b0, int64_t b1, int32_t* __restrict__ flag) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < ncells) flag[i] = off[i + 1] > off[i];
+  if (i < ncells) flag[i] = off[i + 1] > off[i] && bb[i] < b1 && be[i] > b0;
 }
 
 int bits_for(uint64_t v) {
@@ -212,9 +214,16 @@ void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
   }
   c->n_m2l = n_m2l;
   c->n_p2p = n_p2p;
-  // the M2L target list (cells with a non-empty list)
+  // partition (sharded runs), then the M2L target list of this rank
+  if (c->world > 1) {
+    plan_shards(c);
+  } else {
+    c->shard_b0 = 0;
+    c->shard_b1 = c->N;
+  }
   int32_t* flag = c->i32_c.ensure(c->ncells);
-  k_flag_nonempty<<<ceil_div(c->ncells, 256), 256, 0, s>>>(c->m2l_off.p, c->ncells, flag);
+  k_flag_nonempty<<<ceil_div(c->ncells, 256), 256, 0, s>>>(c->m2l_off.p, c->ncells, c->c_body_begin.p,
+                                                           c->c_body_end.p, c->shard_b0, c->shard_b1, flag);
   CK_LAUNCH("k_flag_nonempty");
   int32_t* targets = c->m2l_targets.ensure(c->ncells);
   int64_t* nsel = c->d_counters.p + 1;

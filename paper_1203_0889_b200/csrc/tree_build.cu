@@ -393,6 +393,9 @@ void build_tree(fmm_ctx* c) {
   CK(cudaMemcpyAsync(hp, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   c->nleaves = hp[0];
+  c->wl = leaves;
+  c->nwl = c->nleaves;
+  c->shard_planned = false;
 
   // 6. within-leaf input order: rank sort per leaf; global (leaf, index) sort only when a
   //    level-21 leaf exceeds kRankMax bodies

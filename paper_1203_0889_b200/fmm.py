@@ -218,6 +218,24 @@ class Context:
         self._c(self.lib.fmm_get_expansions(self.h, _ptr(M, _dp), _ptr(L, _dp)))
         return M, L
 
+    # sharding
+    def set_partition(self, rank: int, world: int) -> None:
+        self._c(self.lib.fmm_set_partition(self.h, rank, world))
+
+    def shard_info(self) -> _capi.ShardInfo:
+        info = _capi.ShardInfo()
+        self._c(self.lib.fmm_get_shard_info(self.h, C.byref(info)))
+        return info
+
+    def upward_local(self, d_send: int) -> None:
+        self._c(self.lib.fmm_upward_local(self.h, C.c_void_p(d_send)))
+
+    def upward_finish(self, d_recv: int) -> None:
+        self._c(self.lib.fmm_upward_finish(self.h, C.c_void_p(d_recv)))
+
+    def set_stream(self, stream_handle: int) -> None:
+        self._c(self.lib.fmm_set_stream(self.h, C.c_void_p(stream_handle)))
+
     # injection
     def load_tree(self, cells: dict, perm: np.ndarray) -> None:
         g = {k: np.ascontiguousarray(v) for k, v in cells.items()}
@@ -350,6 +368,42 @@ def evaluate(bodies: np.ndarray, order: int = 6, n_crit: int = 64, theta: float 
     t = ctx.stage_times()
     ctx.close()
     return phi, acc, t
+
+
+def plan_partition(cells: dict, cell_cost: np.ndarray, world: int):
+    """Host-only partition plan (fmm_plan_partition; no GPU needed): returns (bounds[world+1],
+    owner[ncells]) — the contiguous body ranges of the ranks and each cell's owning rank (-1 when
+    the cell straddles ranks)."""
+    bb = np.ascontiguousarray(cells["body_begin"], dtype=np.int32)
+    be = np.ascontiguousarray(cells["body_end"], dtype=np.int32)
+    cc = np.ascontiguousarray(cells["child_count"], dtype=np.int32)
+    cost = np.ascontiguousarray(cell_cost, dtype=np.float64)
+    bounds = np.zeros(world + 1, np.int64)
+    owner = np.zeros(len(bb), np.int32)
+    _check(_capi.load().fmm_plan_partition(len(bb), _ptr(bb, _i32p), _ptr(be, _i32p), _ptr(cc, _i32p),
+                                           _ptr(cost, _dp), world, _ptr(bounds, _i64p), _ptr(owner, _i32p)))
+    return bounds, owner
+
+
+def sharded_step(ctx: "Context", rank: int, world: int, all_gather, alloc):
+    """One sharded FMM step on a context whose bodies are set (see fmm_b200.h):
+    build, traverse (+ partition), local upward, all-gather of the owned multipoles, shared
+    ancestors, M2L, P2P, downward. ``alloc(n)`` returns a device buffer object with ``.ptr``;
+    ``all_gather(recv, send)`` gathers the equal-size chunks of every rank (NCCL in production)."""
+    ctx.set_partition(rank, world)
+    ctx.build_tree()
+    ctx.traverse()
+    info = ctx.shard_info()
+    send = alloc(max(info.chunk_doubles, 1))
+    recv = alloc(max(info.chunk_doubles, 1) * world)
+    ctx.upward_local(send.ptr)
+    all_gather(recv, send)
+    ctx.upward_finish(recv.ptr)
+    ctx.reset_accumulators()
+    ctx.m2l()
+    ctx.p2p()
+    ctx.downward()
+    return info
 
 
 # ------------------------------------------------------------------ operators --------
