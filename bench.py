@@ -166,6 +166,80 @@ def cpu_reference_sample(gen, n_full, p, n_crit, theta, n_sample, steps=1, warmu
                        "n_bodies": n, "order": p, "n_crit": n_crit, "theta": theta}}
 
 
+def run_sharded(args, fb, torch, world, rank, local):
+    """torchrun, one rank per GPU: weak scaling, N = 2^20 * world bodies of the config's
+    distribution held by every rank; target leaves sharded by cost-balanced Morton range; the
+    owned multipoles all-gathered with NCCL over NVLink (the step's only data-path exchange)."""
+    import torch.distributed as dist
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    gen, n1, p, n_crit, theta = CONFIGS[args.config]
+    n = n1 * world
+    bodies = fb.generate_bodies(gen, n, 1)
+    ctx = fb.Context(order=p, n_crit=n_crit, theta=theta, precision=args.precision, device=local, with_acc=True)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)  # NCCL and the FMM kernels share one stream
+    d_bodies = torch.from_numpy(bodies).cuda()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    class Buf:
+        def __init__(self, k):
+            self.t = torch.empty(int(k), dtype=torch.float64, device="cuda")
+            self.ptr = self.t.data_ptr()
+
+    def all_gather(recv, send):
+        dist.all_gather_into_tensor(recv.t, send.t)
+
+    def step():
+        ctx.set_bodies_device(d_bodies.data_ptr(), n)
+        return fb.fmm.sharded_step(ctx, rank, world, all_gather, Buf)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    launches = 0
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            info = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            launches += ctx.stage_times().kernel_launches
+    torch.cuda.synchronize()
+    dist.barrier()
+    total = torch.tensor([float(np.sum(times))], device="cuda")
+    dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    ms_per_step = total.item() / args.steps
+    tinfo = ctx.tree_info()
+    own_p2p = torch.tensor([float(tinfo.p2p_body_pairs)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(own_p2p)
+    inter = int(own_p2p.item()) + int(tinfo.n_m2l)
+    if rank == 0:
+        line = {"metric": METRIC, "value": inter / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32 P2P / f64 expansions" if args.precision == "fp32" else "f64",
+                "data": "synthetic (BASELINE generator, seed 1)",
+                "config": {"workload": f"{args.config} distribution, N={n} (2^20 per GPU), p={p}, n_crit={n_crit}, "
+                                       f"theta={theta}, potential+acceleration",
+                           "n_bodies": n, "order": p, "n_crit": n_crit, "theta": theta, "precision": args.precision,
+                           "parallelism": f"dp{world}: target leaves sharded by cost-balanced Morton range, "
+                                          "NCCL all-gather of owned multipoles",
+                           "l2": "flushed (256 MB write) between steps"},
+                "interactions_per_step": inter, "e2e": None, "cpu_baseline": None, "clocks": clk.summary(),
+                "gpu_launches": launches, "own_body_range_rank0": [int(info.body_begin), int(info.body_end)]}
+        print(json.dumps(line))
+    ctx.close()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -190,13 +264,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dist = None
     if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return run_sharded(args, fb, torch, world, rank, local)
+    dist = None
 
     gen, n, p, n_crit, theta = CONFIGS[args.config]
-    bodies = fb.generate_bodies(gen, n, 1 + rank)
+    bodies = fb.generate_bodies(gen, n, 1)
     ctx = fb.Context(order=p, n_crit=n_crit, theta=theta, precision=args.precision, device=local,
                      with_acc=True)
     d_bodies = torch.from_numpy(bodies).cuda()

@@ -130,6 +130,7 @@ int fmm_set_bodies(fmm_ctx* c, const double* xyzq, int64_t n) {
     if (!xyzq) fail(FMM_ERR_ARG, "null bodies");
     set_device(c);
     c->N = n;
+    c->kernel_launches = 0;
     CK(cudaMemcpyAsync(c->xyzq_in.ensure(n), xyzq, n * sizeof(double4), cudaMemcpyHostToDevice, c->stream));
     c->have_bodies = true;
     c->have_tree = c->have_lists = c->have_M = c->have_L = c->have_out = false;
@@ -143,6 +144,7 @@ int fmm_set_bodies_device(fmm_ctx* c, const double* d_xyzq, int64_t n) {
     if (!d_xyzq) fail(FMM_ERR_ARG, "null bodies");
     set_device(c);
     c->N = n;
+    c->kernel_launches = 0;
     CK(cudaMemcpyAsync(c->xyzq_in.ensure(n), d_xyzq, n * sizeof(double4), cudaMemcpyDeviceToDevice, c->stream));
     c->have_bodies = true;
     c->have_tree = c->have_lists = c->have_M = c->have_L = c->have_out = false;
@@ -315,6 +317,7 @@ int fmm_get_tree_info(fmm_ctx* c, fmm_tree_info* info) {
 int fmm_get_stage_times(fmm_ctx* c, fmm_stage_times* t) {
   if (!c || !t) return FMM_ERR_ARG;
   *t = c->times;
+  t->kernel_launches = c->kernel_launches;  // launches since the bodies were last set
   return FMM_OK;
 }
 
