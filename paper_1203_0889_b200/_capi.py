@@ -90,6 +90,7 @@ SIGNATURES = {
     "fmm_downward": (C.c_int, [_vp]),
     "fmm_evaluate": (C.c_int, [_vp]),
     "fmm_synchronize": (C.c_int, [_vp]),
+    "fmm_set_overlap": (C.c_int, [_vp, C.c_int]),
     "fmm_get_results": (C.c_int, [_vp, _dp, _dp, C.c_int]),
     "fmm_results_device": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
     "fmm_get_tree_info": (C.c_int, [_vp, C.POINTER(TreeInfo)]),

@@ -43,7 +43,7 @@ void require_device() {
 }
 
 enum { EV_BUILD0 = 0, EV_BUILD1, EV_TRAV1, EV_UP1, EV_M2L1, EV_P2P1, EV_DOWN1, EV_P2PK0, EV_P2PK1, EV_M2LK0,
-       EV_M2LK1, EV_COUNT };
+       EV_M2LK1, EV_FORK, EV_COUNT };
 
 float ms_between(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
@@ -97,8 +97,10 @@ int fmm_create(const fmm_config* cfg, fmm_ctx** out) {
     c->ncoef = fmmb::n_coef(cfg->order);
     try {
       set_device(c);
-      CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-      CK(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+      int lo = 0, hi = 0;  // the expansion chain outranks P2P, which fills the SMs it leaves idle
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));
+      CK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, lo));
       for (int i = 0; i < EV_COUNT; ++i) CK(cudaEventCreate(&c->ev[i]));
       CK(cudaMallocHost(&c->hpin, 64 * sizeof(int64_t)));
       c->d_counters.ensure(32);
@@ -227,12 +229,34 @@ int fmm_evaluate(fmm_ctx* c) {
     CK(cudaEventRecord(c->ev[EV_BUILD1], c->stream));
     fmmb::traverse(c);
     CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
-    fmmb::run_upward(c, c->stream);
-    CK(cudaEventRecord(c->ev[EV_UP1], c->stream));
-    do_m2l(c);
-    CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
-    do_p2p(c);
-    CK(cudaEventRecord(c->ev[EV_P2P1], c->stream));
+    if (c->overlap) {
+      // P2P needs only the lists: run it on the second stream, concurrently with the FP64
+      // expansion chain (upward -> M2L), and join before the downward pass reads its output.
+      CK(cudaEventRecord(c->ev[EV_FORK], c->stream));
+      CK(cudaStreamWaitEvent(c->stream2, c->ev[EV_FORK], 0));
+      cudaStream_t keep = c->stream;
+      c->stream = c->stream2;
+      try {
+        do_p2p(c);
+      } catch (...) {
+        c->stream = keep;
+        throw;
+      }
+      c->stream = keep;
+      CK(cudaEventRecord(c->ev[EV_P2P1], c->stream2));
+      fmmb::run_upward(c, c->stream);
+      CK(cudaEventRecord(c->ev[EV_UP1], c->stream));
+      do_m2l(c);
+      CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
+      CK(cudaStreamWaitEvent(c->stream, c->ev[EV_P2P1], 0));
+    } else {
+      fmmb::run_upward(c, c->stream);
+      CK(cudaEventRecord(c->ev[EV_UP1], c->stream));
+      do_m2l(c);
+      CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
+      do_p2p(c);
+      CK(cudaEventRecord(c->ev[EV_P2P1], c->stream));
+    }
     fmmb::run_downward(c, c->stream);
     CK(cudaEventRecord(c->ev[EV_DOWN1], c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -241,8 +265,8 @@ int fmm_evaluate(fmm_ctx* c) {
     t.traverse_ms = ms_between(c->ev[EV_BUILD1], c->ev[EV_TRAV1]);
     t.upward_ms = ms_between(c->ev[EV_TRAV1], c->ev[EV_UP1]);
     t.m2l_ms = ms_between(c->ev[EV_UP1], c->ev[EV_M2L1]);
-    t.p2p_ms = ms_between(c->ev[EV_M2L1], c->ev[EV_P2P1]);
-    t.downward_ms = ms_between(c->ev[EV_P2P1], c->ev[EV_DOWN1]);
+    t.p2p_ms = c->overlap ? ms_between(c->ev[EV_FORK], c->ev[EV_P2P1]) : ms_between(c->ev[EV_M2L1], c->ev[EV_P2P1]);
+    t.downward_ms = ms_between(c->overlap ? c->ev[EV_M2L1] : c->ev[EV_P2P1], c->ev[EV_DOWN1]);
     t.total_ms = ms_between(c->ev[EV_BUILD0], c->ev[EV_DOWN1]);
     t.p2p_kernel_ms = ms_between(c->ev[EV_P2PK0], c->ev[EV_P2PK1]);
     t.m2l_kernel_ms = ms_between(c->ev[EV_M2LK0], c->ev[EV_M2LK1]);
@@ -500,6 +524,12 @@ int fmm_reset_accumulators(fmm_ctx* c) {
     CK(cudaStreamSynchronize(c->stream));
     c->have_L = true;
   });
+}
+
+int fmm_set_overlap(fmm_ctx* c, int on) {
+  if (!c) return FMM_ERR_ARG;
+  c->overlap = on != 0;
+  return FMM_OK;
 }
 
 // ---------------------------------------------------------------------- sharding -------

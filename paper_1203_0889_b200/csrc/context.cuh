@@ -64,6 +64,7 @@ struct fmm_ctx {
 
   // expansions and outputs
   fmmb::DBuf<double> M, L;
+  fmmb::DBuf<double> m2l_mcol;        // multipoles in z-column layout (p >= 7 kernel)
   fmmb::DBuf<double> m2l_scratch;     // per-warp-slot partial Lambda rows (p >= 7 kernel)
   fmmb::DBuf<double> phi, acc;
   fmmb::DBuf<double> phi_p2p, acc_p2p;  // near-field part (tree order)
@@ -95,13 +96,15 @@ struct fmm_ctx {
   int64_t chunk_cells = 0;                 // max cells owned by a rank (exchange chunk)
   bool shard_planned = false;
 
+  bool overlap = true;  // fmm_evaluate: P2P on stream2 concurrently with upward + M2L
+
   // state
   bool have_bodies = false, have_tree = false, have_lists = false, have_M = false,
        have_L = false, have_out = false;
 
   // timing
   fmm_stage_times times{};
-  cudaEvent_t ev[16] = {};
+  cudaEvent_t ev[16] = {};  // stage events (capi.cu EV_*)
   int kernel_launches = 0;
 };
 

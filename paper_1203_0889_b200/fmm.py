@@ -150,6 +150,7 @@ class Context:
     def evaluate(self): self._c(self.lib.fmm_evaluate(self.h))
     def synchronize(self): self._c(self.lib.fmm_synchronize(self.h))
     def reset_accumulators(self): self._c(self.lib.fmm_reset_accumulators(self.h))
+    def set_overlap(self, on: bool): self._c(self.lib.fmm_set_overlap(self.h, int(on)))
 
     # outputs
     def results(self, order: str = "tree", with_acc: bool = True):

@@ -13,8 +13,11 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--precision", default="fp32")
+ap.add_argument("--n", type=int, default=0, help="override the body count")
 a = ap.parse_args()
 gen, n, p, n_crit, theta = CONFIGS[a.config]
+if a.n:
+    n = a.n
 b = fb.generate_bodies(gen, n, 1)
 ctx = fb.Context(order=p, n_crit=n_crit, theta=theta, precision=a.precision)
 ctx.set_bodies(b)
