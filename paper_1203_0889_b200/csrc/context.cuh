@@ -59,12 +59,13 @@ struct fmm_ctx {
   int64_t n_p2p_items = 0;
   fmmb::DBuf<double> p2p_partial;   // [slot][target body][4] (phi, ax, ay, az)
   fmmb::DBuf<int4> p2p_reduce;      // target leaf, first slot, n slots, body begin
+  fmmb::DBuf<int64_t> p2p_pre;      // exclusive prefix of source-body counts over the P2P list
+  fmmb::DBuf<int32_t> p2p_tgt;      // target cell of each P2P list entry
   fmmb::DBuf<int4> p2p_ent;         // per P2P list entry: {body_begin, count, shift.xy} + {shift.z,...}
   int64_t n_p2p_reduce = 0;
 
   // expansions and outputs
   fmmb::DBuf<double> M, L;
-  fmmb::DBuf<double> m2l_mcol;        // multipoles in z-column layout (p >= 7 kernel)
   fmmb::DBuf<double> m2l_scratch;     // per-warp-slot partial Lambda rows (p >= 7 kernel)
   fmmb::DBuf<double> phi, acc;
   fmmb::DBuf<double> phi_p2p, acc_p2p;  // near-field part (tree order)

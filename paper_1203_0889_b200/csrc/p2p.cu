@@ -353,31 +353,6 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
   }
 }
 
-// Resolves every P2P list entry of every target leaf into {source body range, FP32 shift of
-// the source leaf centre into the target leaf's frame} (computed in FP64, rounded once).
-__global__ void k_p2p_entries(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
-                              const int32_t* __restrict__ src, const int32_t* __restrict__ bb,
-                              const int32_t* __restrict__ be, const double4* __restrict__ cr,
-                              P2PEnt* __restrict__ ent) {
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= nleaves) return;
-  const int32_t leaf = leaves[w];
-  const double4 ct = cr[leaf];
-  for (int64_t k = off[leaf] + lane; k < off[leaf + 1]; k += 32) {
-    const int32_t s = src[k];
-    const double4 cs = cr[s];
-    P2PEnt e;
-    e.bb = bb[s];
-    e.n = be[s] - bb[s];
-    e.sx = static_cast<float>(cs.x - ct.x);
-    e.sy = static_cast<float>(cs.y - ct.y);
-    e.sz = static_cast<float>(cs.z - ct.z);
-    e.pad[0] = e.pad[1] = e.pad[2] = 0;
-    ent[k] = e;
-  }
-}
-
 // ------------------------------------------------------------------------ FP64 kernel ----
 // Parity mode: absolute FP64 coordinates and the reference's arithmetic
 // (dx = x_i - y_j, r2 = (dx*dx + dy*dy) + dz*dz, skip r2 == 0, phi += q / sqrt(r2)).
@@ -490,29 +465,6 @@ __global__ void k_p2p_reduce(const int4* __restrict__ red, int64_t nred, const d
 }
 
 // ---------------------------------------------------------------- work list build ----
-// Per target leaf (warp each): sum of source sizes, item count. Leaves are all cells with a
-// non-empty P2P list (every leaf has at least its self pair).
-__global__ void k_leaf_sum(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
-                           const int32_t* __restrict__ src, const int32_t* __restrict__ bb,
-                           const int32_t* __restrict__ be, int64_t* __restrict__ sum_ns,
-                           unsigned long long* __restrict__ total) {
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= nleaves) return;
-  const int32_t leaf = leaves[w];
-  const int64_t l0 = off[leaf], l1 = off[leaf + 1];
-  int64_t s = 0;
-  for (int64_t k = l0 + lane; k < l1; k += 32) {
-    const int32_t q = src[k];
-    s += be[q] - bb[q];
-  }
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) {
-    sum_ns[w] = s;
-    atomicAdd(total, static_cast<unsigned long long>(s) * static_cast<unsigned long long>(be[leaf] - bb[leaf]));
-  }
-}
-
 __global__ void k_leaf_cost(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
                             const int32_t* __restrict__ bb, const int32_t* __restrict__ be, uint64_t cmax,
                             const int64_t* __restrict__ sum_ns, int32_t* __restrict__ nitems,
@@ -533,31 +485,79 @@ __global__ void k_leaf_cost(const int32_t* __restrict__ leaves, int64_t nleaves,
   npart[w] = nsc > 1 ? static_cast<int32_t>(nsc * nt) : 0;
 }
 
-// Writes the items of one target leaf (warp each). Source chunks split the list where the
-// running source-body count crosses j * sum_ns / nsc.
-__global__ void k_write_items(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
-                              const int32_t* __restrict__ src, const int32_t* __restrict__ bb,
-                              const int32_t* __restrict__ be, const int64_t* __restrict__ sum_ns,
-                              const int32_t* __restrict__ nitems, const int32_t* __restrict__ item_off,
-                              const int32_t* __restrict__ red_off, const int32_t* __restrict__ part_off,
-                              P2PItem* __restrict__ items, uint64_t* __restrict__ costs, int4* __restrict__ red) {
+__global__ void k_gather_items(const P2PItem* __restrict__ in, const int32_t* __restrict__ order, int64_t n,
+                               P2PItem* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[order[i]];
+}
+
+// ---- entry-parallel helpers (no per-leaf serial loops: C3's halo leaf has 57 K entries) ----
+__global__ void k_entry_counts(const int32_t* __restrict__ src, int64_t n, const int32_t* __restrict__ bb,
+                               const int32_t* __restrict__ be, int64_t* __restrict__ cnt) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < n) {
+    const int32_t q = src[k];
+    cnt[k] = be[q] - bb[q];
+  } else if (k == n) {
+    cnt[k] = 0;
+  }
+}
+
+__global__ void k_entry_targets(const int64_t* __restrict__ off, int64_t ncells, int32_t* __restrict__ tgt) {
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  if (w >= ncells) return;
+  for (int64_t k = off[w] + lane; k < off[w + 1]; k += 32) tgt[k] = static_cast<int32_t>(w);
+}
+
+// per work leaf: S = sum of source sizes (from the entry prefix), total cost reduced per warp
+__global__ void k_leaf_sum(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
+                            const int64_t* __restrict__ pre, const int32_t* __restrict__ bb,
+                            const int32_t* __restrict__ be, int64_t* __restrict__ sum_ns,
+                            unsigned long long* __restrict__ total) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long v = 0;
+  if (w < nleaves) {
+    const int32_t leaf = leaves[w];
+    const int64_t S = pre[off[leaf + 1]] - pre[off[leaf]];
+    sum_ns[w] = S;
+    v = static_cast<unsigned long long>(S) * static_cast<unsigned long long>(be[leaf] - bb[leaf]);
+  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(total, v);
+}
+
+// items of one work leaf (thread each): chunk j covers list entries [bnd_j, bnd_{j+1}) where
+// bnd_j is the first entry whose source-body prefix reaches j * S / nsc (binary search)
+__global__ void k_write_items(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
+                               const int64_t* __restrict__ pre, const int32_t* __restrict__ bb,
+                               const int32_t* __restrict__ be, const int64_t* __restrict__ sum_ns,
+                               const int32_t* __restrict__ nitems, const int32_t* __restrict__ item_off,
+                               const int32_t* __restrict__ red_off, const int32_t* __restrict__ part_off,
+                               P2PItem* __restrict__ items, uint64_t* __restrict__ costs, int4* __restrict__ red) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (w >= nleaves || nitems[w] == 0) return;
   const int32_t leaf = leaves[w];
   const int32_t tb = bb[leaf], te = be[leaf], nt = te - tb;
   const int32_t ntc = (nt + kThreads - 1) / kThreads;
   const int32_t nsc = nitems[w] / ntc;
   const int64_t l0 = off[leaf], l1 = off[leaf + 1];
-  const int64_t S = sum_ns[w];
-  // chunk boundaries: bnd[j] = first list index whose prefix (exclusive) >= j*S/nsc
-  int64_t prev_b = l0;
-  int64_t prefix = 0;  // exclusive prefix at list index k
-  int32_t j = 1;
-  int32_t out = item_off[w];
+  const int64_t S = sum_ns[w], p0 = pre[l0];
   const int32_t pb = nsc > 1 ? part_off[w] : -1;
-  auto emit = [&](int32_t chunk, int64_t lb, int64_t le, int64_t ns_chunk) {
-    if (lane != 0) return;
+  int32_t out = item_off[w];
+  int64_t lb = l0;
+  for (int32_t j = 0; j < nsc; ++j) {
+    int64_t le = l1;
+    if (j + 1 < nsc) {  // first k in (lb, l1] with pre[k] - p0 >= (j+1) S / nsc (empty once lb = l1)
+      const int64_t target = p0 + (S * (j + 1)) / nsc;
+      int64_t lo = min(lb + 1, l1), hi = l1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (pre[mid] < target) lo = mid + 1; else hi = mid;
+      }
+      le = lo;
+    }
+    const int64_t ns_chunk = pre[le] - pre[lb];
     for (int32_t tc = 0; tc < ntc; ++tc) {
       const int32_t t0 = tb + tc * kThreads;
       const int32_t t1 = min(te, t0 + kThreads);
@@ -568,61 +568,38 @@ __global__ void k_write_items(const int32_t* __restrict__ leaves, int64_t nleave
       itm.lb = static_cast<int32_t>(lb);
       itm.le = static_cast<int32_t>(le);
       // partial layout per leaf: t-chunk regions of nsc * (t1-t0) bodies, source-chunk major
-      itm.pbase = pb < 0 ? -1 : pb + nsc * (t0 - tb) + chunk * (t1 - t0);
+      itm.pbase = pb < 0 ? -1 : pb + nsc * (t0 - tb) + j * (t1 - t0);
       itm.sb0 = 0;
       itm.pad = 0;
       items[out] = itm;
       costs[out] = static_cast<uint64_t>(t1 - t0) * static_cast<uint64_t>(ns_chunk);
       ++out;
     }
-  };
-  if (nsc == 1) {
-    emit(0, l0, l1, S);
-  } else {
-    int64_t chunk_start_prefix = 0;
-    for (int64_t base = l0; base < l1 && j < nsc; base += 32) {
-      const int64_t k = base + lane;
-      const int32_t n = k < l1 ? be[src[k]] - bb[src[k]] : 0;
-      int64_t incl = n;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int64_t excl = prefix + incl - n;
-      // walk boundaries that fall inside this 32-entry window
-      while (j < nsc) {
-        const int64_t target = (S * j) / nsc;
-        const bool hit = (k < l1) && (excl >= target) && (k > prev_b);
-        const unsigned m = __ballot_sync(0xffffffffu, hit);
-        if (!m) break;
-        const int first = __ffs(m) - 1;
-        const int64_t kb = base + first;
-        const int64_t pre = __shfl_sync(0xffffffffu, excl, first);
-        emit(j - 1, prev_b, kb, pre - chunk_start_prefix);
-        chunk_start_prefix = pre;
-        prev_b = kb;
-        ++j;
-      }
-      prefix += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    // remaining chunks (degenerate boundaries collapse onto the list end)
-    while (j < nsc) {
-      emit(j - 1, prev_b, prev_b, 0);
-      ++j;
-    }
-    emit(nsc - 1, prev_b, l1, S - chunk_start_prefix);
-    if (lane == 0)
-      for (int32_t tc = 0; tc < ntc; ++tc) {
-        const int32_t t0 = tb + tc * kThreads;
-        red[red_off[w] + tc] = make_int4(t0, min(te, t0 + kThreads), pb + nsc * (t0 - tb), nsc);
-      }
+    lb = le;
   }
+  if (nsc > 1)
+    for (int32_t tc = 0; tc < ntc; ++tc) {
+      const int32_t t0 = tb + tc * kThreads;
+      red[red_off[w] + tc] = make_int4(t0, min(te, t0 + kThreads), pb + nsc * (t0 - tb), nsc);
+    }
 }
 
-__global__ void k_gather_items(const P2PItem* __restrict__ in, const int32_t* __restrict__ order, int64_t n,
-                               P2PItem* __restrict__ out) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) out[i] = in[order[i]];
+// one P2P list entry per thread: {source body range, FP32 shift into the target leaf frame}
+__global__ void k_p2p_entries(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src, int64_t n,
+                               const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
+                               const double4* __restrict__ cr, P2PEnt* __restrict__ ent) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int32_t s = src[k];
+  const double4 cs = cr[s], ct = cr[tgt[k]];
+  P2PEnt e;
+  e.bb = bb[s];
+  e.n = be[s] - bb[s];
+  e.sx = static_cast<float>(cs.x - ct.x);
+  e.sy = static_cast<float>(cs.y - ct.y);
+  e.sz = static_cast<float>(cs.z - ct.z);
+  e.pad[0] = e.pad[1] = e.pad[2] = 0;
+  ent[k] = e;
 }
 
 __global__ void k_iota(int32_t* __restrict__ v, int64_t n) {
@@ -640,12 +617,21 @@ void exclusive_scan_i32(fmm_ctx* c, const int32_t* in, int32_t* out, int64_t n) 
 
 void build_p2p_worklist(fmm_ctx* c) {
   cudaStream_t s = c->stream;
-  const int64_t nl = c->nwl;
+  const int64_t nl = c->nwl, ne = c->n_p2p;
+  // source-body prefix over all list entries, and each entry's target
+  int64_t* pre = c->p2p_pre.ensure(ne + 2);
+  int64_t* cnt = reinterpret_cast<int64_t*>(c->keys_a.ensure(ne + 2));
+  k_entry_counts<<<ceil_div(ne + 1, 256), 256, 0, s>>>(c->p2p_src.p, ne, c->c_body_begin.p, c->c_body_end.p, cnt);
+  {
+    size_t sb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, cnt, pre, (int)(ne + 1), s));
+    CK(cub::DeviceScan::ExclusiveSum(temp_storage(c, sb), sb, cnt, pre, (int)(ne + 1), s));
+  }
   int64_t* sum_ns = c->scan_a.ensure(nl + 1);
   unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->d_counters.ensure(16)) + 12;
   CK(cudaMemsetAsync(tot, 0, sizeof(unsigned long long), s));
-  k_leaf_sum<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->wl, nl, c->p2p_off.p, c->p2p_src.p, c->c_body_begin.p,
-                                                    c->c_body_end.p, sum_ns, tot);
+  k_leaf_sum<<<ceil_div(nl, 256), 256, 0, s>>>(c->wl, nl, c->p2p_off.p, pre, c->c_body_begin.p, c->c_body_end.p,
+                                               sum_ns, tot);
   CK_LAUNCH("k_leaf_sum");
   CK(cudaMemcpyAsync(c->hpin + 16, tot, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -679,16 +665,18 @@ void build_p2p_worklist(fmm_ctx* c) {
   uint64_t* costs_sorted = c->keys_b.ensure(nitem + 1);
   int4* red = c->p2p_reduce.ensure(nr + 1);
   c->p2p_partial.ensure(4 * (np + 1));
-  k_write_items<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->wl, nl, c->p2p_off.p, c->p2p_src.p, c->c_body_begin.p,
-                                                       c->c_body_end.p, sum_ns, nitems, item_off, red_off, part_off,
-                                                       items_raw, costs, red);
+  k_write_items<<<ceil_div(nl, 128), 128, 0, s>>>(c->wl, nl, c->p2p_off.p, pre, c->c_body_begin.p,
+                                                   c->c_body_end.p, sum_ns, nitems, item_off, red_off, part_off,
+                                                   items_raw, costs, red);
   CK_LAUNCH("k_write_items");
   if (c->cfg.precision == FMM_PREC_FP32_P2P) {
-    P2PEnt* ent = reinterpret_cast<P2PEnt*>(c->p2p_ent.ensure(2 * (c->n_p2p + 1)));
-    k_p2p_entries<<<ceil_div(nl * 32, 256), 256, 0, s>>>(c->wl, nl, c->p2p_off.p, c->p2p_src.p,
-                                                         c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, ent);
+    int32_t* tgt = c->p2p_tgt.ensure(ne + 1);
+    k_entry_targets<<<ceil_div(c->ncells * 32, 256), 256, 0, s>>>(c->p2p_off.p, c->ncells, tgt);
+    P2PEnt* ent = reinterpret_cast<P2PEnt*>(c->p2p_ent.ensure(2 * (ne + 1)));
+    k_p2p_entries<<<ceil_div(ne, 256), 256, 0, s>>>(tgt, c->p2p_src.p, ne, c->c_body_begin.p, c->c_body_end.p,
+                                                     c->c_cr.p, ent);
     CK_LAUNCH("k_p2p_entries");
-    c->kernel_launches += 1;
+    c->kernel_launches += 2;
   }
   // cost-sorted (descending, stable) work list: the longest items launch first
   int32_t* ord_in = c->i32_c.ensure(2 * (nitem + 1));
