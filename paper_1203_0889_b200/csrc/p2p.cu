@@ -104,7 +104,8 @@ __device__ __forceinline__ void tile_setup(int tid, int32_t le, int32_t cursor, 
 struct P2PEnt {  // one P2P list entry (target-specific): source bodies and FP32 frame shift
   int32_t bb, n;
   float sx, sy, sz;
-  int32_t pad[3];
+  int32_t self;  // 1 for the (leaf, leaf) entry: the only one that can hold r^2 == 0 pairs
+  int32_t pad[2];
 };
 static_assert(sizeof(P2PEnt) == 32, "P2PEnt is 32 B");
 
@@ -112,23 +113,24 @@ struct TileTab {
   int32_t off[kTileSegs + 1];
   int32_t bb[kTileSegs];
   float sh[kTileSegs][3];
-  int32_t nseg, next, next_off;
+  int32_t nseg, next, next_off, guard;
 };
 
 // warp 0: take the list entries from (cursor, cur_off) that fit in one tile
 __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cursor, int32_t cur_off,
                                                const P2PEnt* __restrict__ ent, TileTab& tt) {
   const int32_t k = cursor + lane;
-  int32_t n = 0, b = 0;
+  int32_t n = 0, b = 0, self = 0;
   float sx = 0.f, sy = 0.f, sz = 0.f;
   if (k < le) {
     const int4 e0 = reinterpret_cast<const int4*>(ent)[2 * k];
-    const float z = reinterpret_cast<const float*>(ent)[8 * k + 4];
+    const int2 e1 = reinterpret_cast<const int2*>(ent)[4 * k + 2];
     b = e0.x;
     n = e0.y;
     sx = __int_as_float(e0.z);
     sy = __int_as_float(e0.w);
-    sz = z;
+    sz = __int_as_float(e1.x);
+    self = e1.y;
     if (lane == 0) {
       b += cur_off;
       n -= cur_off;
@@ -141,6 +143,7 @@ __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cur
   }
   const bool fits = (k < le) && (incl <= kTileBodies);
   const unsigned m = __ballot_sync(0xffffffffu, fits);
+  const unsigned sm = __ballot_sync(0xffffffffu, self != 0);
   int nseg;
   if (m == 0) {  // one (level-21 overflow) leaf larger than the tile: take kTileBodies of it
     nseg = 1;
@@ -148,6 +151,9 @@ __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cur
   } else {
     nseg = 32 - __clz(m);  // fits is a prefix of the lanes
   }
+  // the self entry gets a tile of its own: only that tile runs the r^2 == 0 guard
+  if (sm & 1u) nseg = 1;
+  else if (sm) nseg = min(nseg, __ffs(sm) - 1);
   if (lane < nseg) {
     tt.off[lane + 1] = incl;
     tt.bb[lane] = b;
@@ -160,34 +166,80 @@ __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cur
     tt.nseg = nseg;
     tt.next = m == 0 ? cursor : cursor + nseg;
     tt.next_off = m == 0 ? cur_off + kTileBodies : 0;
+    tt.guard = static_cast<int32_t>(sm & 1u);
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+// ---- TMA bulk copies (cp.async.bulk global -> shared, completion on an mbarrier) ----
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 
-// all threads: issue the raw copies of one tile (warp w copies segments w, w+4, ...)
-__device__ __forceinline__ void tile_issue(int tid, const TileTab& tt, const float4* __restrict__ bodyf,
-                                           float4* buf) {
-  const int w = tid >> 5, lane = tid & 31;
-  for (int k = w; k < tt.nseg; k += kThreads / 32) {
-    const int32_t base = tt.bb[k], o0 = tt.off[k], n = tt.off[k + 1] - o0;
-    for (int j = lane; j < n; j += 32) cp_async16(&buf[o0 + j], &bodyf[base + j]);
+// warp 0: one bulk copy per list entry of the tile (lane k copies entry k's bodies); the bytes
+// land on `bar`. The proxy fence orders the CTA's earlier generic reads/writes of the buffer
+// (published by the preceding __syncthreads) before the async-proxy writes.
+__device__ __forceinline__ void tile_tma(int lane, const TileTab& tt, const float4* __restrict__ bodyf, float4* buf,
+                                         uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  const int nseg = tt.nseg;
+  if (lane == 0) mbar_arrive_expect_tx(bar, static_cast<unsigned>(tt.off[nseg]) * 16u);
+  if (lane < nseg) {
+    const int32_t o0 = tt.off[lane];
+    bulk_g2s(buf + o0, bodyf + tt.bb[lane], static_cast<unsigned>(tt.off[lane + 1] - o0) * 16u, bar);
   }
 }
 
-// all threads: convert the bodies this thread copied (same mapping as tile_issue)
+// all threads: shift the staged bodies into the target frame and negate (warp w converts list
+// entries w, w+4, ..., two entries per pass for memory-level parallelism)
 __device__ __forceinline__ void tile_convert(int tid, const TileTab& tt, float4* buf) {
   const int w = tid >> 5, lane = tid & 31;
-  for (int k = w; k < tt.nseg; k += kThreads / 32) {
-    const int32_t o0 = tt.off[k], n = tt.off[k + 1] - o0;
+  const int nseg = tt.nseg;
+#pragma unroll 1
+  for (int k = w; k < nseg; k += 8) {
+    const int k1 = k + 4;
+    const int32_t o0 = tt.off[k], n0 = tt.off[k + 1] - o0;
+    int32_t o1 = 0, n1 = 0;
+    float tx = 0.f, ty = 0.f, tz = 0.f;
+    if (k1 < nseg) {
+      o1 = tt.off[k1];
+      n1 = tt.off[k1 + 1] - o1;
+      tx = tt.sh[k1][0];
+      ty = tt.sh[k1][1];
+      tz = tt.sh[k1][2];
+    }
     const float sx = tt.sh[k][0], sy = tt.sh[k][1], sz = tt.sh[k][2];
-    for (int j = lane; j < n; j += 32) {
-      const float4 b = buf[o0 + j];
-      buf[o0 + j] = make_float4(-b.x - sx, -b.y - sy, -b.z - sz, b.w);
+    const int32_t nm = max(n0, n1);
+#pragma unroll 1
+    for (int j = lane; j < nm; j += 32) {
+      float4 a, b;
+      if (j < n0) a = buf[o0 + j];
+      if (j < n1) b = buf[o1 + j];
+      if (j < n0) buf[o0 + j] = make_float4(-a.x - sx, -a.y - sy, -a.z - sz, a.w);
+      if (j < n1) buf[o1 + j] = make_float4(-b.x - tx, -b.y - ty, -b.z - tz, b.w);
     }
   }
 }
@@ -202,18 +254,27 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 // q/r, phi, 1/r^2, q/r^3, 3 acc) and one MUFU.RSQ (XU pipe: 16/clk/SM, so a second MUFU per
 // pair would make the XU the bottleneck); r^2 == 0 pairs (self, coincident;
 // kernels.cpp:185-186) are predicated off.
-template <bool kAcc>
+//
+// kGuard = false (every entry but the self one: the bodies are distinct, r^2 > 0): r^2 is
+// seeded with 1e-30 instead of predicating the MUFU, which keeps the result finite even if
+// two distinct bodies round to the same FP32 offsets, at no instruction cost.
+template <bool kAcc, bool kGuard>
 __device__ __forceinline__ void pair_body(const float4 sv, const float2 X, const float2 Y, const float2 Z, float2& ph,
                                           float2& ax, float2& ay, float2& az) {
   const float2 dx = __fadd2_rn(X, make_float2(sv.x, sv.x));
   const float2 dy = __fadd2_rn(Y, make_float2(sv.y, sv.y));
   const float2 dz = __fadd2_rn(Z, make_float2(sv.z, sv.z));
-  float2 r2 = __fmul2_rn(dx, dx);
+  float2 r2 = kGuard ? __fmul2_rn(dx, dx) : __ffma2_rn(dx, dx, make_float2(1e-30f, 1e-30f));
   r2 = __ffma2_rn(dy, dy, r2);
   r2 = __ffma2_rn(dz, dz, r2);
-  float2 ri = make_float2(0.f, 0.f);
-  if (r2.x > 0.f) ri.x = rsqrt_approx(r2.x);
-  if (r2.y > 0.f) ri.y = rsqrt_approx(r2.y);
+  float2 ri;
+  if constexpr (kGuard) {
+    ri = make_float2(0.f, 0.f);
+    if (r2.x > 0.f) ri.x = rsqrt_approx(r2.x);
+    if (r2.y > 0.f) ri.y = rsqrt_approx(r2.y);
+  } else {
+    ri = make_float2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
+  }
   const float2 qr = __fmul2_rn(make_float2(sv.w, sv.w), ri);
   ph = __fadd2_rn(ph, qr);
   if constexpr (kAcc) {
@@ -224,7 +285,7 @@ __device__ __forceinline__ void pair_body(const float4 sv, const float2 X, const
   }
 }
 
-template <bool kAcc>
+template <bool kAcc, bool kGuard>
 __device__ __forceinline__ void tile_compute(const float4* __restrict__ buf, int nb, int g, int G, float2 X,
                                              float2 Y, float2 Z, double& ph0, double& ph1, double& ax0,
                                              double& ax1, double& ay0, double& ay1, double& az0, double& az1) {
@@ -243,9 +304,9 @@ __device__ __forceinline__ void tile_compute(const float4* __restrict__ buf, int
 #pragma unroll
     for (int u = 0; u < U; ++u) sv[u] = p[u];
 #pragma unroll
-    for (int u = 0; u < U; ++u) pair_body<kAcc>(sv[u], X, Y, Z, ph, ax, ay, az);
+    for (int u = 0; u < U; ++u) pair_body<kAcc, kGuard>(sv[u], X, Y, Z, ph, ax, ay, az);
   }
-  for (; p < end; ++p) pair_body<kAcc>(*p, X, Y, Z, ph, ax, ay, az);
+  for (; p < end; ++p) pair_body<kAcc, kGuard>(*p, X, Y, Z, ph, ax, ay, az);
   // fold this tile's FP32 partials into the FP64 accumulators
   ph0 += ph.x;
   ph1 += ph.y;
@@ -268,6 +329,7 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
            double* __restrict__ phi_out, double* __restrict__ acc_out, double* __restrict__ partial) {
   __shared__ __align__(16) float4 sS[2][kTileBodies];
   __shared__ TileTab tabs[3];  // ring: tile k computes from tabs[k%3] while k+2 is resolved
+  __shared__ __align__(8) uint64_t bars[2];  // TMA completion, one per buffer
 
   const P2PItem it = items[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -288,27 +350,42 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
   double ph0 = 0.0, ph1 = 0.0, ax0 = 0.0, ax1 = 0.0, ay0 = 0.0, ay1 = 0.0, az0 = 0.0, az1 = 0.0;
 
   // prologue: tile 0 staged and converted, tile 1 resolved
-  if (tid < 32) tile_setup_ent(lane, it.le, it.lb, 0, ent, tabs[0]);
-  __syncthreads();
   bool have = it.lb < it.le;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (tid < 32 && have) {
+    tile_setup_ent(lane, it.le, it.lb, 0, ent, tabs[0]);
+    __syncwarp();
+    tile_tma(lane, tabs[0], bodyf, sS[0], &bars[0]);
+    if (tabs[0].next < it.le) tile_setup_ent(lane, it.le, tabs[0].next, tabs[0].next_off, ent, tabs[1]);
+  }
+  __syncthreads();
   if (have) {
-    tile_issue(tid, tabs[0], bodyf, sS[0]);
-    cp_async_wait_all();
+    mbar_wait(&bars[0], 0);
     tile_convert(tid, tabs[0], sS[0]);
-    if (tid < 32 && tabs[0].next < it.le) tile_setup_ent(lane, it.le, tabs[0].next, tabs[0].next_off, ent, tabs[1]);
   }
   __syncthreads();
   int k3 = 0, k2 = 0;  // tile index mod 3 (tables) and mod 2 (buffers)
+  unsigned kt = 0;     // tile index (TMA barrier parity of tile j is (j >> 1) & 1)
   while (have) {
     const TileTab& tc = tabs[k3];
     const int n1 = k3 == 2 ? 0 : k3 + 1, n2 = n1 == 2 ? 0 : n1 + 1;
     const TileTab& tn = tabs[n1];
     const bool more = tc.next < it.le;
     const int nb = tc.off[tc.nseg];
-    if (more) tile_issue(tid, tn, bodyf, sS[k2 ^ 1]);
-    if (active) tile_compute<kAcc>(sS[k2], nb, g, G, X, Y, Z, ph0, ph1, ax0, ax1, ay0, ay1, az0, az1);
+    if (more && tid < 32) tile_tma(lane, tn, bodyf, sS[k2 ^ 1], &bars[k2 ^ 1]);
+    if (active) {
+      if (tc.guard)
+        tile_compute<kAcc, true>(sS[k2], nb, g, G, X, Y, Z, ph0, ph1, ax0, ax1, ay0, ay1, az0, az1);
+      else
+        tile_compute<kAcc, false>(sS[k2], nb, g, G, X, Y, Z, ph0, ph1, ax0, ax1, ay0, ay1, az0, az1);
+    }
     if (more) {
-      cp_async_wait_all();
+      mbar_wait(&bars[k2 ^ 1], ((kt + 1) >> 1) & 1u);
       tile_convert(tid, tn, sS[k2 ^ 1]);
       if (tid < 32 && tn.next < it.le) tile_setup_ent(lane, it.le, tn.next, tn.next_off, ent, tabs[n2]);
     }
@@ -316,6 +393,7 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
     have = more;
     k3 = n1;
     k2 ^= 1;
+    ++kt;
   }
   // reduce the G lane groups in fixed order (reusing the tile buffer) and write
   double* red = reinterpret_cast<double*>(sS);  // [G][slots][2 targets][4]
@@ -584,22 +662,38 @@ __global__ void k_write_items(const int32_t* __restrict__ leaves, int64_t nleave
     }
 }
 
-// one P2P list entry per thread: {source body range, FP32 shift into the target leaf frame}
+// one P2P list entry per thread: {source body range, FP32 shift into the target leaf frame}.
+// Within each target's (source-sorted) list the self entry is rotated to the front, so that a
+// work item's first tile is the only one that needs the r^2 == 0 guard. Items still partition
+// the list positions, so every entry is computed exactly once.
 __global__ void k_p2p_entries(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src, int64_t n,
-                               const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
-                               const double4* __restrict__ cr, P2PEnt* __restrict__ ent) {
+                               const int64_t* __restrict__ off, const int32_t* __restrict__ bb,
+                               const int32_t* __restrict__ be, const double4* __restrict__ cr,
+                               P2PEnt* __restrict__ ent) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const int32_t s = src[k];
-  const double4 cs = cr[s], ct = cr[tgt[k]];
+  const int32_t s = src[k], t = tgt[k];
+  const double4 cs = cr[s], ct = cr[t];
+  int64_t pos = k;
+  if (s == t) {
+    pos = off[t];
+  } else if (s < t) {  // before the self entry: shift right by one if the list holds it
+    int64_t lo = k + 1, hi = off[t + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (src[mid] < t) lo = mid + 1; else hi = mid;
+    }
+    if (lo < off[t + 1] && src[lo] == t) pos = k + 1;
+  }
   P2PEnt e;
   e.bb = bb[s];
   e.n = be[s] - bb[s];
   e.sx = static_cast<float>(cs.x - ct.x);
   e.sy = static_cast<float>(cs.y - ct.y);
   e.sz = static_cast<float>(cs.z - ct.z);
-  e.pad[0] = e.pad[1] = e.pad[2] = 0;
-  ent[k] = e;
+  e.self = s == t ? 1 : 0;
+  e.pad[0] = e.pad[1] = 0;
+  ent[pos] = e;
 }
 
 __global__ void k_iota(int32_t* __restrict__ v, int64_t n) {
@@ -673,8 +767,8 @@ void build_p2p_worklist(fmm_ctx* c) {
     int32_t* tgt = c->p2p_tgt.ensure(ne + 1);
     k_entry_targets<<<ceil_div(c->ncells * 32, 256), 256, 0, s>>>(c->p2p_off.p, c->ncells, tgt);
     P2PEnt* ent = reinterpret_cast<P2PEnt*>(c->p2p_ent.ensure(2 * (ne + 1)));
-    k_p2p_entries<<<ceil_div(ne, 256), 256, 0, s>>>(tgt, c->p2p_src.p, ne, c->c_body_begin.p, c->c_body_end.p,
-                                                     c->c_cr.p, ent);
+    k_p2p_entries<<<ceil_div(ne, 256), 256, 0, s>>>(tgt, c->p2p_src.p, ne, c->p2p_off.p, c->c_body_begin.p,
+                                                     c->c_body_end.p, c->c_cr.p, ent);
     CK_LAUNCH("k_p2p_entries");
     c->kernel_launches += 2;
   }

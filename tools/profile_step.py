@@ -14,6 +14,7 @@ ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--precision", default="fp32")
 ap.add_argument("--n", type=int, default=0, help="override the body count")
+ap.add_argument("--serial", action="store_true", help="no P2P/far-field overlap (isolated kernel times)")
 a = ap.parse_args()
 gen, n, p, n_crit, theta = CONFIGS[a.config]
 if a.n:
@@ -21,6 +22,8 @@ if a.n:
 b = fb.generate_bodies(gen, n, 1)
 ctx = fb.Context(order=p, n_crit=n_crit, theta=theta, precision=a.precision)
 ctx.set_bodies(b)
+if a.serial:
+    ctx.set_overlap(False)
 for _ in range(a.warmup + a.steps):
     ctx.evaluate()
 t = ctx.stage_times()
