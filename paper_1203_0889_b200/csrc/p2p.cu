@@ -116,15 +116,32 @@ struct TileTab {
   int32_t nseg, next, next_off, guard;
 };
 
-// warp 0: take the list entries from (cursor, cur_off) that fit in one tile
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// warp 0: stage list entries [cursor, cursor + 32) into shared memory ahead of tile_setup_ent,
+// so that the global-load latency overlaps a tile's compute instead of the tile barrier
+__device__ __forceinline__ void ent_prefetch(int lane, int32_t cursor, int32_t le, const P2PEnt* __restrict__ ent,
+                                             P2PEnt* st) {
+  if (cursor + lane < le) {
+    cp_async16(&st[lane], &ent[cursor + lane]);
+    cp_async16(reinterpret_cast<char*>(&st[lane]) + 16, reinterpret_cast<const char*>(&ent[cursor + lane]) + 16);
+  }
+}
+
+// warp 0: take the list entries from (cursor, cur_off) that fit in one tile; e[lane] is list
+// entry cursor + lane (global memory, or the shared staging copy)
 __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cursor, int32_t cur_off,
-                                               const P2PEnt* __restrict__ ent, TileTab& tt) {
+                                               const P2PEnt* e, TileTab& tt) {
   const int32_t k = cursor + lane;
   int32_t n = 0, b = 0, self = 0;
   float sx = 0.f, sy = 0.f, sz = 0.f;
   if (k < le) {
-    const int4 e0 = reinterpret_cast<const int4*>(ent)[2 * k];
-    const int2 e1 = reinterpret_cast<const int2*>(ent)[4 * k + 2];
+    const int4 e0 = reinterpret_cast<const int4*>(e)[2 * lane];
+    const int2 e1 = reinterpret_cast<const int2*>(e)[4 * lane + 2];
     b = e0.x;
     n = e0.y;
     sx = __int_as_float(e0.z);
@@ -330,6 +347,7 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
   __shared__ __align__(16) float4 sS[2][kTileBodies];
   __shared__ TileTab tabs[3];  // ring: tile k computes from tabs[k%3] while k+2 is resolved
   __shared__ __align__(8) uint64_t bars[2];  // TMA completion, one per buffer
+  __shared__ __align__(16) P2PEnt st[32];    // list entries staged for the next tile_setup_ent
 
   const P2PItem it = items[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -358,10 +376,11 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
   }
   __syncthreads();
   if (tid < 32 && have) {
-    tile_setup_ent(lane, it.le, it.lb, 0, ent, tabs[0]);
+    tile_setup_ent(lane, it.le, it.lb, 0, ent + it.lb, tabs[0]);
     __syncwarp();
     tile_tma(lane, tabs[0], bodyf, sS[0], &bars[0]);
-    if (tabs[0].next < it.le) tile_setup_ent(lane, it.le, tabs[0].next, tabs[0].next_off, ent, tabs[1]);
+    const int32_t c1 = tabs[0].next;
+    if (c1 < it.le) tile_setup_ent(lane, it.le, c1, tabs[0].next_off, ent + c1, tabs[1]);
   }
   __syncthreads();
   if (have) {
@@ -377,7 +396,10 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
     const TileTab& tn = tabs[n1];
     const bool more = tc.next < it.le;
     const int nb = tc.off[tc.nseg];
-    if (more && tid < 32) tile_tma(lane, tn, bodyf, sS[k2 ^ 1], &bars[k2 ^ 1]);
+    if (more && tid < 32) {
+      tile_tma(lane, tn, bodyf, sS[k2 ^ 1], &bars[k2 ^ 1]);
+      ent_prefetch(lane, tn.next, it.le, ent, st);
+    }
     if (active) {
       if (tc.guard)
         tile_compute<kAcc, true>(sS[k2], nb, g, G, X, Y, Z, ph0, ph1, ax0, ax1, ay0, ay1, az0, az1);
@@ -387,7 +409,11 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
     if (more) {
       mbar_wait(&bars[k2 ^ 1], ((kt + 1) >> 1) & 1u);
       tile_convert(tid, tn, sS[k2 ^ 1]);
-      if (tid < 32 && tn.next < it.le) tile_setup_ent(lane, it.le, tn.next, tn.next_off, ent, tabs[n2]);
+      if (tid < 32 && tn.next < it.le) {
+        cp_async_wait_all();
+        __syncwarp();
+        tile_setup_ent(lane, it.le, tn.next, tn.next_off, st, tabs[n2]);
+      }
     }
     __syncthreads();  // tile k+1 published, tile k+2 resolved; everyone is done with tile k
     have = more;
