@@ -60,7 +60,6 @@ struct fmm_ctx {
   fmmb::DBuf<double> p2p_partial;   // [slot][target body][4] (phi, ax, ay, az)
   fmmb::DBuf<int4> p2p_reduce;      // target leaf, first slot, n slots, body begin
   fmmb::DBuf<int64_t> p2p_pre;      // exclusive prefix of source-body counts over the P2P list
-  fmmb::DBuf<int32_t> p2p_tgt;      // target cell of each P2P list entry
   fmmb::DBuf<int4> p2p_ent;         // per P2P list entry: {body_begin, count, shift.xy} + {shift.z,...}
   int64_t n_p2p_reduce = 0;
 
@@ -82,6 +81,7 @@ struct fmm_ctx {
   fmmb::DBuf<double> small;
   fmmb::DBuf<int2> pairs_d;         // second traversal frontier
   fmmb::DBuf<uint64_t> m2l_keys, p2p_keys;  // emitted (target << sbits | source)
+  fmmb::DBuf<uint64_t> trav_ctr;            // traversal level counters
   fmmb::DBuf<int32_t> bnd;           // child boundaries of one level (9 per cell)
   int64_t* hpin = nullptr;           // pinned host scratch (64 x int64)
 

@@ -607,13 +607,6 @@ __global__ void k_entry_counts(const int32_t* __restrict__ src, int64_t n, const
   }
 }
 
-__global__ void k_entry_targets(const int64_t* __restrict__ off, int64_t ncells, int32_t* __restrict__ tgt) {
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= ncells) return;
-  for (int64_t k = off[w] + lane; k < off[w + 1]; k += 32) tgt[k] = static_cast<int32_t>(w);
-}
-
 // per work leaf: S = sum of source sizes (from the entry prefix), total cost reduced per warp
 __global__ void k_leaf_sum(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
                             const int64_t* __restrict__ pre, const int32_t* __restrict__ bb,
@@ -688,38 +681,43 @@ __global__ void k_write_items(const int32_t* __restrict__ leaves, int64_t nleave
     }
 }
 
-// one P2P list entry per thread: {source body range, FP32 shift into the target leaf frame}.
-// Within each target's (source-sorted) list the self entry is rotated to the front, so that a
-// work item's first tile is the only one that needs the r^2 == 0 guard. Items still partition
-// the list positions, so every entry is computed exactly once.
-__global__ void k_p2p_entries(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src, int64_t n,
-                               const int64_t* __restrict__ off, const int32_t* __restrict__ bb,
-                               const int32_t* __restrict__ be, const double4* __restrict__ cr,
-                               P2PEnt* __restrict__ ent) {
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int32_t s = src[k], t = tgt[k];
-  const double4 cs = cr[s], ct = cr[t];
-  int64_t pos = k;
-  if (s == t) {
-    pos = off[t];
-  } else if (s < t) {  // before the self entry: shift right by one if the list holds it
-    int64_t lo = k + 1, hi = off[t + 1];
+// P2P list entries of one target cell per warp: {source body range, FP32 shift into the target
+// leaf frame}. Within each target's (source-sorted) list the self entry is rotated to the
+// front, so that a work item's first tile is the only one that needs the r^2 == 0 guard.
+// Items still partition the list positions, so every entry is computed exactly once.
+__global__ void k_p2p_entries(const int64_t* __restrict__ off, int64_t ncells, const int32_t* __restrict__ src,
+                              const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
+                              const double4* __restrict__ cr, P2PEnt* __restrict__ ent) {
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= ncells) return;
+  const int64_t l0 = off[t], l1 = off[t + 1];
+  if (l0 == l1) return;
+  int64_t sp = -1;  // position of the self entry
+  if (lane == 0) {
+    int64_t lo = l0, hi = l1;
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
       if (src[mid] < t) lo = mid + 1; else hi = mid;
     }
-    if (lo < off[t + 1] && src[lo] == t) pos = k + 1;
+    if (lo < l1 && src[lo] == t) sp = lo;
   }
-  P2PEnt e;
-  e.bb = bb[s];
-  e.n = be[s] - bb[s];
-  e.sx = static_cast<float>(cs.x - ct.x);
-  e.sy = static_cast<float>(cs.y - ct.y);
-  e.sz = static_cast<float>(cs.z - ct.z);
-  e.self = s == t ? 1 : 0;
-  e.pad[0] = e.pad[1] = 0;
-  ent[pos] = e;
+  sp = __shfl_sync(0xffffffffu, sp, 0);
+  const double4 ct = cr[t];
+  for (int64_t k = l0 + lane; k < l1; k += 32) {
+    const int32_t s = src[k];
+    const double4 cs = cr[s];
+    const int64_t pos = sp < 0 ? k : (k == sp ? l0 : (k < sp ? k + 1 : k));
+    P2PEnt e;
+    e.bb = bb[s];
+    e.n = be[s] - bb[s];
+    e.sx = static_cast<float>(cs.x - ct.x);
+    e.sy = static_cast<float>(cs.y - ct.y);
+    e.sz = static_cast<float>(cs.z - ct.z);
+    e.self = k == sp ? 1 : 0;
+    e.pad[0] = e.pad[1] = 0;
+    ent[pos] = e;
+  }
 }
 
 __global__ void k_iota(int32_t* __restrict__ v, int64_t n) {
@@ -790,13 +788,11 @@ void build_p2p_worklist(fmm_ctx* c) {
                                                    items_raw, costs, red);
   CK_LAUNCH("k_write_items");
   if (c->cfg.precision == FMM_PREC_FP32_P2P) {
-    int32_t* tgt = c->p2p_tgt.ensure(ne + 1);
-    k_entry_targets<<<ceil_div(c->ncells * 32, 256), 256, 0, s>>>(c->p2p_off.p, c->ncells, tgt);
     P2PEnt* ent = reinterpret_cast<P2PEnt*>(c->p2p_ent.ensure(2 * (ne + 1)));
-    k_p2p_entries<<<ceil_div(ne, 256), 256, 0, s>>>(tgt, c->p2p_src.p, ne, c->p2p_off.p, c->c_body_begin.p,
-                                                     c->c_body_end.p, c->c_cr.p, ent);
+    k_p2p_entries<<<ceil_div(c->ncells * 32, 256), 256, 0, s>>>(c->p2p_off.p, c->ncells, c->p2p_src.p,
+                                                                c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, ent);
     CK_LAUNCH("k_p2p_entries");
-    c->kernel_launches += 2;
+    c->kernel_launches += 1;
   }
   // cost-sorted (descending, stable) work list: the longest items launch first
   int32_t* ord_in = c->i32_c.ensure(2 * (nitem + 1));

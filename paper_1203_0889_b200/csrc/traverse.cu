@@ -59,60 +59,92 @@ __device__ __forceinline__ void classify(const int2 pr, const double4* __restric
   nchild = split_t ? tc : sc;
 }
 
-// One frontier step: every pair is classified (process_pair) and its outputs are placed with
-// warp-aggregated atomics. The emission order is therefore not deterministic, but the lists
-// are canonicalised afterwards by a radix sort on (target, source), so everything downstream
-// (CSR order, summation order, results) is deterministic.
+// One frontier step (frontier level L): every pair is classified (process_pair) and emits an
+// M2L or P2P key or pushes its child pairs to level L+1. The launch does not know the frontier
+// size: it reads it from the level counters written by the previous launch, so all levels are
+// queued back to back without a host round trip. Each block takes chunks of kStepChunk pairs
+// (kStepPer per thread) and reserves its output slots with one atomic per counter (block-level
+// aggregation: the per-warp variant was bound by same-address atomic throughput). Output that
+// would exceed a buffer's capacity is dropped and flagged; the host then grows the buffers and
+// reruns the traversal. Emission order is not deterministic; the lists are canonicalised
+// afterwards by a radix sort on (target, source), so everything downstream is deterministic.
+// Counters (ctr): [0] M2L total, [1] P2P total, [2] overflow flag, [4 + L] frontier size of
+// level L (level 0 = the root pair).
+constexpr int kStepThreads = 256;
+constexpr int kStepPer = 4;
+constexpr int kStepChunk = kStepThreads * kStepPer;
+
 template <class KeyT>
-__global__ void __launch_bounds__(256)
-k_step(const int2* __restrict__ fr, int64_t n, const double4* __restrict__ cr, const int32_t* __restrict__ cc,
-       const int32_t* __restrict__ cb, double theta, double theta2, int mutual, int sbits,
-       KeyT* __restrict__ m2l_keys, KeyT* __restrict__ p2p_keys, int2* __restrict__ next,
-       unsigned long long* __restrict__ ctr) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  int kind = -1, nchild = 0;
-  int2 pr = make_int2(0, 0);
-  if (i < n) {
-    pr = fr[i];
-    classify(pr, cr, cc, theta, theta2, mutual, kind, nchild);
-  }
-  const unsigned bm = __ballot_sync(0xffffffffu, kind == 0);
-  const unsigned bp = __ballot_sync(0xffffffffu, kind == 1);
-  int incl = nchild;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  const int wtot = __shfl_sync(0xffffffffu, incl, 31);
-  unsigned long long base_m = 0, base_p = 0, base_c = 0;
-  if (lane == 0) {
-    if (bm) base_m = atomicAdd(&ctr[0], (unsigned long long)__popc(bm));
-    if (bp) base_p = atomicAdd(&ctr[1], (unsigned long long)__popc(bp));
-    if (wtot) base_c = atomicAdd(&ctr[2], (unsigned long long)wtot);
-  }
-  base_m = __shfl_sync(0xffffffffu, base_m, 0);
-  base_p = __shfl_sync(0xffffffffu, base_p, 0);
-  base_c = __shfl_sync(0xffffffffu, base_c, 0);
-  const unsigned lt = (1u << lane) - 1u;
-  const KeyT key = static_cast<KeyT>(((uint64_t)(uint32_t)pr.x << sbits) | (uint32_t)pr.y);
-  if (kind == 0) {
-    m2l_keys[base_m + __popc(bm & lt)] = key;
-  } else if (kind == 1) {
-    p2p_keys[base_p + __popc(bp & lt)] = key;
-  } else if (kind >= 2) {
-    int64_t q = (int64_t)base_c + incl - nchild;
-    if (kind == 2) {
-      const int32_t b = cb[pr.x];
-      for (int k = 0; k < nchild; ++k) next[q + k] = make_int2(b + k, pr.y);
-    } else if (kind == 3) {
-      const int32_t b = cb[pr.y];
-      for (int k = 0; k < nchild; ++k) next[q + k] = make_int2(pr.x, b + k);
-    } else {
-      const int32_t b = cb[pr.x], m = cc[pr.x];
-      for (int a = 0; a < m; ++a)
-        for (int c = a; c < m; ++c) next[q++] = make_int2(b + a, b + c);
+__global__ void __launch_bounds__(kStepThreads)
+k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, const int32_t* __restrict__ cc,
+       const int32_t* __restrict__ cb, double theta, double theta2, int mutual, int sbits, KeyT* __restrict__ m2l_keys,
+       KeyT* __restrict__ p2p_keys, int2* __restrict__ next, unsigned long long* __restrict__ ctr, int64_t cap_m,
+       int64_t cap_p, int64_t cap_f) {
+  using Scan = cub::BlockScan<unsigned long long, kStepThreads>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ unsigned long long sbase[3];
+  // a frontier that overflowed its buffer is only partially written (the run is flagged and
+  // repeated with larger buffers): read no further than the capacity
+  const int64_t n = min(static_cast<int64_t>(ctr[4 + level]), cap_f);
+  for (int64_t c0 = static_cast<int64_t>(blockIdx.x) * kStepChunk; c0 < n; c0 += static_cast<int64_t>(gridDim.x) * kStepChunk) {
+    int kind[kStepPer], nch[kStepPer];
+    int2 pr[kStepPer];
+    // packed per-thread counts: M2L (bits 0..20) | P2P (21..41) | children (42..63)
+    unsigned long long mine = 0;
+#pragma unroll
+    for (int j = 0; j < kStepPer; ++j) {
+      const int64_t i = c0 + j * kStepThreads + threadIdx.x;
+      kind[j] = -1;
+      nch[j] = 0;
+      pr[j] = make_int2(0, 0);
+      if (i < n) {
+        pr[j] = fr[i];
+        classify(pr[j], cr, cc, theta, theta2, mutual, kind[j], nch[j]);
+        mine += kind[j] == 0 ? 1ull : kind[j] == 1 ? (1ull << 21) : (static_cast<unsigned long long>(nch[j]) << 42);
+      }
     }
+    unsigned long long excl, tot;
+    Scan(scan_tmp).ExclusiveSum(mine, excl, tot);
+    if (threadIdx.x == 0) {
+      const unsigned long long tm = tot & 0x1fffffull, tp = (tot >> 21) & 0x1fffffull, tc = tot >> 42;
+      sbase[0] = tm ? atomicAdd(&ctr[0], tm) : 0ull;
+      sbase[1] = tp ? atomicAdd(&ctr[1], tp) : 0ull;
+      sbase[2] = tc ? atomicAdd(&ctr[4 + level + 1], tc) : 0ull;
+    }
+    __syncthreads();
+    int64_t om = static_cast<int64_t>(sbase[0] + (excl & 0x1fffffull));
+    int64_t op = static_cast<int64_t>(sbase[1] + ((excl >> 21) & 0x1fffffull));
+    int64_t oc = static_cast<int64_t>(sbase[2] + (excl >> 42));
+    bool over = false;
+#pragma unroll
+    for (int j = 0; j < kStepPer; ++j) {
+      const KeyT key = static_cast<KeyT>(((uint64_t)(uint32_t)pr[j].x << sbits) | (uint32_t)pr[j].y);
+      if (kind[j] == 0) {
+        if (om < cap_m) m2l_keys[om] = key; else over = true;
+        ++om;
+      } else if (kind[j] == 1) {
+        if (op < cap_p) p2p_keys[op] = key; else over = true;
+        ++op;
+      } else if (kind[j] >= 2) {
+        if (oc + nch[j] > cap_f) {
+          over = true;
+        } else if (kind[j] == 2) {
+          const int32_t b = cb[pr[j].x];
+          for (int k = 0; k < nch[j]; ++k) next[oc + k] = make_int2(b + k, pr[j].y);
+        } else if (kind[j] == 3) {
+          const int32_t b = cb[pr[j].y];
+          for (int k = 0; k < nch[j]; ++k) next[oc + k] = make_int2(pr[j].x, b + k);
+        } else {
+          const int32_t b = cb[pr[j].x], m = cc[pr[j].x];
+          int64_t q = oc;
+          for (int a = 0; a < m; ++a)
+            for (int c = a; c < m; ++c) next[q++] = make_int2(b + a, b + c);
+        }
+        oc += nch[j];
+      }
+    }
+    if (over) ctr[2] = 1ull;
+    __syncthreads();  // sbase / scan storage reuse
   }
 }
 
@@ -146,19 +178,6 @@ int bits_for(uint64_t v) {
   int b = 1;
   while (b < 63 && (v >> b)) ++b;
   return b;
-}
-
-template <class T>
-void grow_keep(fmm_ctx* c, DBuf<T>& buf, size_t used, size_t need) {
-  if (need <= buf.cap) return;
-  T* fresh = nullptr;
-  const size_t want = need + need / 2 + 1024;
-  CK(cudaMalloc(&fresh, want * sizeof(T)));
-  if (buf.p && used) CK(cudaMemcpyAsync(fresh, buf.p, used * sizeof(T), cudaMemcpyDeviceToDevice, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  if (buf.p) CK(cudaFree(buf.p));
-  buf.p = fresh;
-  buf.cap = want;
 }
 
 // Sorts packed (target, source) keys (2 * ceil(log2 ncells) bits) and splits them into CSR by
@@ -246,45 +265,66 @@ void traverse(fmm_ctx* c) {
   if (!(theta > 0.0 && theta < 1.0)) fail(FMM_ERR_THETA, "theta must be in (0,1)");
   cudaStream_t s = c->stream;
   const int mutual = c->cfg.mutual ? 1 : 0;
-  const int fan = mutual ? 36 : 8;  // max pairs pushed per pair
   const int sbits = bits_for(static_cast<uint64_t>(c->ncells));
   const bool small = small_keys(c->ncells);
-
-  int64_t nf = 1, nm = 0, np = 0;
-  const int2 root = make_int2(0, 0);
-  DBuf<int2>* fa = &c->pairs_a;
-  DBuf<int2>* fb = &c->pairs_d;
-  fa->ensure(1024);
-  CK(cudaMemcpyAsync(fa->p, &root, sizeof(int2), cudaMemcpyHostToDevice, s));
-  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(c->d_counters.ensure(8)) + 4;
+  // Every split descends the target or the source by one level (a mutual self split both), so
+  // the frontier is empty after at most 2 * depth + 1 levels.
+  const int nlev = 2 * c->depth + 2;
+  if (4 + nlev + 1 > 60) fail(FMM_ERR_UNSUPPORTED, "traverse: tree too deep");
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(c->trav_ctr.ensure(64));
   unsigned long long* h = reinterpret_cast<unsigned long long*>(c->hpin);
-  int launches = 0;
-  while (nf > 0) {
-    grow_keep(c, c->m2l_keys, nm, nm + nf);
-    grow_keep(c, c->p2p_keys, np, np + nf);
-    fb->ensure(fan * nf);
-    h[0] = nm;
-    h[1] = np;
-    h[2] = 0;
-    CK(cudaMemcpyAsync(ctr, h, 3 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
-    if (small)
-      k_step<<<ceil_div(nf, 256), 256, 0, s>>>(fa->p, nf, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
-                                               theta * theta, mutual, sbits, (uint32_t*)c->m2l_keys.p,
-                                               (uint32_t*)c->p2p_keys.p, fb->p, ctr);
-    else
-      k_step<<<ceil_div(nf, 256), 256, 0, s>>>(fa->p, nf, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
-                                               theta * theta, mutual, sbits, c->m2l_keys.p, c->p2p_keys.p, fb->p, ctr);
-    CK_LAUNCH("k_step");
-    CK(cudaMemcpyAsync(h + 4, ctr, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  // first call: capacities from the cell count; afterwards the buffers keep their size
+  const int64_t want_f = std::max<int64_t>(c->ncells * 256, 1 << 16);
+  const int64_t want_m = std::max<int64_t>(c->ncells * 512, 1 << 16);
+  const int64_t want_p = std::max<int64_t>(c->nleaves * 256, 1 << 16);
+  if (c->pairs_a.cap < static_cast<size_t>(want_f)) c->pairs_a.ensure(want_f);
+  if (c->pairs_d.cap < static_cast<size_t>(want_f)) c->pairs_d.ensure(want_f);
+  if (c->m2l_keys.cap < static_cast<size_t>(want_m)) c->m2l_keys.ensure(want_m);
+  if (c->p2p_keys.cap < static_cast<size_t>(want_p)) c->p2p_keys.ensure(want_p);
+  const int grid = 148 * (2048 / kStepThreads);
+  const int2 root = make_int2(0, 0);
+  for (int attempt = 0;; ++attempt) {
+    const int64_t cap_f = static_cast<int64_t>(std::min(c->pairs_a.cap, c->pairs_d.cap));
+    // KeyT buffers are uint64_t arrays; 32-bit keys use twice the count
+    const int64_t cap_m = static_cast<int64_t>(c->m2l_keys.cap) * (small ? 2 : 1);
+    const int64_t cap_p = static_cast<int64_t>(c->p2p_keys.cap) * (small ? 2 : 1);
+    CK(cudaMemsetAsync(ctr, 0, 64 * sizeof(unsigned long long), s));
+    const unsigned long long one = 1;
+    CK(cudaMemcpyAsync(ctr + 4, &one, sizeof(one), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(c->pairs_a.p, &root, sizeof(int2), cudaMemcpyHostToDevice, s));
+    for (int L = 0; L < nlev; ++L) {
+      const int2* fr = (L & 1) ? c->pairs_d.p : c->pairs_a.p;
+      int2* nx = (L & 1) ? c->pairs_a.p : c->pairs_d.p;
+      if (small)
+        k_step<<<grid, kStepThreads, 0, s>>>(L, fr, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
+                                             theta * theta, mutual, sbits, (uint32_t*)c->m2l_keys.p,
+                                             (uint32_t*)c->p2p_keys.p, nx, ctr, cap_m, cap_p, cap_f);
+      else
+        k_step<<<grid, kStepThreads, 0, s>>>(L, fr, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
+                                             theta * theta, mutual, sbits, c->m2l_keys.p, c->p2p_keys.p, nx, ctr,
+                                             cap_m, cap_p, cap_f);
+      CK_LAUNCH("k_step");
+    }
+    CK(cudaMemcpyAsync(h, ctr, (4 + nlev + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    ++launches;
-    nm = static_cast<int64_t>(h[4]);
-    np = static_cast<int64_t>(h[5]);
-    nf = static_cast<int64_t>(h[6]);
-    std::swap(fa, fb);
+    c->kernel_launches += nlev;
+    const int64_t nm = static_cast<int64_t>(h[0]), np = static_cast<int64_t>(h[1]);
+    int64_t fmax = 0;
+    for (int L = 0; L <= nlev; ++L) fmax = std::max<int64_t>(fmax, static_cast<int64_t>(h[4 + L]));
+    const bool unfinished = h[4 + nlev] != 0;
+    if (unfinished) fail(FMM_ERR_CUDA, "traverse: frontier not empty after 2*depth+2 levels");
+    if (h[2] == 0) {
+      finish_lists(c, nm, np);
+      return;
+    }
+    if (attempt > 0) fail(FMM_ERR_CUDA, "traverse: output overflow after regrow");
+    // grow to the exact sizes (+ slack) and run again
+    c->pairs_a.ensure(fmax + fmax / 8 + 1024);
+    c->pairs_d.ensure(fmax + fmax / 8 + 1024);
+    const int64_t div = small ? 2 : 1;
+    c->m2l_keys.ensure((nm + nm / 8 + 1024) / div + 1);
+    c->p2p_keys.ensure((np + np / 8 + 1024) / div + 1);
   }
-  c->kernel_launches += launches;
-  finish_lists(c, nm, np);
 }
 
 }  // namespace fmmb
