@@ -54,35 +54,70 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML polled every ~2 ms
+    from a thread (the handle is opened before the region starts), nvidia-smi -lms as fallback."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int = 0):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, set of reasons)
         self._stop = threading.Event()
         self._proc = None
+        self._nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._bits = {"hw_slowdown": pynvml.nvmlClocksThrottleReasonHwSlowdown,
+                          "hw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
+                          "sw_thermal_slowdown": pynvml.nvmlClocksThrottleReasonSwThermalSlowdown,
+                          "sw_power_cap": pynvml.nvmlClocksThrottleReasonSwPowerCap}
+        except Exception:
+            self._nv = None
+
+    def _poll_nvml(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+                self.samples.append((float(sm), float(self._max), {k for k, v in self._bits.items() if r & v}))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._poll_nvml, daemon=True)
+            self._t.start()
+            return self
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
             self._proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
                  "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t = threading.Thread(target=self._read_smi, daemon=True)
             self._t.start()
         except Exception:
             self._proc = None
         return self
 
-    def _read(self):
+    def _read_smi(self):
         for line in self._proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                self.samples.append(parts)
+            if len(parts) >= 6 and parts[0].replace(".", "").isdigit():
+                self.samples.append((float(parts[0]), float(parts[1]),
+                                     {self.NAMES[k] for k in range(4) if parts[2 + k] == "Active"}))
 
     def __exit__(self, *a):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join(timeout=1)
         if self._proc:
             self._proc.terminate()
             try:
@@ -92,13 +127,12 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[3 + k] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted(set().union(*[s[2] for s in self.samples]))
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml" if self._nv is not None else "nvidia-smi"}
 
 
 def flush_l2(buf):
@@ -327,6 +361,13 @@ def main():
     ctx.set_overlap(True)
     p2p_kernel = float(np.mean(iso_p2p))
     achieved = FLOPS_PER_PAIR * info.p2p_body_pairs / (p2p_kernel * 1e-3) / 1e12
+    # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f)["k_p2p_fp32"]["dram_bytes_per_launch"]
+    except Exception:
+        traffic = None
 
     # e2e through the C-ABI with host buffers (pinned), H2D + step + D2H in the timed region
     e2e = None
@@ -397,7 +438,8 @@ def main():
             "p2p_kernel_ms_overlapped": overlapped_p2p_ms, "m2l_kernel_ms_overlapped": float(np.mean(m2l_ms)),
             "overlap": "P2P on a second stream concurrent with upward+M2L in the timed steps",
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                         "frac": achieved / fp32_peak, "traffic": None,
+                         "frac": achieved / fp32_peak, "traffic": traffic,
+                         "traffic_unit": "bytes per launch (dram read + write, ncu --set full, C2)",
                          "kernel": "k_p2p_fp32", "flops_per_unit": FLOPS_PER_PAIR,
                          "timing": "CUDA events around the P2P launch, stages serialised (kernel alone), L2 flushed",
                          "peak_source": f"derived: {sms} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz "

@@ -32,3 +32,24 @@ for row in r[2:]:
     tot = sum(v for _, v in stalls) or 1
     print("  stalls:", ", ".join(f"{k.replace('smsp__pcsamp_warps_issue_stalled_', '')} {100 * v / tot:.0f}%"
                                  for k, v in sorted(stalls, key=lambda x: -x[1]) if v / tot > 0.02))
+
+# optional: per-kernel DRAM traffic of this capture as JSON (read by bench.py's roofline.traffic)
+if len(sys.argv) > 2:
+    import json
+    import re
+
+    def num(row, k):
+        v = row[h.index(k)].replace(",", "")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1.0, "us": 1e-3, "ns": 1e-6,
+                 "msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6}.get(units[h.index(k)], 1)
+        return float(v) * scale
+
+    out = {}
+    for row in r[2:]:
+        name = row[h.index("Kernel Name")]
+        m = re.search(r"(k_[a-z0-9_]+)", name)
+        key = m.group(1) if m else name[:40]
+        out[key] = {"dram_bytes_per_launch": num(row, "dram__bytes_read.sum") + num(row, "dram__bytes_write.sum"),
+                    "gpu_time_ms": num(row, "gpu__time_duration.sum"), "report": rep}
+    with open(sys.argv[2], "w") as f:
+        json.dump(out, f, indent=1)
