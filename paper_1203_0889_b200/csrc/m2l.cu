@@ -3,6 +3,7 @@
 #include <algorithm>
 
 #include "expansions.cuh"
+#include "tma.cuh"
 
 namespace fmmb {
 namespace {
@@ -159,6 +160,15 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
   extern __shared__ double smem[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* sR = smem + (size_t)w * 32 * S;  // per-warp source rows, then reduction rows
+  // rows of 16-B multiples arrive by one TMA bulk copy per lane on a per-warp mbarrier
+  constexpr bool kBulk = (N * 8) % 16 == 0;
+  __shared__ __align__(8) uint64_t bars[4];
+  if (kBulk && lane == 0) {
+    mbar_init(&bars[w], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  unsigned phase = 0;
   const int64_t wid = blockIdx.x * 4ll + w;
   if (wid >= ntargets) return;
   const int32_t t = targets[wid];
@@ -176,6 +186,9 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
     // stage this lane's source multipole (async; hidden behind the Dt recurrence)
     if (!valid) {
       for (int e = 0; e < N; ++e) sR[lane * S + e] = 0.0;  // tail lanes contribute nothing
+    } else if constexpr (kBulk) {
+      fence_proxy_async_smem();  // earlier generic reads of this row before the async write
+      bulk_g2s(sR + lane * S, M + (int64_t)s * N, N * 8, &bars[w]);
     } else {
       const char* row = reinterpret_cast<const char*>(M + (int64_t)s * N);
       const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(sR + lane * S));
@@ -189,7 +202,14 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + e), "l"(row + e));
       }
     }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    if constexpr (kBulk) {
+      if (lane == 0) {
+        const int64_t nv = l1 - base < 32 ? l1 - base : 32;
+        mbar_arrive_expect_tx(&bars[w], static_cast<unsigned>(nv * N * 8));
+      }
+    } else {
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
     if (base + 32 + lane < l1) s_next = src[base + 32 + lane];
     double rx = 1.0, ry = 0.0, rz = 0.0;
     if (valid) {
@@ -200,7 +220,12 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
     }
     double D[N];
     derivs_reg<P>(rx, ry, rz, D);
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if constexpr (kBulk) {
+      mbar_wait(&bars[w], phase);
+      phase ^= 1u;
+    } else {
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
     __syncwarp();
     const double* Ms = sR + lane * S;
     auto contract = [&](auto IA, const double m) {
