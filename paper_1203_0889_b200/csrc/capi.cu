@@ -473,6 +473,7 @@ int fmm_load_tree(fmm_ctx* c, int64_t ncells, const int32_t* level, const uint64
     c->wl = c->leaves.p;
     c->nwl = c->nleaves;
     c->shard_planned = false;
+    c->body_keys_valid = false;
     c->depth = depth;
     c->center[0] = center3[0];
     c->center[1] = center3[1];
@@ -537,6 +538,7 @@ int fmm_set_partition(fmm_ctx* c, int rank, int world) {
   if (!c) return FMM_ERR_ARG;
   return guard(c, [&] {
     if (world < 1 || rank < 0 || rank >= world) fail(FMM_ERR_ARG, "bad rank/world");
+    if (world != c->world) c->plan_world = 0;
     c->rank = rank;
     c->world = world;
     c->shard_planned = false;

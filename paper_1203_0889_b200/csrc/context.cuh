@@ -96,6 +96,16 @@ struct fmm_ctx {
   std::vector<int64_t> rank_cells_off;     // world + 1 offsets into rank_cells
   int64_t chunk_cells = 0;                 // max cells owned by a rank (exchange chunk)
   bool shard_planned = false;
+  // partition reuse: the first sharded step plans from its full lists (cost-balanced) and keeps
+  // the rank boundaries as Morton keys; later steps map them onto the new tree (snapped to leaf
+  // starts) and traverse only pairs whose target meets the rank's range
+  std::vector<uint64_t> plan_keys;         // world + 1 boundary keys
+  int plan_world = 0;                      // world the plan was made for (0 = none)
+  bool shard_from_plan = false;            // this step's bounds came from plan_keys
+  fmmb::DBuf<uint64_t> body_keys;          // sorted 63-bit body keys (tree order), sharded runs
+  bool body_keys_valid = false;
+  fmmb::DBuf<int64_t> shard_bounds;        // device copy of the world + 1 body bounds
+  int64_t trav_b0 = 0, trav_b1 = 0;        // traversal target filter [b0, b1)
 
   bool overlap = true;  // fmm_evaluate: P2P on stream2 concurrently with upward + M2L
 
@@ -122,6 +132,8 @@ void lists_from_pairs(fmm_ctx* c, const int2* d_m2l, int64_t n_m2l, const int2* 
                       int64_t n_p2p);
 // shard.cu
 void plan_shards(fmm_ctx* c);      // after the lists: partition, own leaves, owners
+bool shard_bounds_from_plan(fmm_ctx* c);  // before the traversal: bounds from the kept plan
+void shard_assign(fmm_ctx* c);     // owners, per-rank cell lists, own leaves from c->shard_bounds
 void shard_pack(fmm_ctx* c, double* d_send, cudaStream_t s);
 void shard_unpack(fmm_ctx* c, const double* d_recv, cudaStream_t s);
 void plan_partition_host(int64_t ncells, const int32_t* bb, const int32_t* be, const int32_t* cc,

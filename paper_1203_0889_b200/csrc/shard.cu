@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "context.cuh"
 
 namespace fmmb {
@@ -86,6 +88,77 @@ void plan_partition_host(int64_t ncells, const int32_t* bb, const int32_t* be, c
   }
 }
 
+namespace {
+
+// owner[i] = the rank whose body range contains cell i, -1 when it straddles ranks (or is empty)
+__global__ void k_owner(const int32_t* __restrict__ bb, const int32_t* __restrict__ be, int64_t ncells,
+                        const int64_t* __restrict__ bounds, int world, int32_t* __restrict__ owner,
+                        uint32_t* __restrict__ okey, int32_t* __restrict__ iota) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= ncells) return;
+  int32_t o = -1;
+  for (int q = 0; q < world; ++q)
+    if (bounds[q] <= bb[i] && be[i] <= bounds[q + 1] && bounds[q] < bounds[q + 1]) {
+      o = q;
+      break;
+    }
+  owner[i] = o;
+  okey[i] = static_cast<uint32_t>(o + 1);  // 0 = shared, q + 1 = rank q
+  iota[i] = static_cast<int32_t>(i);
+}
+
+// offsets of each rank's cells in the owner-sorted cell list
+__global__ void k_rank_offsets(const uint32_t* __restrict__ skey, int64_t ncells, int world, int64_t* __restrict__ off) {
+  const int q = threadIdx.x;
+  if (q > world) return;
+  int64_t lo = 0, hi = ncells;  // first index with key >= q + 1
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (skey[mid] < static_cast<uint32_t>(q + 1)) lo = mid + 1; else hi = mid;
+  }
+  off[q] = lo;
+}
+
+__global__ void k_flag_own_leaves(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __restrict__ owner,
+                                  int rank, int32_t* __restrict__ flag) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < nleaves) flag[k] = owner[leaves[k]] == rank;
+}
+
+// Morton boundary keys -> body bounds on this tree: first body whose key reaches the boundary,
+// snapped down to the start of its leaf (leaves never straddle ranks)
+__global__ void k_plan_bounds(const uint64_t* __restrict__ pk, int world, const uint64_t* __restrict__ keys, int64_t n,
+                              const int32_t* __restrict__ leaf_of_body, const int32_t* __restrict__ bb,
+                              int64_t* __restrict__ bounds) {
+  const int q = threadIdx.x;
+  if (q > world) return;
+  int64_t b;
+  if (q == 0) {
+    b = 0;
+  } else if (q == world) {
+    b = n;
+  } else {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < pk[q]) lo = mid + 1; else hi = mid;
+    }
+    b = lo < n ? bb[leaf_of_body[lo]] : n;
+  }
+  bounds[q] = b;
+}
+
+__global__ void k_bound_keys(const int64_t* __restrict__ bounds, int world, const uint64_t* __restrict__ keys, int64_t n,
+                             uint64_t* __restrict__ pk) {
+  const int q = threadIdx.x;
+  if (q > world) return;
+  pk[q] = bounds[q] < n ? keys[bounds[q]] : ~0ull;
+}
+
+}  // namespace
+
+// First sharded step: cost-balanced plan from this step's full lists; the bounds are kept as
+// Morton keys for the following steps.
 void plan_shards(fmm_ctx* c) {
   cudaStream_t s = c->stream;
   const int64_t nl = c->nleaves, nc = c->ncells;
@@ -106,37 +179,92 @@ void plan_shards(fmm_ctx* c) {
   CK(cudaStreamSynchronize(s));
   std::vector<double> cell_cost(nc, 0.0);
   for (int64_t k = 0; k < nl; ++k) cell_cost[hleaves[k]] = hcost[k];
-  // 2. host plan
+  // 2. host plan (bounds; owners are recomputed on the device by shard_assign)
   std::vector<int64_t> bounds(c->world + 1);
   std::vector<int32_t> owner(nc);
   plan_partition_host(nc, bb.data(), be.data(), cc.data(), cell_cost.data(), c->world, bounds.data(), owner.data());
-  // 3. own leaves, per-rank owned cell lists, chunk size
-  std::vector<int32_t> own_leaves;
-  for (int64_t k = 0; k < nl; ++k)
-    if (owner[hleaves[k]] == c->rank) own_leaves.push_back(hleaves[k]);
-  std::vector<int32_t> cells;
-  c->rank_cells_off.assign(c->world + 1, 0);
-  for (int q = 0; q < c->world; ++q) {
-    c->rank_cells_off[q] = static_cast<int64_t>(cells.size());
-    for (int64_t i = 0; i < nc; ++i)
-      if (owner[i] == q) cells.push_back(static_cast<int32_t>(i));
+  int64_t* dbounds = c->shard_bounds.ensure(c->world + 1);
+  CK(cudaMemcpyAsync(dbounds, bounds.data(), (c->world + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  // 3. keep the plan as Morton boundary keys (when this tree has its sorted keys)
+  if (c->body_keys_valid) {
+    uint64_t* dk = reinterpret_cast<uint64_t*>(c->small.p) + 0;  // cost buffer is consumed
+    k_bound_keys<<<1, 128, 0, s>>>(dbounds, c->world, c->body_keys.p, c->N, dk);
+    CK_LAUNCH("k_bound_keys");
+    c->plan_keys.assign(c->world + 1, 0);
+    CK(cudaMemcpyAsync(c->plan_keys.data(), dk, (c->world + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->plan_world = c->world;
   }
-  c->rank_cells_off[c->world] = static_cast<int64_t>(cells.size());
-  c->chunk_cells = 0;
-  for (int q = 0; q < c->world; ++q)
-    c->chunk_cells = std::max(c->chunk_cells, c->rank_cells_off[q + 1] - c->rank_cells_off[q]);
-  CK(cudaMemcpyAsync(c->owner.ensure(nc), owner.data(), nc * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(c->own_leaves.ensure(own_leaves.size() + 1), own_leaves.data(),
-                     own_leaves.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(c->rank_cells.ensure(cells.size() + 1), cells.data(), cells.size() * sizeof(int32_t),
-                     cudaMemcpyHostToDevice, s));
-  CK(cudaStreamSynchronize(s));  // host vectors leave scope
-  c->wl = c->own_leaves.p;
-  c->nwl = static_cast<int64_t>(own_leaves.size());
   c->shard_b0 = bounds[c->rank];
   c->shard_b1 = bounds[c->rank + 1];
-  c->shard_planned = true;
+  c->kernel_launches += 2;
+  shard_assign(c);
+}
+
+// Later sharded steps (before the traversal): the kept Morton boundaries mapped onto this tree.
+bool shard_bounds_from_plan(fmm_ctx* c) {
+  if (c->plan_world != c->world || !c->body_keys_valid || static_cast<int>(c->plan_keys.size()) != c->world + 1)
+    return false;
+  cudaStream_t s = c->stream;
+  uint64_t* dk = reinterpret_cast<uint64_t*>(c->small.ensure(2 * (c->world + 1) + 8));
+  CK(cudaMemcpyAsync(dk, c->plan_keys.data(), (c->world + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  int64_t* dbounds = c->shard_bounds.ensure(c->world + 1);
+  k_plan_bounds<<<1, 128, 0, s>>>(dk, c->world, c->body_keys.p, c->N, c->leaf_of_body.p, c->c_body_begin.p, dbounds);
+  CK_LAUNCH("k_plan_bounds");
+  int64_t* h = c->hpin;
+  CK(cudaMemcpyAsync(h, dbounds + c->rank, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  c->shard_b0 = h[0];
+  c->shard_b1 = h[1];
   c->kernel_launches += 1;
+  return true;
+}
+
+// Owners, every rank's owned-cell list (ascending cell index), own leaves and the exchange chunk
+// size, all from c->shard_bounds on the device.
+void shard_assign(fmm_ctx* c) {
+  cudaStream_t s = c->stream;
+  const int64_t nc = c->ncells, nl = c->nleaves;
+  const int world = c->world;
+  int32_t* owner = c->owner.ensure(nc);
+  uint32_t* okey = reinterpret_cast<uint32_t*>(c->i32_a.ensure(2 * (nc + 1)));
+  uint32_t* okey_s = okey + (nc + 1);
+  int32_t* iota = c->i32_b.ensure(nc + 1);
+  int32_t* cells = c->rank_cells.ensure(nc + 1);
+  k_owner<<<ceil_div(nc, 256), 256, 0, s>>>(c->c_body_begin.p, c->c_body_end.p, nc, c->shard_bounds.p, world, owner,
+                                            okey, iota);
+  CK_LAUNCH("k_owner");
+  int end_bit = 1;
+  while ((1 << end_bit) <= world) ++end_bit;
+  size_t sb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, sb, okey, okey_s, iota, cells, (int)nc, 0, end_bit, s));
+  CK(cub::DeviceRadixSort::SortPairs(temp_storage(c, sb), sb, okey, okey_s, iota, cells, (int)nc, 0, end_bit, s));
+  int64_t* doff = c->scan_a.ensure(world + 2);
+  k_rank_offsets<<<1, 128, 0, s>>>(okey_s, nc, world, doff);
+  CK_LAUNCH("k_rank_offsets");
+  // own leaves (ascending cell index)
+  int32_t* flag = c->i32_c.ensure(nl + 1);
+  k_flag_own_leaves<<<ceil_div(nl, 256), 256, 0, s>>>(c->leaves.p, nl, owner, c->rank, flag);
+  CK_LAUNCH("k_flag_own_leaves");
+  int32_t* own = c->own_leaves.ensure(nl + 1);
+  int64_t* nsel = c->d_counters.ensure(32) + 2;
+  sb = 0;
+  CK(cub::DeviceSelect::Flagged(nullptr, sb, c->leaves.p, flag, own, nsel, (int)nl, s));
+  CK(cub::DeviceSelect::Flagged(temp_storage(c, sb), sb, c->leaves.p, flag, own, nsel, (int)nl, s));
+  int64_t* h = c->hpin;
+  CK(cudaMemcpyAsync(h, doff, (world + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h + world + 1, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // rank_cells_off[q] = start of rank q's cells in the owner-sorted list (shared cells sort first)
+  c->rank_cells_off.assign(world + 1, 0);
+  for (int q = 0; q <= world; ++q) c->rank_cells_off[q] = h[q];
+  c->chunk_cells = 0;
+  for (int q = 0; q < world; ++q)
+    c->chunk_cells = std::max(c->chunk_cells, c->rank_cells_off[q + 1] - c->rank_cells_off[q]);
+  c->wl = own;
+  c->nwl = h[world + 1];
+  c->shard_planned = true;
+  c->kernel_launches += 5;
 }
 
 void shard_pack(fmm_ctx* c, double* d_send, cudaStream_t s) {

@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(kStepThreads)
 k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, const int32_t* __restrict__ cc,
        const int32_t* __restrict__ cb, double theta, double theta2, int mutual, int sbits, KeyT* __restrict__ m2l_keys,
        KeyT* __restrict__ p2p_keys, int2* __restrict__ next, unsigned long long* __restrict__ ctr, int64_t cap_m,
-       int64_t cap_p, int64_t cap_f) {
+       int64_t cap_p, int64_t cap_f, const int32_t* __restrict__ bb, const int32_t* __restrict__ be, int32_t tb0,
+       int32_t tb1, int filter) {
   using Scan = cub::BlockScan<unsigned long long, kStepThreads>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ unsigned long long sbase[3];
@@ -100,6 +101,12 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
       if (i < n) {
         pr[j] = fr[i];
         classify(pr[j], cr, cc, theta, theta2, mutual, kind[j], nch[j]);
+        if (filter && kind[j] == 2) {  // sharded: keep only target children meeting [tb0, tb1)
+          const int32_t b = cb[pr[j].x];
+          int kept = 0;
+          for (int q = 0; q < nch[j]; ++q) kept += (bb[b + q] < tb1 && be[b + q] > tb0) ? 1 : 0;
+          nch[j] = kept;
+        }
         mine += kind[j] == 0 ? 1ull : kind[j] == 1 ? (1ull << 21) : (static_cast<unsigned long long>(nch[j]) << 42);
       }
     }
@@ -130,7 +137,13 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
           over = true;
         } else if (kind[j] == 2) {
           const int32_t b = cb[pr[j].x];
-          for (int k = 0; k < nch[j]; ++k) next[oc + k] = make_int2(b + k, pr[j].y);
+          if (filter) {
+            int64_t q = oc;
+            for (int k = 0; k < cc[pr[j].x]; ++k)
+              if (bb[b + k] < tb1 && be[b + k] > tb0) next[q++] = make_int2(b + k, pr[j].y);
+          } else {
+            for (int k = 0; k < nch[j]; ++k) next[oc + k] = make_int2(b + k, pr[j].y);
+          }
         } else if (kind[j] == 3) {
           const int32_t b = cb[pr[j].y];
           for (int k = 0; k < nch[j]; ++k) next[oc + k] = make_int2(pr[j].x, b + k);
@@ -235,7 +248,8 @@ void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
   c->n_p2p = n_p2p;
   // partition (sharded runs), then the M2L target list of this rank
   if (c->world > 1) {
-    plan_shards(c);
+    if (c->shard_from_plan) shard_assign(c);  // bounds already mapped from the kept plan
+    else plan_shards(c);                      // full lists: plan from this step's costs
   } else {
     c->shard_b0 = 0;
     c->shard_b1 = c->N;
@@ -283,6 +297,11 @@ void traverse(fmm_ctx* c) {
   if (c->p2p_keys.cap < static_cast<size_t>(want_p)) c->p2p_keys.ensure(want_p);
   const int grid = 148 * (2048 / kStepThreads);
   const int2 root = make_int2(0, 0);
+  // sharded steps after the first: targets restricted to the rank's range (kept plan)
+  c->shard_from_plan = c->world > 1 && shard_bounds_from_plan(c);
+  const int filter = c->shard_from_plan ? 1 : 0;
+  const int32_t tb0 = static_cast<int32_t>(filter ? c->shard_b0 : 0);
+  const int32_t tb1 = static_cast<int32_t>(filter ? c->shard_b1 : c->N);
   for (int attempt = 0;; ++attempt) {
     const int64_t cap_f = static_cast<int64_t>(std::min(c->pairs_a.cap, c->pairs_d.cap));
     // KeyT buffers are uint64_t arrays; 32-bit keys use twice the count
@@ -298,11 +317,13 @@ void traverse(fmm_ctx* c) {
       if (small)
         k_step<<<grid, kStepThreads, 0, s>>>(L, fr, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
                                              theta * theta, mutual, sbits, (uint32_t*)c->m2l_keys.p,
-                                             (uint32_t*)c->p2p_keys.p, nx, ctr, cap_m, cap_p, cap_f);
+                                             (uint32_t*)c->p2p_keys.p, nx, ctr, cap_m, cap_p, cap_f,
+                                             c->c_body_begin.p, c->c_body_end.p, tb0, tb1, filter);
       else
         k_step<<<grid, kStepThreads, 0, s>>>(L, fr, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
                                              theta * theta, mutual, sbits, c->m2l_keys.p, c->p2p_keys.p, nx, ctr,
-                                             cap_m, cap_p, cap_f);
+                                             cap_m, cap_p, cap_f, c->c_body_begin.p, c->c_body_end.p, tb0, tb1,
+                                             filter);
       CK_LAUNCH("k_step");
     }
     CK(cudaMemcpyAsync(h, ctr, (4 + nlev + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));

@@ -318,6 +318,12 @@ void build_tree(fmm_ctx* c) {
   CK(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, keys, skeys, idx, sidx, (int)n, 0, 3 * kLevels, s));
   void* tmp = temp_storage(c, tbytes);
   CK(cub::DeviceRadixSort::SortPairs(tmp, tbytes, keys, skeys, idx, sidx, (int)n, 0, 3 * kLevels, s));
+  if (c->world > 1) {  // partition reuse maps Morton boundaries onto this tree (shard.cu)
+    CK(cudaMemcpyAsync(c->body_keys.ensure(n), skeys, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    c->body_keys_valid = true;
+  } else {
+    c->body_keys_valid = false;
+  }
 
   // 4. level-by-level cell materialisation
   auto ensure_cells = [&](size_t used, size_t need) {

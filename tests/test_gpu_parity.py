@@ -372,47 +372,58 @@ def test_sharded_step_emulated(fmmlib, world):
     """The multi-GPU data path with `world` ranks emulated sequentially on one GPU (no rank waits
     on another): per-rank partition, local upward, the all-gather as a concatenation of the
     equal-size chunks, shared ancestors, then M2L/P2P/downward; the union of the ranks' own body
-    ranges reproduces the single-context step."""
+    ranges reproduces the single-context step. Two steps: the first plans the partition from its
+    full lists, the second reuses it (Morton boundaries) with a target-filtered traversal."""
     import torch
     fb = fmmlib
     bodies = fb.generate_bodies(3, 60000, 21)
     for precision, tol in (("fp64", 1e-12), ("fp32", 1e-6)):
         full = run_gpu(fb, bodies, 64, 6, 0.5, precision)
         phi_full, acc_full = full.results("tree")
-        ctxs, sends, infos = [], [], []
+        n_m2l_full = full.tree_info().n_m2l
+        ctxs = []
         for r in range(world):
             ctx = fb.Context(order=6, n_crit=64, theta=0.5, precision=precision)
             ctx.set_bodies(bodies)
             ctx.set_partition(r, world)
-            ctx.build_tree()
-            ctx.traverse()
-            info = ctx.shard_info()
-            send = _DevBuf(max(info.chunk_doubles, 1))
-            ctx.upward_local(send.ptr)
-            ctx.synchronize()
             ctxs.append(ctx)
-            sends.append(send)
-            infos.append((info.body_begin, info.body_end, info.chunk_doubles))
-        assert len({i[2] for i in infos}) == 1  # equal chunks on every rank
-        assert infos[0][0] == 0 and infos[-1][1] == len(bodies)
-        for a, b in zip(infos, infos[1:]):
-            assert a[1] == b[0]
-        recv = _DevBuf(1)
-        recv.t = torch.cat([s.t for s in sends])
-        recv.ptr = recv.t.data_ptr()
-        torch.cuda.synchronize()
-        phi = np.zeros_like(phi_full)
-        acc = np.zeros_like(acc_full)
-        for r, ctx in enumerate(ctxs):
-            ctx.upward_finish(recv.ptr)
-            ctx.reset_accumulators()
-            ctx.m2l()
-            ctx.p2p()
-            ctx.downward()
-            p_r, a_r = ctx.results("tree")
-            b0, b1, _ = infos[r]
-            phi[b0:b1] = p_r[b0:b1]
-            acc[b0:b1] = a_r[b0:b1]
+        bounds_seen = []
+        for step in range(2):
+            sends, infos = [], []
+            for ctx in ctxs:
+                ctx.build_tree()
+                ctx.traverse()
+                info = ctx.shard_info()
+                send = _DevBuf(max(info.chunk_doubles, 1))
+                ctx.upward_local(send.ptr)
+                ctx.synchronize()
+                sends.append(send)
+                infos.append((info.body_begin, info.body_end, info.chunk_doubles))
+            assert len({i[2] for i in infos}) == 1  # equal chunks on every rank
+            assert infos[0][0] == 0 and infos[-1][1] == len(bodies)
+            for a, b in zip(infos, infos[1:]):
+                assert a[1] == b[0]
+            bounds_seen.append([i[:2] for i in infos])
+            if step == 1:  # filtered traversal: each rank holds only lists of targets meeting its range
+                assert max(c.tree_info().n_m2l for c in ctxs) < n_m2l_full
+            recv = _DevBuf(1)
+            recv.t = torch.cat([s.t for s in sends])
+            recv.ptr = recv.t.data_ptr()
+            torch.cuda.synchronize()
+            phi = np.zeros_like(phi_full)
+            acc = np.zeros_like(acc_full)
+            for r, ctx in enumerate(ctxs):
+                ctx.upward_finish(recv.ptr)
+                ctx.reset_accumulators()
+                ctx.m2l()
+                ctx.p2p()
+                ctx.downward()
+                p_r, a_r = ctx.results("tree")
+                b0, b1, _ = infos[r]
+                phi[b0:b1] = p_r[b0:b1]
+                acc[b0:b1] = a_r[b0:b1]
+            assert rel_l2(phi, phi_full) < tol, (precision, step, rel_l2(phi, phi_full))
+            assert rel_l2(acc, acc_full) < tol, (precision, step, rel_l2(acc, acc_full))
+        assert bounds_seen[0] == bounds_seen[1]  # the kept plan maps back onto the same leaves
+        for ctx in ctxs:
             ctx.close()
-        assert rel_l2(phi, phi_full) < tol, (precision, rel_l2(phi, phi_full))
-        assert rel_l2(acc, acc_full) < tol, (precision, rel_l2(acc, acc_full))
