@@ -427,3 +427,69 @@ def test_sharded_step_emulated(fmmlib, world):
         assert bounds_seen[0] == bounds_seen[1]  # the kept plan maps back onto the same leaves
         for ctx in ctxs:
             ctx.close()
+
+
+@pytest.mark.gpu
+def test_sharded_step_threads(fmmlib):
+    """fmm.sharded_step (the bench's multi-GPU step) driven by two host threads on one GPU, one
+    context per rank; the all-gather is a host-side rendezvous (device synchronised, chunks
+    concatenated), so no kernel ever waits on another rank. Three steps: the first plans the
+    partition, the later ones reuse it. The union of the ranks' ranges matches one context."""
+    import threading
+
+    import torch
+    fb = fmmlib
+    world = 2
+    bodies = fb.generate_bodies(2, 50000, 5)
+    full = run_gpu(fb, bodies, 64, 6, 0.5, "fp32")
+    phi_full, acc_full = full.results("tree")
+    barrier = threading.Barrier(world)
+    sends = [None] * world
+    out = [None] * world
+    errors = []
+
+    class Buf:
+        def __init__(self, k):
+            self.t = torch.zeros(int(k), dtype=torch.float64, device="cuda")
+            self.ptr = self.t.data_ptr()
+
+    def worker(rank):
+        try:
+            ctx = fb.Context(order=6, n_crit=64, theta=0.5, precision="fp32")
+
+            def all_gather(recv, send):
+                torch.cuda.synchronize()
+                sends[rank] = send.t
+                barrier.wait()
+                recv.t.copy_(torch.cat(sends))
+                torch.cuda.synchronize()
+                barrier.wait()
+
+            res = []
+            for _ in range(3):
+                ctx.set_bodies(bodies)
+                info = fb.fmm.sharded_step(ctx, rank, world, all_gather, Buf)
+                p, a = ctx.results("tree")
+                res.append((int(info.body_begin), int(info.body_end), p, a))
+            out[rank] = res
+            ctx.close()
+        except Exception as e:  # surfaced below
+            errors.append(e)
+            barrier.abort()
+
+    ths = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errors, errors
+    for step in range(3):
+        phi = np.zeros_like(phi_full)
+        acc = np.zeros_like(acc_full)
+        for r in range(world):
+            b0, b1, p, a = out[r][step]
+            phi[b0:b1] = p[b0:b1]
+            acc[b0:b1] = a[b0:b1]
+        assert out[0][step][1] == out[1][step][0] and out[1][step][1] == len(bodies)
+        assert rel_l2(phi, phi_full) < 1e-6, (step, rel_l2(phi, phi_full))
+        assert rel_l2(acc, acc_full) < 1e-6, (step, rel_l2(acc, acc_full))
