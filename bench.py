@@ -338,6 +338,9 @@ def main():
     d_bodies = torch.from_numpy(bodies).cuda()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     ctx.set_bodies_device(d_bodies.data_ptr(), n)
+    # stages serialised on one stream: the measured P2P || (upward + M2L) two-stream overlap
+    # gained nothing (the kernels cannot co-reside: P2P fills registers/smem of every SM)
+    ctx.set_overlap(False)
 
     for _ in range(args.warmup):
         ctx.evaluate()
@@ -370,25 +373,13 @@ def main():
     ms_per_step = total_ms / args.steps
     value = inter * world / (ms_per_step * 1e-3)
 
-    # roofline: the P2P kernel, FP32 pipe (20 flops per body pair). In the timed steps P2P runs
-    # concurrently with the FP64 upward/M2L chain, so its duration there includes sharing the SMs;
-    # the roofline uses a second pass with the stages serialised (each kernel alone).
+    # roofline: the P2P kernel, FP32 pipe (20 flops per body pair), CUDA events around its
+    # launch inside the timed steps (stages serialised, so the kernel runs alone)
     peaks = load_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     fp32_peak = sms * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s
-    overlapped_p2p_ms = float(np.mean(p2p_ms))
-    ctx.set_overlap(False)
-    iso_p2p, iso_m2l = [], []
-    for _ in range(max(3, min(args.steps, 10))):
-        flush_l2(flush)
-        torch.cuda.synchronize()
-        ctx.evaluate()
-        t = ctx.stage_times()
-        iso_p2p.append(t.p2p_kernel_ms)
-        iso_m2l.append(t.m2l_kernel_ms)
-    ctx.set_overlap(True)
-    p2p_kernel = float(np.mean(iso_p2p))
+    p2p_kernel = float(np.mean(p2p_ms))
     achieved = FLOPS_PER_PAIR * info.p2p_body_pairs / (p2p_kernel * 1e-3) / 1e12
     # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
     traffic = None
@@ -463,14 +454,12 @@ def main():
             "m2l_pairs": int(info.n_m2l), "p2p_pairs_per_s": info.p2p_body_pairs / (ms_per_step * 1e-3),
             "m2l_pairs_per_s": info.n_m2l / (ms_per_step * 1e-3),
             "stage_ms": {k: v / args.steps for k, v in stage_acc.items()},
-            "p2p_kernel_ms": p2p_kernel, "m2l_kernel_ms": float(np.mean(iso_m2l)),
-            "p2p_kernel_ms_overlapped": overlapped_p2p_ms, "m2l_kernel_ms_overlapped": float(np.mean(m2l_ms)),
-            "overlap": "P2P on a second stream concurrent with upward+M2L in the timed steps",
+            "p2p_kernel_ms": p2p_kernel, "m2l_kernel_ms": float(np.mean(m2l_ms)),
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                          "frac": achieved / fp32_peak, "traffic": traffic,
                          "traffic_unit": "bytes per launch (dram read + write, ncu --set full, C2)",
                          "kernel": "k_p2p_fp32", "flops_per_unit": FLOPS_PER_PAIR,
-                         "timing": "CUDA events around the P2P launch, stages serialised (kernel alone), L2 flushed",
+                         "timing": "CUDA events around the P2P launch in the timed steps (stages serialised), L2 flushed",
                          "peak_source": f"derived: {sms} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz "
                                         "(sm_max_mhz of MEASURED_PEAKS.json; FFMA microbenchmark "
                                         "measured 126-128 lane-ops/clk/SM)"},
