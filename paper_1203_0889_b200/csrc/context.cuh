@@ -65,6 +65,7 @@ struct fmm_ctx {
 
   // expansions and outputs
   fmmb::DBuf<double> M, L;
+  fmmb::DBuf<double> m2l_mt;          // detraced multipoles (p <= 6 kernel)
   fmmb::DBuf<double> m2l_scratch;     // per-warp-slot partial Lambda rows (p >= 7 kernel)
   fmmb::DBuf<double> phi, acc;
   fmmb::DBuf<double> phi_p2p, acc_p2p;  // near-field part (tree order)

@@ -104,108 +104,179 @@ k_m2l_big(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
 }
 
 // ---------------------------------------------------------------- register M2L (p <= 6) ----
-// Dt_g = g! D_g = d^g(1/|R|) computed in registers by the reference's degree recurrence
-// rescaled by g! (multi_index.cpp:64-83 times g!):
-//   n r^2 Dt_g = -(2n-1) sum_d g_d r_d Dt_{g-e_d} - (n-1) sum_d g_d (g_d - 1) Dt_{g-2e_d},
-// every index and coefficient a compile-time constant; then the fully unrolled folded
-// contraction Lambda_b += M_a Dt_{a+b} with Lambda in registers (one FMA per term). Lane =
-// source, warp = target; the lane partials are reduced through shared memory per target.
-// Row stride (doubles) of the staged multipoles: even (16-B aligned rows for cp.async) with an
-// odd half, so a quarter-warp's LDS.128 of 8 distinct rows hits 8 distinct bank groups.
-constexpr int m2l_row_stride(int n) {
-  int s = n + (n & 1);
-  return (s / 2) % 2 == 1 ? s : s + 2;
+// Harmonic (traceless) reduction. Dt_g = g! D_g = d^g(1/|R|) is harmonic, so
+//   Dt_{g+2ex} + Dt_{g+2ey} + Dt_{g+2ez} = 0   (R != 0),
+// which makes every index with c >= 2 a combination of same-degree indices with smaller c.
+//  * Source side: M_a Dt_{a+b} with a_c >= 2 equals -M_a Dt_{(a-2ez+2ex)+b} - M_a Dt_{(a-2ez+2ey)+b}
+//    for every b, so each multipole is folded once ("detraced", k_detrace) onto the p^2
+//    indices with a_c <= 1, exactly (the fold is linear and independent of b and R).
+//  * Target side: Lambda_b = sum_a M'_a Dt_{a+b} inherits the identity in b (the truncation
+//    |a| + |b| <= p-1 depends on |b| only), so Lambda is contracted for b_c <= 1 and the c >= 2
+//    entries are filled afterwards: Lambda_{a,b,c} = -Lambda_{a+2,b,c-2} - Lambda_{a,b+2,c-2}.
+//  * Only Dt_g with g_c <= 2 then appear (the recurrence for them never leaves that set).
+// p = 6: 301 contraction terms instead of 462, 46 derivatives instead of 56, 36 accumulators
+// instead of 56 (the register budget limits this kernel's occupancy). The folded arithmetic
+// differs from the reference's only by rounding.
+template <int P>
+struct HM {
+  static constexpr int N = n_coef(P);
+  struct Tab {
+    int na, ng;
+    int a_full[N], a_of[N], g_of[N];
+  };
+  static constexpr Tab make() {
+    Tab t{};
+    t.na = 0;
+    t.ng = 0;
+    for (int i = 0; i < N; ++i) {
+      t.a_of[i] = -1;
+      t.g_of[i] = -1;
+      const int c = MI<P>::ec(i);
+      if (c <= 1) {
+        t.a_of[i] = t.na;
+        t.a_full[t.na++] = i;
+      }
+      if (c <= 2) t.g_of[i] = t.ng++;
+    }
+    return t;
+  }
+  static constexpr Tab tab = make();
+  static constexpr int NA = tab.na, NG = tab.ng;
+  static constexpr int a_full(int k) { return tab.a_full[k]; }
+  static constexpr int a_of(int i) { return tab.a_of[i]; }
+  static constexpr int g_of(int i) { return tab.g_of[i]; }
+};
+
+// M' = detraced multipoles (HM<P>::NA per cell, compact a_c <= 1 order); thread per cell
+template <int P>
+__global__ void k_detrace(const double* __restrict__ M, int64_t ncells, double* __restrict__ Mt) {
+  using T = MI<P>;
+  using H = HM<P>;
+  constexpr int N = T::N;
+  const int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (cell >= ncells) return;
+  double m[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) m[i] = M[cell * N + i];
+  // fold the c >= 2 entries onto c - 2, highest c first
+  static_for<P>([&](auto K) {
+    constexpr int c = P - 1 - decltype(K)::value;
+    if constexpr (c >= 2) {
+      static_for<N>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        if constexpr (T::ec(i) == c) {
+          constexpr int a = T::ea(i), b = T::eb(i);
+          m[index_of(a + 2, b, c - 2)] -= m[i];
+          m[index_of(a, b + 2, c - 2)] -= m[i];
+        }
+      });
+    }
+  });
+  static_for<H::NA>([&](auto K) {
+    constexpr int k = decltype(K)::value;
+    Mt[cell * H::NA + k] = m[H::a_full(k)];
+  });
 }
 
+// Dt_g for g_c <= 2 (compact HM::g_of order) by the reference's degree recurrence
+// (multi_index.cpp:64-83) rescaled by g!:
+//   n r^2 Dt_g = -(2n-1) sum_d g_d r_d Dt_{g-e_d} - (n-1) sum_d g_d (g_d - 1) Dt_{g-2e_d},
+// every index and coefficient a compile-time constant, all in registers.
 template <int P>
-__device__ __forceinline__ void derivs_reg(double rx, double ry, double rz, double (&D)[MI<P>::N]) {
+__device__ __forceinline__ void derivs_reg(double rx, double ry, double rz, double (&D)[HM<P>::NG]) {
   using T = MI<P>;
+  using H = HM<P>;
   const double r2 = (rx * rx + ry * ry) + rz * rz;
   D[0] = rsqrt(r2);
   const double inv_r2 = D[0] * D[0];
-  double rk[3][P];  // k * r_d
-#pragma unroll
-  for (int k = 0; k < P; ++k) {
-    rk[0][k] = double(k) * rx;
-    rk[1][k] = double(k) * ry;
-    rk[2][k] = double(k) * rz;
-  }
   double an[P];  // -(2n-1)/(n r^2); the s2 weight -(n-1)/(n r^2) = an * (n-1)/(2n-1) is folded
 #pragma unroll
   for (int n = 1; n < P; ++n) an[n] = (-double(2 * n - 1) / double(n)) * inv_r2;
   static_for<T::N>([&](auto I) {
     constexpr int i = decltype(I)::value;
-    if constexpr (i > 0) {
-      constexpr int a = T::ea(i), b = T::eb(i), c = T::ec(i), n = T::deg(i);
+    constexpr int a = T::ea(i), b = T::eb(i), c = T::ec(i), n = T::deg(i);
+    if constexpr (i > 0 && c <= 2) {
       constexpr double cn = double(n - 1) / double(2 * n - 1);
       double acc = 0.0;
-      if constexpr (a >= 1) acc = fma(rk[0][a], D[index_of(a - 1, b, c)], acc);
-      if constexpr (b >= 1) acc = fma(rk[1][b], D[index_of(a, b - 1, c)], acc);
-      if constexpr (c >= 1) acc = fma(rk[2][c], D[index_of(a, b, c - 1)], acc);
-      if constexpr (a >= 2) acc = fma(double(a * (a - 1)) * cn, D[index_of(a - 2, b, c)], acc);
-      if constexpr (b >= 2) acc = fma(double(b * (b - 1)) * cn, D[index_of(a, b - 2, c)], acc);
-      if constexpr (c >= 2) acc = fma(double(c * (c - 1)) * cn, D[index_of(a, b, c - 2)], acc);
-      D[i] = an[n] * acc;
+      if constexpr (a >= 1) acc = fma(double(a) * rx, D[H::g_of(index_of(a - 1, b, c))], acc);
+      if constexpr (b >= 1) acc = fma(double(b) * ry, D[H::g_of(index_of(a, b - 1, c))], acc);
+      if constexpr (c >= 1) acc = fma(double(c) * rz, D[H::g_of(index_of(a, b, c - 1))], acc);
+      if constexpr (a >= 2) acc = fma(double(a * (a - 1)) * cn, D[H::g_of(index_of(a - 2, b, c))], acc);
+      if constexpr (b >= 2) acc = fma(double(b * (b - 1)) * cn, D[H::g_of(index_of(a, b - 2, c))], acc);
+      if constexpr (c >= 2) acc = fma(double(c * (c - 1)) * cn, D[H::g_of(index_of(a, b, c - 2))], acc);
+      D[H::g_of(i)] = an[n] * acc;
     }
   });
 }
 
+// Row stride (doubles) of the staged rows: even (16-B aligned rows) with an odd half, so a
+// quarter-warp's LDS.128 of 8 distinct rows hits 8 distinct bank groups.
+constexpr int m2l_row_stride(int n) {
+  int s = n + (n & 1);
+  return (s / 2) % 2 == 1 ? s : s + 2;
+}
+
+// Lane = source, warp = target. Dt (g_c <= 2) in registers; the contraction
+// Lambda_b += M'_a Dt_{a+b} over a_c, b_c <= 1 (one FMA per term) with Lambda in registers. Each
+// lane's detraced source row arrives by one TMA bulk copy (8-byte cp.async when the row is not
+// a 16-byte multiple) on a per-warp mbarrier while the recurrence runs; one shared-memory
+// transpose reduction per target, then the c >= 2 entries of Lambda by the trace identity.
+#ifndef FMM_M2L_MINB
+#define FMM_M2L_MINB 10
+#endif
+#ifndef FMM_M2L_WARPS
+#define FMM_M2L_WARPS 1
+#endif
+constexpr int kM2LWarps = FMM_M2L_WARPS;  // warps (targets) per CTA
 template <int P>
-__global__ void __launch_bounds__(128, 2)
+__global__ void __launch_bounds__(32 * kM2LWarps, FMM_M2L_MINB)
 k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* __restrict__ off,
-          const int32_t* __restrict__ src, const double4* __restrict__ cr, const double* __restrict__ M,
+          const int32_t* __restrict__ src, const double4* __restrict__ cr, const double* __restrict__ Mt,
           double* __restrict__ L) {
   using T = MI<P>;
-  constexpr int N = T::N, S = m2l_row_stride(N);
+  using H = HM<P>;
+  constexpr int N = T::N, NA = H::NA, NG = H::NG, S = m2l_row_stride(NA);
   extern __shared__ double smem[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* sR = smem + (size_t)w * 32 * S;  // per-warp source rows, then reduction rows
-  // rows of 16-B multiples arrive by one TMA bulk copy per lane on a per-warp mbarrier
-  constexpr bool kBulk = (N * 8) % 16 == 0;
-  __shared__ __align__(8) uint64_t bars[4];
+  constexpr bool kBulk = (NA * 8) % 16 == 0;
+  __shared__ __align__(8) uint64_t bars[kM2LWarps];
   if (kBulk && lane == 0) {
     mbar_init(&bars[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncwarp();
   unsigned phase = 0;
-  const int64_t wid = blockIdx.x * 4ll + w;
+  const int64_t wid = blockIdx.x * (int64_t)kM2LWarps + w;
   if (wid >= ntargets) return;
   const int32_t t = targets[wid];
   const double4 ct = cr[t];
   const int64_t l0 = off[t], l1 = off[t + 1];
-  double lam[N];
+  double lam[NA];
 #pragma unroll
-  for (int i = 0; i < N; ++i) lam[i] = 0.0;
-  static_assert((N * 8) % 16 == 0 || N % 2 == 1, "row copy granularity");
+  for (int i = 0; i < NA; ++i) lam[i] = 0.0;
   int32_t s_next = (l0 + lane < l1) ? src[l0 + lane] : t;
   for (int64_t base = l0; base < l1; base += 32) {
     const int64_t k = base + lane;
     const bool valid = k < l1;
     const int32_t s = s_next;
-    // stage this lane's source multipole (async; hidden behind the Dt recurrence)
+    // stage this lane's detraced source multipole (async; hidden behind the Dt recurrence)
     if (!valid) {
-      for (int e = 0; e < N; ++e) sR[lane * S + e] = 0.0;  // tail lanes contribute nothing
+      for (int e = 0; e < NA; ++e) sR[lane * S + e] = 0.0;  // tail lanes contribute nothing
     } else if constexpr (kBulk) {
       fence_proxy_async_smem();  // earlier generic reads of this row before the async write
-      bulk_g2s(sR + lane * S, M + (int64_t)s * N, N * 8, &bars[w]);
+      bulk_g2s(sR + lane * S, Mt + (int64_t)s * NA, NA * 8, &bars[w]);
     } else {
-      const char* row = reinterpret_cast<const char*>(M + (int64_t)s * N);
+      const char* row = reinterpret_cast<const char*>(Mt + (int64_t)s * NA);
       const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(sR + lane * S));
-      if constexpr ((N * 8) % 16 == 0) {
 #pragma unroll
-        for (int e = 0; e < N * 8; e += 16)
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + e), "l"(row + e));
-      } else {
-#pragma unroll
-        for (int e = 0; e < N * 8; e += 8)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + e), "l"(row + e));
-      }
+      for (int e = 0; e < NA * 8; e += 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + e), "l"(row + e));
     }
     if constexpr (kBulk) {
       if (lane == 0) {
         const int64_t nv = l1 - base < 32 ? l1 - base : 32;
-        mbar_arrive_expect_tx(&bars[w], static_cast<unsigned>(nv * N * 8));
+        mbar_arrive_expect_tx(&bars[w], static_cast<unsigned>(nv * NA * 8));
       }
     } else {
       asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -218,7 +289,7 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
       ry = cs.y - ct.y;
       rz = cs.z - ct.z;
     }
-    double D[N];
+    double D[NG];
     derivs_reg<P>(rx, ry, rz, D);
     if constexpr (kBulk) {
       mbar_wait(&bars[w], phase);
@@ -228,65 +299,93 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
     }
     __syncwarp();
     const double* Ms = sR + lane * S;
-    auto contract = [&](auto IA, const double m) {
-      constexpr int ia = decltype(IA)::value;
+    auto contract = [&](auto KA, const double m) {
+      constexpr int ia = H::a_full(decltype(KA)::value);
       constexpr int aa = T::ea(ia), ab = T::eb(ia), ac = T::ec(ia), da = T::deg(ia);
-      static_for<N>([&](auto IB) {
-        constexpr int ib = decltype(IB)::value;
+      static_for<NA>([&](auto KB) {
+        constexpr int kb = decltype(KB)::value;
+        constexpr int ib = H::a_full(kb);
         if constexpr (da + T::deg(ib) <= P - 1) {
-          constexpr int ig = index_of(aa + T::ea(ib), ab + T::eb(ib), ac + T::ec(ib));
-          lam[ib] = fma(m, D[ig], lam[ib]);
+          constexpr int ig = H::g_of(index_of(aa + T::ea(ib), ab + T::eb(ib), ac + T::ec(ib)));
+          lam[kb] = fma(m, D[ig], lam[kb]);
         }
       });
     };
     // 16-B loads of the staged row (conflict-free: S/2 is odd), two coefficients at a time
-    static_for<N / 2>([&](auto IP) {
+    static_for<NA / 2>([&](auto IP) {
       constexpr int i0 = 2 * decltype(IP)::value;
       const double2 mm = *reinterpret_cast<const double2*>(Ms + i0);
       contract(std::integral_constant<int, i0>{}, mm.x);
       contract(std::integral_constant<int, i0 + 1>{}, mm.y);
     });
-    if constexpr (N & 1) contract(std::integral_constant<int, N - 1>{}, Ms[N - 1]);
+    if constexpr (NA & 1) contract(std::integral_constant<int, NA - 1>{}, Ms[NA - 1]);
     __syncwarp();  // every lane done reading sR before the next chunk's copies land
   }
-  // reduce the 32 lane partials (shared-memory transpose), then L_b += (-1)^{|b|}/b! Lambda_b
+  // reduce the 32 lane partials (shared-memory transpose) ...
 #pragma unroll
-  for (int i = 0; i < N; ++i) sR[lane * S + i] = lam[i];
+  for (int i = 0; i < NA; ++i) sR[lane * S + i] = lam[i];
   __syncwarp();
-  double* Lt = L + (int64_t)t * N;
-  for (int i = lane; i < N; i += 32) {
+  constexpr int R = (NA + 31) / 32;
+  double red[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int kk = lane + 32 * r;
     double acc = 0.0;
+    if (kk < NA) {
 #pragma unroll 8
-    for (int j = 0; j < 32; ++j) acc += sR[j * S + i];
-    int n = 0;
-    while (n_coef(n + 1) <= i) ++n;
-    int r = i - n_coef(n), a = 0;
-    while (r >= n - a + 1) { r -= n - a + 1; ++a; }
-    const int bexp = r, cexp = n - a - r;
-    double f = 1.0;
-    for (int q = 2; q <= a; ++q) f *= q;
-    for (int q = 2; q <= bexp; ++q) f *= q;
-    for (int q = 2; q <= cexp; ++q) f *= q;
-    Lt[i] += ((n & 1) ? -acc : acc) / f;
+      for (int j = 0; j < 32; ++j) acc += sR[j * S + kk];
+    }
+    red[r] = acc;
   }
+  __syncwarp();
+  // ... place at the full (reference-order) index, fill c >= 2 by the trace identity ...
+  double* full = sR;  // N doubles
+  static_for<NA>([&](auto K) {
+    constexpr int kk = decltype(K)::value;
+    if (lane == kk % 32) full[H::a_full(kk)] = red[kk / 32];
+  });
+  __syncwarp();
+  static_for<P>([&](auto C) {
+    constexpr int c = decltype(C)::value;
+    if constexpr (c >= 2) {
+      static_for<N>([&](auto I) {
+        constexpr int i = decltype(I)::value;
+        if constexpr (T::ec(i) == c) {
+          constexpr int a = T::ea(i), b = T::eb(i);
+          if (lane == i % 32) full[i] = -full[index_of(a + 2, b, c - 2)] - full[index_of(a, b + 2, c - 2)];
+        }
+      });
+      __syncwarp();
+    }
+  });
+  // ... then L_b += (-1)^{|b|}/b! Lambda_b
+  double* Lt = L + (int64_t)t * N;
+  static_for<N>([&](auto I) {
+    constexpr int i = decltype(I)::value;
+    constexpr double w = ((T::deg(i) & 1) ? -1.0 : 1.0) / T::fact(i);
+    if (lane == i % 32) Lt[i] += w * full[i];
+  });
 }
 
 template <int P>
 struct M2L {
   static void run(fmm_ctx* c, cudaStream_t s) {
     if constexpr (P <= 6) {
-      constexpr int S = m2l_row_stride(MI<P>::N);
-      const size_t smem = sizeof(double) * 4 * 32 * S;
+      constexpr int S = m2l_row_stride(HM<P>::NA);
+      const size_t smem = sizeof(double) * kM2LWarps * 32 * S;
       static bool attr = false;
       if (!attr) {
         CK(cudaFuncSetAttribute(k_m2l_reg<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
       }
       if (c->n_m2l_targets == 0) return;
-      k_m2l_reg<P><<<ceil_div(c->n_m2l_targets, 4), 128, smem, s>>>(c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p,
-                                                                    c->m2l_src.p, c->c_cr.p, c->M.p, c->L.p);
+      double* Mt = c->m2l_mt.ensure(c->ncells * HM<P>::NA + 1);
+      k_detrace<P><<<ceil_div(c->ncells, 128), 128, 0, s>>>(c->M.p, c->ncells, Mt);
+      CK_LAUNCH("k_detrace");
+      k_m2l_reg<P><<<ceil_div(c->n_m2l_targets, kM2LWarps), 32 * kM2LWarps, smem, s>>>(c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p,
+                                                                    c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
       CK_LAUNCH("k_m2l_reg");
-      c->kernel_launches += 1;
+      c->kernel_launches += 2;
       return;
     }
     using C = BigCfg<P>;
