@@ -52,18 +52,21 @@ struct HM {
   static constexpr int g_of(int i) { return tab.g_of[i]; }
 };
 
-// M' = detraced multipoles (HM<P>::NA per cell, compact a_c <= 1 order); thread per cell
+// M' = detraced multipoles (HM<P>::NA per cell, compact a_c <= 1 order); thread per cell, the
+// row in a per-thread shared-memory slice (odd stride: the lanes always touch the same entry, so
+// the accesses are conflict-free). Fold c >= 2 onto c - 2, highest c first.
+constexpr int kDetraceThreads = 64;
 template <int P>
-__global__ void k_detrace(const double* __restrict__ M, int64_t ncells, double* __restrict__ Mt) {
+__global__ void __launch_bounds__(kDetraceThreads) k_detrace(const double* __restrict__ M, int64_t ncells,
+                                                             double* __restrict__ Mt) {
   using T = MI<P>;
   using H = HM<P>;
-  constexpr int N = T::N;
-  const int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  constexpr int N = T::N, S = odd_stride(N);
+  extern __shared__ double dsm[];
+  const int64_t cell = blockIdx.x * (int64_t)kDetraceThreads + threadIdx.x;
   if (cell >= ncells) return;
-  double m[N];
-#pragma unroll
+  double* m = dsm + threadIdx.x * S;
   for (int i = 0; i < N; ++i) m[i] = M[cell * N + i];
-  // fold the c >= 2 entries onto c - 2, highest c first
   static_for<P>([&](auto K) {
     constexpr int c = P - 1 - decltype(K)::value;
     if constexpr (c >= 2) {
@@ -71,8 +74,9 @@ __global__ void k_detrace(const double* __restrict__ M, int64_t ncells, double* 
         constexpr int i = decltype(I)::value;
         if constexpr (T::ec(i) == c) {
           constexpr int a = T::ea(i), b = T::eb(i);
-          m[index_of(a + 2, b, c - 2)] -= m[i];
-          m[index_of(a, b + 2, c - 2)] -= m[i];
+          const double v = m[i];
+          m[index_of(a + 2, b, c - 2)] -= v;
+          m[index_of(a, b + 2, c - 2)] -= v;
         }
       });
     }
@@ -81,6 +85,18 @@ __global__ void k_detrace(const double* __restrict__ M, int64_t ncells, double* 
     constexpr int k = decltype(K)::value;
     Mt[cell * H::NA + k] = m[H::a_full(k)];
   });
+}
+
+template <int P>
+void launch_detrace(fmm_ctx* c, double* Mt, cudaStream_t s) {
+  const size_t smem = sizeof(double) * kDetraceThreads * odd_stride(MI<P>::N);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_detrace<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  k_detrace<P><<<ceil_div(c->ncells, kDetraceThreads), kDetraceThreads, smem, s>>>(c->M.p, c->ncells, Mt);
+  CK_LAUNCH("k_detrace");
 }
 
 // Dt_g for g_c <= 2 (compact HM::g_of order) by the reference's degree recurrence
@@ -438,8 +454,7 @@ struct M2L {
       }
       if (c->n_m2l_targets == 0) return;
       double* Mt = c->m2l_mt.ensure(c->ncells * HM<P>::NA + 1);
-      k_detrace<P><<<ceil_div(c->ncells, 128), 128, 0, s>>>(c->M.p, c->ncells, Mt);
-      CK_LAUNCH("k_detrace");
+      launch_detrace<P>(c, Mt, s);
       k_m2l_reg<P><<<ceil_div(c->n_m2l_targets, kM2LWarps), 32 * kM2LWarps, smem, s>>>(c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p,
                                                                     c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
       CK_LAUNCH("k_m2l_reg");
@@ -464,8 +479,7 @@ struct M2L {
     double* zero_row = scratch + (size_t)grid * C::kWarps * 32 * C::NA;
     CK(cudaMemsetAsync(zero_row, 0, sizeof(double) * C::NA, s));
     double* Mt = c->m2l_mt.ensure(c->ncells * C::NA + 1);
-    k_detrace<P><<<ceil_div(c->ncells, 128), 128, 0, s>>>(c->M.p, c->ncells, Mt);
-    CK_LAUNCH("k_detrace");
+    launch_detrace<P>(c, Mt, s);
     k_m2l_big<P><<<(unsigned)grid, 32 * C::kWarps, smem, s>>>(c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p,
                                                               c->m2l_src.p, c->c_cr.p, Mt, zero_row, c->L.p,
                                                               scratch);
