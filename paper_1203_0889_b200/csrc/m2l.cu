@@ -301,8 +301,14 @@ struct BigCfg {
   static constexpr int N = MI<P>::N;
   static constexpr int NA = HM<P>::NA, NG = HM<P>::NG;
   static constexpr int S = odd_stride(NG);
-  static constexpr int kWarps = 4;
-  static constexpr int kBlk = 32;
+#ifndef FMM_BIG_WARPS
+#define FMM_BIG_WARPS 6
+#endif
+#ifndef FMM_BIG_BLK
+#define FMM_BIG_BLK 32
+#endif
+  static constexpr int kWarps = FMM_BIG_WARPS;
+  static constexpr int kBlk = FMM_BIG_BLK;
   static constexpr int kBlocks = (NA + kBlk - 1) / kBlk;
 };
 
