@@ -128,39 +128,57 @@ __device__ __forceinline__ int32_t lower_digit(const uint64_t* __restrict__ k, i
   return lo;
 }
 
-// Children of every cell of one level (warp per cell): lanes 1..7 binary-search the seven
-// octant boundaries in parallel; bnd[9*k + o] = first body of octant o (bnd[9*k+8] = end).
-__global__ void k_count_children(int32_t cbeg, int32_t cend, int level, int n_crit,
+// Children of every cell of one level (warp per cell, grid-stride; the level's cell range is
+// read from the device level table, so all levels queue without a host round trip): lanes 1..7
+// binary-search the seven octant boundaries in parallel; bnd[9*k + o] = first body of octant o
+// (bnd[9*k+8] = end).
+__global__ void k_count_children(const int32_t* __restrict__ lev, int level, int n_crit,
                                  const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
                                  const uint64_t* __restrict__ skeys, int32_t* __restrict__ nchild,
                                  int32_t* __restrict__ bnd) {
-  const int32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int32_t cbeg = lev[level], cend = lev[level + 1];
   const int lane = threadIdx.x & 31;
-  const int32_t ci = cbeg + k;
-  if (ci >= cend) return;
-  const int32_t b = bb[ci], e = be[ci];
-  const bool split = e - b > n_crit && level < kLevels;  // tree.cpp:78
-  int32_t pos = e;
-  if (split && lane >= 1 && lane <= 7) pos = lower_digit(skeys, b, e, level + 1, lane);
-  if (lane == 0) pos = b;
-  if (split && lane <= 8) bnd[9 * k + lane] = pos;
-  const int32_t nxt = __shfl_down_sync(0xffffffffu, pos, 1);
-  const unsigned nonempty = __ballot_sync(0xffffffffu, split && lane < 8 && nxt > pos);
-  if (lane == 0) nchild[k] = __popc(nonempty);
+  const int32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (int32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; cbeg + k < cend; k += nw) {
+    const int32_t ci = cbeg + k;
+    const int32_t b = bb[ci], e = be[ci];
+    const bool split = e - b > n_crit && level < kLevels;  // tree.cpp:78
+    int32_t pos = e;
+    if (split && lane >= 1 && lane <= 7) pos = lower_digit(skeys, b, e, level + 1, lane);
+    if (lane == 0) pos = b;
+    if (split && lane <= 8) bnd[9 * k + lane] = pos;
+    const int32_t nxt = __shfl_down_sync(0xffffffffu, pos, 1);
+    const unsigned nonempty = __ballot_sync(0xffffffffu, split && lane < 8 && nxt > pos);
+    if (lane == 0) nchild[k] = __popc(nonempty);
+  }
 }
 
-// Materialises the children of one level; offs = exclusive scan of nchild.
-__global__ void k_write_children(int32_t cbeg, int32_t cend, int level, int32_t next_begin,
+// next level's range: lev[level + 2] = lev[level + 1] + (children of this level), clamped to
+// the cell capacity (overflow flagged; the build is then repeated with larger arrays)
+__global__ void k_level_advance(int32_t* __restrict__ lev, int level, const int32_t* __restrict__ offs, int64_t cap,
+                                int32_t* __restrict__ overflow) {
+  const int32_t m = lev[level + 1] - lev[level];
+  int64_t next = static_cast<int64_t>(lev[level + 1]) + offs[m];
+  if (next > cap) {
+    *overflow = 1;
+    next = lev[level + 1];
+  }
+  lev[level + 2] = static_cast<int32_t>(next);
+}
+
+// Materialises the children of one level (grid-stride); offs = exclusive scan of nchild.
+__global__ void k_write_children(const int32_t* __restrict__ lev, int level, int64_t cap,
                                  const int32_t* __restrict__ nchild, const int32_t* __restrict__ offs,
                                  const int32_t* __restrict__ bnd, int32_t* __restrict__ c_level,
                                  uint64_t* __restrict__ c_key, double4* __restrict__ c_cr,
                                  int32_t* __restrict__ bb, int32_t* __restrict__ be,
                                  int32_t* __restrict__ cb, int32_t* __restrict__ cc,
                                  int32_t* __restrict__ par) {
-  const int32_t ci = cbeg + blockIdx.x * blockDim.x + threadIdx.x;
-  if (ci >= cend) return;
+  const int32_t cbeg = lev[level], cend = lev[level + 1], next_begin = cend;
+  for (int32_t ci = cbeg + blockIdx.x * blockDim.x + threadIdx.x; ci < cend; ci += gridDim.x * blockDim.x) {
   const int k = ci - cbeg;
-  if (nchild[k] == 0) return;
+  if (nchild[k] == 0) continue;
+  if (static_cast<int64_t>(next_begin) + offs[k] + nchild[k] > cap) continue;  // overflow: flagged
   const double4 pc = c_cr[ci];
   const uint64_t pkey = c_key[ci];
   const double cr = __dmul_rn(0.5, pc.w);
@@ -181,6 +199,7 @@ __global__ void k_write_children(int32_t cbeg, int32_t cend, int level, int32_t 
       par[out] = ci;
       ++out;
     }
+  }
   }
 }
 
@@ -325,55 +344,89 @@ void build_tree(fmm_ctx* c) {
     c->body_keys_valid = false;
   }
 
-  // 4. level-by-level cell materialisation
-  auto ensure_cells = [&](size_t used, size_t need) {
-    grow_preserve(c, c->c_level, used, need);
-    grow_preserve(c, c->c_key, used, need);
-    grow_preserve(c, c->c_cr, used, need);
-    grow_preserve(c, c->c_body_begin, used, need);
-    grow_preserve(c, c->c_body_end, used, need);
-    grow_preserve(c, c->c_child_begin, used, need);
-    grow_preserve(c, c->c_child_count, used, need);
-    grow_preserve(c, c->c_parent, used, need);
-  };
-  ensure_cells(0, 1024);
-  k_init_root<<<1, 1, 0, s>>>(dom, (int32_t)n, c->c_level.p, c->c_key.p, c->c_cr.p, c->c_body_begin.p,
-                              c->c_body_end.p, c->c_child_begin.p, c->c_child_count.p, c->c_parent.p);
-  CK_LAUNCH("k_init_root");
-  int64_t ncells = 1;
+  // 4. level-by-level cell materialisation, queued in batches without host round trips: the
+  // level ranges live in a device table; the host reads it once per batch (one batch covers the
+  // previous build's depth + 2 levels, so a steady sequence of steps syncs once).
+  const int64_t want_cap = std::max<int64_t>(4096, 16 * n / std::max(1, c->cfg.n_crit) + 1024);
+  int32_t* dlev = reinterpret_cast<int32_t*>(c->bnd_lev.ensure(FMM_MAX_LEVEL + 4));
+  int32_t* overflow = dlev + FMM_MAX_LEVEL + 3;
   int level = 0;
-  for (int l = 0; l < FMM_MAX_LEVEL + 2; ++l) c->level_start[l] = 0;
-  c->level_start[1] = 1;
+  int64_t ncells = 1;
   int launches = 4;
-  while (true) {
-    const int32_t cb = c->level_start[level], ce = c->level_start[level + 1];
-    const int32_t m = ce - cb;
-    int32_t* nchild = c->i32_a.ensure(m + 1);
-    int32_t* offs = c->i32_b.ensure(m + 1);
-    int32_t* bnd = c->bnd.ensure(9 * (size_t)m + 9);
-    k_count_children<<<ceil_div((int64_t)m * 32, 128), 128, 0, s>>>(cb, ce, level, c->cfg.n_crit, c->c_body_begin.p,
-                                                                    c->c_body_end.p, skeys, nchild, bnd);
-    CK_LAUNCH("k_count_children");
+  for (int attempt = 0;; ++attempt) {
+    const int64_t cap = std::max<int64_t>(want_cap, static_cast<int64_t>(c->c_level.cap));
+    auto ensure_cells = [&](size_t need) {
+      grow_preserve(c, c->c_level, 0, need);
+      grow_preserve(c, c->c_key, 0, need);
+      grow_preserve(c, c->c_cr, 0, need);
+      grow_preserve(c, c->c_body_begin, 0, need);
+      grow_preserve(c, c->c_body_end, 0, need);
+      grow_preserve(c, c->c_child_begin, 0, need);
+      grow_preserve(c, c->c_child_count, 0, need);
+      grow_preserve(c, c->c_parent, 0, need);
+    };
+    ensure_cells(cap);
+    const int64_t ccap = std::min<int64_t>(static_cast<int64_t>(c->c_level.cap), static_cast<int64_t>(c->c_parent.cap));
+    int32_t* nchild = c->i32_a.ensure(ccap + 1);
+    int32_t* offs = c->i32_b.ensure(ccap + 1);
+    int32_t* bnd = c->bnd.ensure(9 * (size_t)ccap + 9);
     size_t sb = 0;
-    CK(cudaMemsetAsync(nchild + m, 0, sizeof(int32_t), s));
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, nchild, offs, m + 1, s));
-    CK(cub::DeviceScan::ExclusiveSum(temp_storage(c, sb), sb, nchild, offs, m + 1, s));
-    CK(cudaMemcpyAsync(hp, offs + m, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    const int32_t nnew = static_cast<int32_t>(*reinterpret_cast<int32_t*>(hp));
-    launches += 2;
-    if (nnew == 0) break;
-    ensure_cells(ncells, ncells + nnew);
-    k_write_children<<<ceil_div(m, 128), 128, 0, s>>>(cb, ce, level, ce, nchild, offs, bnd, c->c_level.p,
-                                                     c->c_key.p, c->c_cr.p, c->c_body_begin.p, c->c_body_end.p,
-                                                     c->c_child_begin.p, c->c_child_count.p, c->c_parent.p);
-    CK_LAUNCH("k_write_children");
-    ++launches;
-    ncells += nnew;
-    ++level;
-    c->level_start[level + 1] = static_cast<int32_t>(ncells);
-    if (ncells >= (int64_t(1) << 31) - 16) fail(FMM_ERR_UNSUPPORTED, "too many cells");
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, nchild, offs, (int)(ccap + 1), s));
+    void* scan_tmp = temp_storage(c, sb);
+    {
+      int32_t h0[3] = {0, 1, 0};
+      CK(cudaMemcpyAsync(dlev, h0, 2 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      CK(cudaMemsetAsync(overflow, 0, sizeof(int32_t), s));
+    }
+    k_init_root<<<1, 1, 0, s>>>(dom, (int32_t)n, c->c_level.p, c->c_key.p, c->c_cr.p, c->c_body_begin.p,
+                                c->c_body_end.p, c->c_child_begin.p, c->c_child_count.p, c->c_parent.p);
+    CK_LAUNCH("k_init_root");
+    int32_t hlev[FMM_MAX_LEVEL + 4];
+    int done_level = -1;  // last level whose children have been counted
+    bool finished = false, over = false;
+    int batch = std::max(2, c->last_depth + 2);
+    while (!finished) {
+      const int l_end = std::min(done_level + batch, kLevels);
+      for (int L = done_level + 1; L <= l_end; ++L) {
+        CK(cudaMemsetAsync(nchild, 0, (ccap + 1) * sizeof(int32_t), s));
+        k_count_children<<<148 * 16, 128, 0, s>>>(dlev, L, c->cfg.n_crit, c->c_body_begin.p, c->c_body_end.p,
+                                                  skeys, nchild, bnd);
+        CK_LAUNCH("k_count_children");
+        CK(cub::DeviceScan::ExclusiveSum(scan_tmp, sb, nchild, offs, (int)(ccap + 1), s));
+        k_write_children<<<148 * 8, 128, 0, s>>>(dlev, L, ccap, nchild, offs, bnd, c->c_level.p, c->c_key.p,
+                                                 c->c_cr.p, c->c_body_begin.p, c->c_body_end.p, c->c_child_begin.p,
+                                                 c->c_child_count.p, c->c_parent.p);
+        CK_LAUNCH("k_write_children");
+        k_level_advance<<<1, 1, 0, s>>>(dlev, L, offs, ccap, overflow);
+        CK_LAUNCH("k_level_advance");
+        launches += 5;
+      }
+      CK(cudaMemcpyAsync(hlev, dlev, (FMM_MAX_LEVEL + 4) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      over = hlev[FMM_MAX_LEVEL + 3] != 0;
+      if (over) break;
+      // the tree ends at the first level that has no children (or at kLevels)
+      for (int L = done_level + 1; L <= l_end; ++L) {
+        if (hlev[L + 2] == hlev[L + 1] || L == kLevels) {
+          finished = true;
+          level = L;
+          break;
+        }
+      }
+      done_level = l_end;
+    }
+    if (!over) {
+      // cells exist at levels 0..level (level = the first level without children)
+      for (int l = 0; l <= level + 1; ++l) c->level_start[l] = hlev[l];
+      ncells = hlev[level + 1];
+      while (level > 0 && hlev[level + 1] == hlev[level]) --level;  // deepest non-empty level
+      break;
+    }
+    if (attempt > 0) fail(FMM_ERR_CUDA, "tree build: cell overflow after regrow");
+    ensure_cells(static_cast<size_t>(ccap) * 4);  // regrow and rebuild
   }
+  c->last_depth = level;
+  if (ncells >= (int64_t(1) << 31) - 16) fail(FMM_ERR_UNSUPPORTED, "too many cells");
   for (int l = level + 2; l < FMM_MAX_LEVEL + 2; ++l) c->level_start[l] = static_cast<int32_t>(ncells);
   c->ncells = ncells;
   c->depth = level;
