@@ -85,7 +85,8 @@ struct fmm_ctx {
   fmmb::DBuf<uint64_t> trav_ctr;            // traversal level counters
   fmmb::DBuf<int32_t> bnd;           // child boundaries of one level (9 per cell)
   fmmb::DBuf<int32_t> bnd_lev;       // device level table (tree build)
-  int last_depth = 6;                // depth of the previous build (level batch size)
+  int last_depth = 6;                // depth of the previous build (level batch, sorted digits)
+  bool depth_known = false;
   int64_t* hpin = nullptr;           // pinned host scratch (64 x int64)
 
   // sharding: target leaves split by contiguous body (Morton) range

@@ -133,25 +133,34 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
         if (op < cap_p) p2p_keys[op] = key; else over = true;
         ++op;
       } else if (kind[j] >= 2) {
-        if (oc + nch[j] > cap_f) {
-          over = true;
-        } else if (kind[j] == 2) {
+        // children past the frontier capacity are dropped (and the run flagged), but every slot
+        // below the capacity is written, so a truncated frontier still holds only valid pairs
+        if (oc + nch[j] > cap_f) over = true;
+        if (kind[j] == 2) {
           const int32_t b = cb[pr[j].x];
           if (filter) {
             int64_t q = oc;
             for (int k = 0; k < cc[pr[j].x]; ++k)
-              if (bb[b + k] < tb1 && be[b + k] > tb0) next[q++] = make_int2(b + k, pr[j].y);
+              if (bb[b + k] < tb1 && be[b + k] > tb0) {
+                if (q < cap_f) next[q] = make_int2(b + k, pr[j].y);
+                ++q;
+              }
           } else {
-            for (int k = 0; k < nch[j]; ++k) next[oc + k] = make_int2(b + k, pr[j].y);
+            for (int k = 0; k < nch[j]; ++k)
+              if (oc + k < cap_f) next[oc + k] = make_int2(b + k, pr[j].y);
           }
         } else if (kind[j] == 3) {
           const int32_t b = cb[pr[j].y];
-          for (int k = 0; k < nch[j]; ++k) next[oc + k] = make_int2(pr[j].x, b + k);
+          for (int k = 0; k < nch[j]; ++k)
+            if (oc + k < cap_f) next[oc + k] = make_int2(pr[j].x, b + k);
         } else {
           const int32_t b = cb[pr[j].x], m = cc[pr[j].x];
           int64_t q = oc;
           for (int a = 0; a < m; ++a)
-            for (int c = a; c < m; ++c) next[q++] = make_int2(b + a, b + c);
+            for (int c = a; c < m; ++c) {
+              if (q < cap_f) next[q] = make_int2(b + a, b + c);
+              ++q;
+            }
         }
         oc += nch[j];
       }
@@ -332,9 +341,8 @@ void traverse(fmm_ctx* c) {
     const int64_t nm = static_cast<int64_t>(h[0]), np = static_cast<int64_t>(h[1]);
     int64_t fmax = 0;
     for (int L = 0; L <= nlev; ++L) fmax = std::max<int64_t>(fmax, static_cast<int64_t>(h[4 + L]));
-    const bool unfinished = h[4 + nlev] != 0;
-    if (unfinished) fail(FMM_ERR_CUDA, "traverse: frontier not empty after 2*depth+2 levels");
-    if (h[2] == 0) {
+    if (h[2] == 0) {  // no overflow: the lists are complete
+      if (h[4 + nlev] != 0) fail(FMM_ERR_CUDA, "traverse: frontier not empty after 2*depth+2 levels");
       finish_lists(c, nm, np);
       return;
     }

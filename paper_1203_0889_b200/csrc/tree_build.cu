@@ -132,17 +132,21 @@ __device__ __forceinline__ int32_t lower_digit(const uint64_t* __restrict__ k, i
 // read from the device level table, so all levels queue without a host round trip): lanes 1..7
 // binary-search the seven octant boundaries in parallel; bnd[9*k + o] = first body of octant o
 // (bnd[9*k+8] = end).
-__global__ void k_count_children(const int32_t* __restrict__ lev, int level, int n_crit,
+__global__ void k_count_children(const int32_t* __restrict__ lev, int level, int n_crit, int sort_levels,
                                  const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
                                  const uint64_t* __restrict__ skeys, int32_t* __restrict__ nchild,
-                                 int32_t* __restrict__ bnd) {
+                                 int32_t* __restrict__ bnd, int32_t* __restrict__ deeper) {
   const int32_t cbeg = lev[level], cend = lev[level + 1];
   const int lane = threadIdx.x & 31;
   const int32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (int32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; cbeg + k < cend; k += nw) {
     const int32_t ci = cbeg + k;
     const int32_t b = bb[ci], e = be[ci];
-    const bool split = e - b > n_crit && level < kLevels;  // tree.cpp:78
+    bool split = e - b > n_crit && level < kLevels;  // tree.cpp:78
+    if (split && level >= sort_levels) {  // digits below the sorted ones: full sort needed
+      if (lane == 0) *deeper = 1;
+      split = false;
+    }
     int32_t pos = e;
     if (split && lane >= 1 && lane <= 7) pos = lower_digit(skeys, b, e, level + 1, lane);
     if (lane == 0) pos = b;
@@ -333,10 +337,21 @@ void build_tree(fmm_ctx* c) {
   CK_LAUNCH("k_keys");
   uint64_t* skeys = c->keys_b.ensure(n);
   int32_t* sidx = c->idx_b.ensure(n);
-  size_t tbytes = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, keys, skeys, idx, sidx, (int)n, 0, 3 * kLevels, s));
-  void* tmp = temp_storage(c, tbytes);
-  CK(cub::DeviceRadixSort::SortPairs(tmp, tbytes, keys, skeys, idx, sidx, (int)n, 0, 3 * kLevels, s));
+  // The stable sort only needs the digits of the levels the tree will have: with the previous
+  // build's depth D known, sort the top 3(D+1) key bits (C2: 18 bits, 3 passes instead of 8);
+  // bodies with equal top digits keep input order, which is the reference's order inside a leaf
+  // (stable partitions, tree.cpp:80-98). A cell that would need a deeper split triggers a full
+  // sort and rebuild. Sharded runs keep the full sort (their partition keys compare full keys).
+  int sort_levels = (c->world > 1 || !c->depth_known) ? kLevels : std::min(kLevels, c->last_depth + 1);
+  auto sort_keys = [&]() {
+    const int begin_bit = 3 * (kLevels - sort_levels);
+    size_t tbytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tbytes, keys, skeys, idx, sidx, (int)n, begin_bit, 3 * kLevels, s));
+    CK(cub::DeviceRadixSort::SortPairs(temp_storage(c, tbytes), tbytes, keys, skeys, idx, sidx, (int)n, begin_bit,
+                                       3 * kLevels, s));
+    c->kernel_launches += 1;
+  };
+  sort_keys();
   if (c->world > 1) {  // partition reuse maps Morton boundaries onto this tree (shard.cu)
     CK(cudaMemcpyAsync(c->body_keys.ensure(n), skeys, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
     c->body_keys_valid = true;
@@ -348,8 +363,9 @@ void build_tree(fmm_ctx* c) {
   // level ranges live in a device table; the host reads it once per batch (one batch covers the
   // previous build's depth + 2 levels, so a steady sequence of steps syncs once).
   const int64_t want_cap = std::max<int64_t>(4096, 16 * n / std::max(1, c->cfg.n_crit) + 1024);
-  int32_t* dlev = reinterpret_cast<int32_t*>(c->bnd_lev.ensure(FMM_MAX_LEVEL + 4));
+  int32_t* dlev = reinterpret_cast<int32_t*>(c->bnd_lev.ensure(FMM_MAX_LEVEL + 5));
   int32_t* overflow = dlev + FMM_MAX_LEVEL + 3;
+  int32_t* deeper = dlev + FMM_MAX_LEVEL + 4;
   int level = 0;
   int64_t ncells = 1;
   int launches = 4;
@@ -376,12 +392,12 @@ void build_tree(fmm_ctx* c) {
     {
       int32_t h0[3] = {0, 1, 0};
       CK(cudaMemcpyAsync(dlev, h0, 2 * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      CK(cudaMemsetAsync(overflow, 0, sizeof(int32_t), s));
+      CK(cudaMemsetAsync(overflow, 0, 2 * sizeof(int32_t), s));
     }
     k_init_root<<<1, 1, 0, s>>>(dom, (int32_t)n, c->c_level.p, c->c_key.p, c->c_cr.p, c->c_body_begin.p,
                                 c->c_body_end.p, c->c_child_begin.p, c->c_child_count.p, c->c_parent.p);
     CK_LAUNCH("k_init_root");
-    int32_t hlev[FMM_MAX_LEVEL + 4];
+    int32_t hlev[FMM_MAX_LEVEL + 5];
     int done_level = -1;  // last level whose children have been counted
     bool finished = false, over = false;
     int batch = std::max(2, c->last_depth + 2);
@@ -389,8 +405,8 @@ void build_tree(fmm_ctx* c) {
       const int l_end = std::min(done_level + batch, kLevels);
       for (int L = done_level + 1; L <= l_end; ++L) {
         CK(cudaMemsetAsync(nchild, 0, (ccap + 1) * sizeof(int32_t), s));
-        k_count_children<<<148 * 16, 128, 0, s>>>(dlev, L, c->cfg.n_crit, c->c_body_begin.p, c->c_body_end.p,
-                                                  skeys, nchild, bnd);
+        k_count_children<<<148 * 16, 128, 0, s>>>(dlev, L, c->cfg.n_crit, sort_levels, c->c_body_begin.p,
+                                                  c->c_body_end.p, skeys, nchild, bnd, deeper);
         CK_LAUNCH("k_count_children");
         CK(cub::DeviceScan::ExclusiveSum(scan_tmp, sb, nchild, offs, (int)(ccap + 1), s));
         k_write_children<<<148 * 8, 128, 0, s>>>(dlev, L, ccap, nchild, offs, bnd, c->c_level.p, c->c_key.p,
@@ -401,10 +417,10 @@ void build_tree(fmm_ctx* c) {
         CK_LAUNCH("k_level_advance");
         launches += 5;
       }
-      CK(cudaMemcpyAsync(hlev, dlev, (FMM_MAX_LEVEL + 4) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(hlev, dlev, (FMM_MAX_LEVEL + 5) * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       over = hlev[FMM_MAX_LEVEL + 3] != 0;
-      if (over) break;
+      if (over || hlev[FMM_MAX_LEVEL + 4] != 0) break;
       // the tree ends at the first level that has no children (or at kLevels)
       for (int L = done_level + 1; L <= l_end; ++L) {
         if (hlev[L + 2] == hlev[L + 1] || L == kLevels) {
@@ -414,6 +430,12 @@ void build_tree(fmm_ctx* c) {
         }
       }
       done_level = l_end;
+    }
+    if (!over && hlev[FMM_MAX_LEVEL + 4] != 0) {  // deeper than the partial sort: full sort, rebuild
+      sort_levels = kLevels;
+      sort_keys();
+      --attempt;
+      continue;
     }
     if (!over) {
       // cells exist at levels 0..level (level = the first level without children)
@@ -426,6 +448,7 @@ void build_tree(fmm_ctx* c) {
     ensure_cells(static_cast<size_t>(ccap) * 4);  // regrow and rebuild
   }
   c->last_depth = level;
+  c->depth_known = true;
   if (ncells >= (int64_t(1) << 31) - 16) fail(FMM_ERR_UNSUPPORTED, "too many cells");
   for (int l = level + 2; l < FMM_MAX_LEVEL + 2; ++l) c->level_start[l] = static_cast<int32_t>(ncells);
   c->ncells = ncells;

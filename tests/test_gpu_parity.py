@@ -216,6 +216,26 @@ def test_pipeline_vs_oracle(fmmlib, orc, case):
         assert info.p2p_body_pairs == int((nb[op[:, 0]] * nb[op[:, 1]]).sum())
 
 
+def test_tree_reuse_across_distributions(fmmlib, orc):
+    """One context, successive body sets of growing depth: the partial-digit sort keyed on the
+    previous depth must fall back to the full sort (and the level batches must continue) so that
+    every tree and permutation stays bit-exact with the reference restatement."""
+    ctx = fmmlib.Context(order=4, n_crit=32, theta=0.5, precision="fp64")
+    for gen, n, seed in ((1, 20000, 3), (3, 20000, 4), (5, 30000, 6), (1, 5000, 7), (3, 40000, 8)):
+        bodies = fmmlib.generate_bodies(gen, n, seed)
+        t = oracle_run(orc, bodies, 32, 4, 0.5)
+        ocells = t.cells()
+        ctx.set_bodies(bodies)
+        ctx.evaluate()
+        cells = ctx.cells()
+        for k in CELL_KEYS:
+            assert np.array_equal(cells[k], getattr(ocells, k)), (gen, n, k)
+        assert np.array_equal(ctx.permutation(), t.perm()), (gen, n)
+        phi, _ = ctx.results("tree")
+        assert rel_l2(phi, t.phi()) < 1e-12, (gen, n)
+    ctx.close()
+
+
 def test_stage_isolated_m2l_and_p2p(fmmlib, orc):
     """Inject the oracle's tree, lists and multipoles; the GPU M2L locals and P2P near field
     then match the oracle's per coefficient / per body."""
