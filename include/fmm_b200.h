@@ -101,9 +101,9 @@ int fmm_p2p(fmm_ctx* ctx);          /* KernelVisitor::p2p_pair over the P2P list
 int fmm_downward(fmm_ctx* ctx);     /* downward_pass       traversal.cpp:52-63 (+ output) */
 int fmm_evaluate(fmm_ctx* ctx);     /* all of the above */
 int fmm_synchronize(fmm_ctx* ctx);
-/* 1: fmm_evaluate runs P2P on a second stream concurrently with upward + M2L; 0 (default)
- * serialises the stages on one stream. On B200 the overlap measured no gain: P2P occupies the
- * registers and shared memory of every SM, so the FP64 kernels cannot co-reside. */
+/* 1 (default): fmm_evaluate runs the upward pass (P2M/M2M, needs only the tree) on a second
+ * stream concurrently with the dual tree traversal and its list building; M2L joins both.
+ * 0 serialises every stage on one stream (each kernel timed alone). */
 int fmm_set_overlap(fmm_ctx* ctx, int on);
 
 /* ---- outputs ------------------------------------------------------------------------ */

@@ -227,46 +227,38 @@ int fmm_evaluate(fmm_ctx* c) {
     CK(cudaEventRecord(c->ev[EV_BUILD0], c->stream));
     fmmb::build_tree(c);
     CK(cudaEventRecord(c->ev[EV_BUILD1], c->stream));
-    fmmb::traverse(c);
-    CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
     if (c->overlap) {
-      // P2P needs only the lists: run it on the second stream, concurrently with the FP64
-      // expansion chain (upward -> M2L), and join before the downward pass reads its output.
+      // The upward pass needs only the tree: it runs on the second stream while the traversal
+      // (and its host round trips) proceeds on the first; M2L joins both.
+      CK(cudaStreamWaitEvent(c->stream2, c->ev[EV_BUILD1], 0));
+      fmmb::run_upward(c, c->stream2);
+      CK(cudaEventRecord(c->ev[EV_UP1], c->stream2));
+      fmmb::traverse(c);
+      CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
+      CK(cudaStreamWaitEvent(c->stream, c->ev[EV_UP1], 0));
       CK(cudaEventRecord(c->ev[EV_FORK], c->stream));
-      CK(cudaStreamWaitEvent(c->stream2, c->ev[EV_FORK], 0));
-      cudaStream_t keep = c->stream;
-      c->stream = c->stream2;
-      try {
-        do_p2p(c);
-      } catch (...) {
-        c->stream = keep;
-        throw;
-      }
-      c->stream = keep;
-      CK(cudaEventRecord(c->ev[EV_P2P1], c->stream2));
-      fmmb::run_upward(c, c->stream);
-      CK(cudaEventRecord(c->ev[EV_UP1], c->stream));
-      do_m2l(c);
-      CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
-      CK(cudaStreamWaitEvent(c->stream, c->ev[EV_P2P1], 0));
     } else {
+      fmmb::traverse(c);
+      CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
       fmmb::run_upward(c, c->stream);
       CK(cudaEventRecord(c->ev[EV_UP1], c->stream));
-      do_m2l(c);
-      CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
-      do_p2p(c);
-      CK(cudaEventRecord(c->ev[EV_P2P1], c->stream));
+      CK(cudaEventRecord(c->ev[EV_FORK], c->stream));
     }
+    do_m2l(c);
+    CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
+    do_p2p(c);
+    CK(cudaEventRecord(c->ev[EV_P2P1], c->stream));
     fmmb::run_downward(c, c->stream);
     CK(cudaEventRecord(c->ev[EV_DOWN1], c->stream));
     CK(cudaStreamSynchronize(c->stream));
     fmm_stage_times& t = c->times;
     t.build_ms = ms_between(c->ev[EV_BUILD0], c->ev[EV_BUILD1]);
     t.traverse_ms = ms_between(c->ev[EV_BUILD1], c->ev[EV_TRAV1]);
-    t.upward_ms = ms_between(c->ev[EV_TRAV1], c->ev[EV_UP1]);
-    t.m2l_ms = ms_between(c->ev[EV_UP1], c->ev[EV_M2L1]);
-    t.p2p_ms = c->overlap ? ms_between(c->ev[EV_FORK], c->ev[EV_P2P1]) : ms_between(c->ev[EV_M2L1], c->ev[EV_P2P1]);
-    t.downward_ms = ms_between(c->overlap ? c->ev[EV_M2L1] : c->ev[EV_P2P1], c->ev[EV_DOWN1]);
+    // overlap: upward ran concurrently with the traversal (BUILD1 -> UP1 on the second stream)
+    t.upward_ms = c->overlap ? ms_between(c->ev[EV_BUILD1], c->ev[EV_UP1]) : ms_between(c->ev[EV_TRAV1], c->ev[EV_UP1]);
+    t.m2l_ms = ms_between(c->ev[EV_FORK], c->ev[EV_M2L1]);
+    t.p2p_ms = ms_between(c->ev[EV_M2L1], c->ev[EV_P2P1]);
+    t.downward_ms = ms_between(c->ev[EV_P2P1], c->ev[EV_DOWN1]);
     t.total_ms = ms_between(c->ev[EV_BUILD0], c->ev[EV_DOWN1]);
     t.p2p_kernel_ms = ms_between(c->ev[EV_P2PK0], c->ev[EV_P2PK1]);
     t.m2l_kernel_ms = ms_between(c->ev[EV_M2LK0], c->ev[EV_M2LK1]);

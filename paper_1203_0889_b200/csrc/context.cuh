@@ -111,7 +111,7 @@ struct fmm_ctx {
   fmmb::DBuf<int64_t> shard_bounds;        // device copy of the world + 1 body bounds
   int64_t trav_b0 = 0, trav_b1 = 0;        // traversal target filter [b0, b1)
 
-  bool overlap = false;  // fmm_evaluate: P2P on stream2 concurrently with upward + M2L (opt-in)
+  bool overlap = true;  // fmm_evaluate: upward pass on stream2 concurrently with the traversal
 
   // state
   bool have_bodies = false, have_tree = false, have_lists = false, have_M = false,

@@ -14,7 +14,8 @@ ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--precision", default="fp32")
 ap.add_argument("--n", type=int, default=0, help="override the body count")
-ap.add_argument("--serial", action="store_true", help="no P2P/far-field overlap (isolated kernel times)")
+ap.add_argument("--serial", action="store_true", help="stages serialised on one stream")
+ap.add_argument("--overlap", action="store_true", help="upward pass concurrent with the traversal")
 a = ap.parse_args()
 gen, n, p, n_crit, theta = CONFIGS[a.config]
 if a.n:
@@ -24,6 +25,8 @@ ctx = fb.Context(order=p, n_crit=n_crit, theta=theta, precision=a.precision)
 ctx.set_bodies(b)
 if a.serial:
     ctx.set_overlap(False)
+if a.overlap:
+    ctx.set_overlap(True)
 for _ in range(a.warmup + a.steps):
     ctx.evaluate()
 t = ctx.stage_times()
