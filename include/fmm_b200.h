@@ -32,7 +32,7 @@ typedef enum {
   FMM_ERR_SINGULAR_EVAL = 6,     /* "singular evaluation point"     kernels.cpp:200 */
   FMM_ERR_CANNOT_SPLIT = 7,      /* "cannot split leaf pair"        traversal.cpp:19 */
   FMM_ERR_THETA = 8,             /* "theta must be in (0,1)"        engine.cpp:63 */
-  FMM_ERR_UNSUPPORTED = 20,      /* order > FMM_MAX_ORDER, mutual mode, ... */
+  FMM_ERR_UNSUPPORTED = 20,      /* order > FMM_MAX_ORDER, mutual + sharded, ... */
   FMM_ERR_ARG = 21,              /* null pointer / bad size */
   FMM_ERR_STATE = 22,            /* stage called before its inputs exist */
   FMM_ERR_CUDA = 30,             /* CUDA runtime error (message has the detail) */
@@ -53,7 +53,8 @@ typedef struct {
   int order;        /* p: degrees 0..p-1 (kernels.cpp:25) */
   int n_crit;       /* max bodies per leaf (tree.cpp:78) */
   double theta;     /* MAC opening parameter, in (0,1) (traversal.cpp:8-13) */
-  int mutual;       /* must be 0 in this release (non-mutual, target-owned writes) */
+  int mutual;       /* 1: mutual traversal (traversal.hpp:76-84): each unordered pair emitted
+                       once; executed by the target-owned kernels on the symmetrised lists */
   int precision;    /* fmm_precision */
   int device;       /* CUDA device ordinal */
   int with_acc;     /* 1: also produce acceleration = -grad phi (extension) */
@@ -66,10 +67,13 @@ typedef struct {
   int32_t depth;            /* deepest level present */
   double center[3];         /* Domain (types.hpp:21-28) */
   double half_side;
-  int64_t n_m2l;            /* emitted M2L pairs */
-  int64_t n_p2p;            /* emitted P2P leaf pairs */
-  int64_t p2p_body_pairs;   /* sum over P2P leaf pairs of n_t * n_s */
+  int64_t n_m2l;            /* emitted M2L pairs (mutual: once per unordered pair) */
+  int64_t n_p2p;            /* emitted P2P leaf pairs (mutual: once per unordered pair) */
+  int64_t p2p_body_pairs;   /* sum over the executed P2P leaf pairs of n_t * n_s */
   int32_t level_start[FMM_MAX_LEVEL + 2]; /* cells of level l are [level_start[l], level_start[l+1]) */
+  int32_t mutual;           /* lists were emitted by the mutual traversal */
+  int64_t n_m2l_exec;       /* executed (target-owned) M2L pairs: n_m2l, or 2 n_m2l in mutual mode */
+  int64_t n_p2p_exec;       /* executed P2P leaf pairs: n_p2p, or 2 n_p2p - nleaves in mutual mode */
 } fmm_tree_info;
 
 /* Per-stage device times (ms) of the last fmm_evaluate / stage call, CUDA-event timed. */
@@ -105,6 +109,11 @@ int fmm_synchronize(fmm_ctx* ctx);
  * stream concurrently with the dual tree traversal and its list building; M2L joins both.
  * 0 serialises every stage on one stream (each kernel timed alone). */
 int fmm_set_overlap(fmm_ctx* ctx, int on);
+/* TraversalConfig::mutual (traversal.hpp:19-23) for the next traversal / load_lists: 1 = each
+ * unordered pair emitted once (m2l_mutual / mutual p2p semantics, kernels.cpp:113-126, :153-180).
+ * The GPU executes the symmetrised lists with target-owned writes (no atomics): results equal
+ * the non-mutual mode's. Invalidates the current lists. Not supported with fmm_set_partition. */
+int fmm_set_mutual(fmm_ctx* ctx, int on);
 
 /* ---- outputs ------------------------------------------------------------------------ */
 /* order: 0 = tree (sorted) body order (potentials(), tree.cpp:121-126), 1 = input order.
@@ -114,6 +123,17 @@ int fmm_get_results(fmm_ctx* ctx, double* phi, double* acc, int order);
 int fmm_results_device(fmm_ctx* ctx, const double** d_phi, const double** d_acc);
 int fmm_get_tree_info(fmm_ctx* ctx, fmm_tree_info* info);
 int fmm_get_stage_times(fmm_ctx* ctx, fmm_stage_times* t);
+/* Stage-level execution trace of the last fmm_evaluate, in the reference's trace CSV vocabulary
+ * (Scheduler::export_trace, scheduler.cpp:305-317: task_id,worker_id,kind,start_ns,end_ns):
+ * one row per GPU stage (build, traversal, upward, m2l, p2p, downward); worker_id = the stream
+ * (0 = FMM stream, 1 = overlap stream); times from CUDA events, relative to the step start.
+ * Writes min(max_rows, *n_rows) rows; *n_rows = rows available. */
+typedef struct {
+  int32_t task_id, worker_id;
+  char kind[16];
+  int64_t start_ns, end_ns;
+} fmm_trace_row;
+int fmm_get_stage_trace(fmm_ctx* ctx, fmm_trace_row* rows, int max_rows, int* n_rows);
 
 /* ---- parity exports (reference layout; any pointer may be NULL) --------------------- */
 int fmm_get_cells(fmm_ctx* ctx, int32_t* level, uint64_t* key, double* center3, double* radius,
@@ -121,7 +141,9 @@ int fmm_get_cells(fmm_ctx* ctx, int32_t* level, uint64_t* key, double* center3, 
                   int32_t* child_count, int32_t* parent);
 int fmm_get_permutation(fmm_ctx* ctx, int64_t* perm); /* perm[i] = input index of body i */
 /* Lists as CSR by target cell: offsets[ncells+1], sources[n]; sources are in ascending
- * order within each target (a canonical form of the emitted multiset). */
+ * order within each target (a canonical form of the emitted multiset). In mutual mode these
+ * are the emitted pairs (n = info.n_m2l / n_p2p), each unordered pair once in the orientation
+ * the mutual traversal emitted it. */
 int fmm_get_lists(fmm_ctx* ctx, int64_t* m2l_offsets, int32_t* m2l_sources,
                   int64_t* p2p_offsets, int32_t* p2p_sources);
 /* Multipoles / locals, ncells x n_coef in the reference coefficient order and convention

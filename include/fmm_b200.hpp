@@ -138,14 +138,18 @@ class KernelTables {  // kernels.hpp:24-54 (term tables are compile-time on the 
 // lists run through the GPU M2L and P2P kernels.
 class KernelVisitor {
  public:
-  KernelVisitor(Tree& targets, Tree& sources, const KernelTables&, bool mutual) : tree_(&targets) {
+  KernelVisitor(Tree& targets, Tree& sources, const KernelTables&, bool mutual)
+      : tree_(&targets), mutual_(mutual) {
     if (&targets != &sources) throw std::invalid_argument("distinct target/source trees are not supported");
-    if (mutual) throw std::invalid_argument("mutual mode is not implemented on the GPU path");
   }
   Tree* tree() const { return tree_; }
+  // mutual (m2l_mutual / mutual p2p, kernels.cpp:113-126, :153-180): the GPU executes the
+  // symmetrised lists with target-owned writes, accumulating the same sums
+  bool mutual() const { return mutual_; }
 
  private:
   Tree* tree_;
+  bool mutual_;
 };
 
 inline void upward_pass(Tree& tree, const KernelTables&) { check(fmm_upward(tree.ctx()), tree.ctx()); }
@@ -156,8 +160,10 @@ inline void downward_pass(Tree& tree, const KernelTables&) {  // traversal.cpp:5
 }
 
 namespace detail {
-inline void traverse_lists(const Tree& t, std::vector<std::int64_t>& mo, std::vector<std::int32_t>& ms,
-                           std::vector<std::int64_t>& po, std::vector<std::int32_t>& ps) {
+inline void traverse_lists(const Tree& t, bool mutual, std::vector<std::int64_t>& mo,
+                           std::vector<std::int32_t>& ms, std::vector<std::int64_t>& po,
+                           std::vector<std::int32_t>& ps) {
+  check(fmm_set_mutual(t.ctx(), mutual ? 1 : 0), t.ctx());
   check(fmm_traverse(t.ctx()), t.ctx());
   fmm_tree_info info{};
   check(fmm_get_tree_info(t.ctx(), &info), t.ctx());
@@ -178,7 +184,7 @@ void dual_tree_traverse(const Tree& targets, const Tree& sources, const Traversa
   if (!(cfg.theta > 0.0 && cfg.theta < 1.0)) throw std::invalid_argument("theta must be in (0,1)");
   std::vector<std::int64_t> mo, po;
   std::vector<std::int32_t> ms, ps;
-  detail::traverse_lists(targets, mo, ms, po, ps);
+  detail::traverse_lists(targets, cfg.mutual, mo, ms, po, ps);
   for (std::size_t t = 0; t + 1 < mo.size(); ++t)
     for (std::int64_t k = mo[t]; k < mo[t + 1]; ++k) visit.m2l_pair(static_cast<std::int32_t>(t), ms[k]);
   for (std::size_t t = 0; t + 1 < po.size(); ++t)
@@ -188,7 +194,9 @@ void dual_tree_traverse(const Tree& targets, const Tree& sources, const Traversa
 template <class DrainSink>
 void dual_tree_traverse(Tree& targets, Tree&, const TraversalConfig& cfg, KernelVisitor& visit, DrainSink&&) {
   if (!(cfg.theta > 0.0 && cfg.theta < 1.0)) throw std::invalid_argument("theta must be in (0,1)");
+  if (visit.mutual() != cfg.mutual) throw std::invalid_argument("KernelVisitor and TraversalConfig disagree on mutual");
   fmm_ctx* c = visit.tree()->ctx();
+  check(fmm_set_mutual(c, cfg.mutual ? 1 : 0), c);
   check(fmm_traverse(c), c);
   check(fmm_m2l(c), c);
   check(fmm_p2p(c), c);

@@ -51,7 +51,8 @@ class TreeInfo(C.Structure):
     _fields_ = [("nbodies", C.c_int64), ("ncells", C.c_int64), ("nleaves", C.c_int64),
                 ("depth", C.c_int32), ("center", C.c_double * 3), ("half_side", C.c_double),
                 ("n_m2l", C.c_int64), ("n_p2p", C.c_int64), ("p2p_body_pairs", C.c_int64),
-                ("level_start", C.c_int32 * (FMM_MAX_LEVEL + 2))]
+                ("level_start", C.c_int32 * (FMM_MAX_LEVEL + 2)), ("mutual", C.c_int32),
+                ("n_m2l_exec", C.c_int64), ("n_p2p_exec", C.c_int64)]
 
 
 class StageTimes(C.Structure):
@@ -60,6 +61,11 @@ class StageTimes(C.Structure):
                 ("total_ms", C.c_float), ("p2p_kernel_ms", C.c_float),
                 ("m2l_kernel_ms", C.c_float), ("p2p_launches", C.c_int32),
                 ("m2l_launches", C.c_int32), ("kernel_launches", C.c_int32)]
+
+
+class TraceRow(C.Structure):
+    _fields_ = [("task_id", C.c_int32), ("worker_id", C.c_int32), ("kind", C.c_char * 16),
+                ("start_ns", C.c_int64), ("end_ns", C.c_int64)]
 
 
 class ShardInfo(C.Structure):
@@ -91,6 +97,8 @@ SIGNATURES = {
     "fmm_evaluate": (C.c_int, [_vp]),
     "fmm_synchronize": (C.c_int, [_vp]),
     "fmm_set_overlap": (C.c_int, [_vp, C.c_int]),
+    "fmm_set_mutual": (C.c_int, [_vp, C.c_int]),
+    "fmm_get_stage_trace": (C.c_int, [_vp, _vp, C.c_int, C.POINTER(C.c_int)]),
     "fmm_get_results": (C.c_int, [_vp, _dp, _dp, C.c_int]),
     "fmm_results_device": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(_vp)]),
     "fmm_get_tree_info": (C.c_int, [_vp, C.POINTER(TreeInfo)]),

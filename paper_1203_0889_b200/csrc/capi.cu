@@ -88,7 +88,6 @@ int fmm_create(const fmm_config* cfg, fmm_ctx** out) {
     if (cfg->order > FMM_MAX_ORDER) fail(FMM_ERR_UNSUPPORTED, "expansion order above FMM_MAX_ORDER (10)");
     if (cfg->n_crit < 1) fail(FMM_ERR_NCRIT, "n_crit must be >= 1");
     if (!(cfg->theta > 0.0 && cfg->theta < 1.0)) fail(FMM_ERR_THETA, "theta must be in (0,1)");
-    if (cfg->mutual) fail(FMM_ERR_UNSUPPORTED, "mutual mode is not implemented on the GPU path");
     if (cfg->precision != FMM_PREC_FP64 && cfg->precision != FMM_PREC_FP32_P2P)
       fail(FMM_ERR_ARG, "unknown precision mode");
     require_device();
@@ -268,6 +267,37 @@ int fmm_evaluate(fmm_ctx* c) {
   });
 }
 
+int fmm_get_stage_trace(fmm_ctx* c, fmm_trace_row* rows, int max_rows, int* n_rows) {
+  if (!c || !n_rows || (max_rows > 0 && !rows)) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_out) fail(FMM_ERR_STATE, "stage trace: no evaluated step");
+    struct Span {
+      const char* kind;
+      int worker, a, b;
+    };
+    // fmm_evaluate's event graph: stream 0 = the FMM stream, 1 = the overlap stream (upward)
+    const Span spans[] = {
+        {"build", 0, EV_BUILD0, EV_BUILD1},
+        {"traversal", 0, EV_BUILD1, EV_TRAV1},
+        {"upward", c->overlap ? 1 : 0, c->overlap ? EV_BUILD1 : EV_TRAV1, EV_UP1},
+        {"m2l", 0, EV_FORK, EV_M2L1},
+        {"p2p", 0, EV_M2L1, EV_P2P1},
+        {"downward", 0, EV_P2P1, EV_DOWN1},
+    };
+    const int n = static_cast<int>(sizeof(spans) / sizeof(spans[0]));
+    *n_rows = n;
+    for (int i = 0; i < n && i < max_rows; ++i) {
+      fmm_trace_row& r = rows[i];
+      std::memset(&r, 0, sizeof(r));
+      r.task_id = i;
+      r.worker_id = spans[i].worker;
+      std::strncpy(r.kind, spans[i].kind, sizeof(r.kind) - 1);
+      r.start_ns = static_cast<int64_t>(1e6 * ms_between(c->ev[EV_BUILD0], c->ev[spans[i].a]));
+      r.end_ns = static_cast<int64_t>(1e6 * ms_between(c->ev[EV_BUILD0], c->ev[spans[i].b]));
+    }
+  });
+}
+
 int fmm_synchronize(fmm_ctx* c) {
   if (!c) return FMM_ERR_ARG;
   return guard(c, [&] {
@@ -323,10 +353,13 @@ int fmm_get_tree_info(fmm_ctx* c, fmm_tree_info* info) {
     info->depth = c->depth;
     for (int d = 0; d < 3; ++d) info->center[d] = c->center[d];
     info->half_side = c->half_side;
-    info->n_m2l = c->have_lists ? c->n_m2l : -1;
-    info->n_p2p = c->have_lists ? c->n_p2p : -1;
+    info->n_m2l = c->have_lists ? c->n_m2l_emit : -1;
+    info->n_p2p = c->have_lists ? c->n_p2p_emit : -1;
     info->p2p_body_pairs = c->have_lists ? c->p2p_body_pairs : -1;
     for (int l = 0; l < FMM_MAX_LEVEL + 2; ++l) info->level_start[l] = c->level_start[l];
+    info->mutual = c->cfg.mutual ? 1 : 0;
+    info->n_m2l_exec = c->have_lists ? c->n_m2l : -1;
+    info->n_p2p_exec = c->have_lists ? c->n_p2p : -1;
   });
 }
 
@@ -392,11 +425,39 @@ int fmm_get_lists(fmm_ctx* c, int64_t* m2l_offsets, int32_t* m2l_sources, int64_
     auto cp = [&](void* dst, const void* src, size_t bytes) {
       if (dst && bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
     };
-    cp(m2l_offsets, c->m2l_off.p, (c->ncells + 1) * 8);
-    cp(m2l_sources, c->m2l_src.p, c->n_m2l * 4);
-    cp(p2p_offsets, c->p2p_off.p, (c->ncells + 1) * 8);
-    cp(p2p_sources, c->p2p_src.p, c->n_p2p * 4);
-    CK(cudaStreamSynchronize(c->stream));
+    if (!c->cfg.mutual) {
+      cp(m2l_offsets, c->m2l_off.p, (c->ncells + 1) * 8);
+      cp(m2l_sources, c->m2l_src.p, c->n_m2l * 4);
+      cp(p2p_offsets, c->p2p_off.p, (c->ncells + 1) * 8);
+      cp(p2p_sources, c->p2p_src.p, c->n_p2p * 4);
+      CK(cudaStreamSynchronize(c->stream));
+      return;
+    }
+    // mutual: the emitted list (once per unordered pair, in its emitted orientation) = the
+    // executed CSR without the mirrored entries
+    auto emitted = [&](const fmmb::DBuf<int64_t>& off, const fmmb::DBuf<int32_t>& src,
+                       const fmmb::DBuf<uint8_t>& mir, int64_t n, int64_t* o_off, int32_t* o_src) {
+      if (!o_off && !o_src) return;
+      std::vector<int64_t> ho(c->ncells + 1);
+      std::vector<int32_t> hs(n);
+      std::vector<uint8_t> hm(n);
+      cp(ho.data(), off.p, (c->ncells + 1) * 8);
+      cp(hs.data(), src.p, n * 4);
+      cp(hm.data(), mir.p, n);
+      CK(cudaStreamSynchronize(c->stream));
+      int64_t k = 0;
+      for (int64_t t = 0; t < c->ncells; ++t) {
+        if (o_off) o_off[t] = k;
+        for (int64_t i = ho[t]; i < ho[t + 1]; ++i)
+          if (!hm[i]) {
+            if (o_src) o_src[k] = hs[i];
+            ++k;
+          }
+      }
+      if (o_off) o_off[c->ncells] = k;
+    };
+    emitted(c->m2l_off, c->m2l_src, c->m2l_mir, c->n_m2l, m2l_offsets, m2l_sources);
+    emitted(c->p2p_off, c->p2p_src, c->p2p_mir, c->n_p2p, p2p_offsets, p2p_sources);
   });
 }
 
@@ -525,11 +586,22 @@ int fmm_set_overlap(fmm_ctx* c, int on) {
   return FMM_OK;
 }
 
+int fmm_set_mutual(fmm_ctx* c, int on) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if ((c->cfg.mutual != 0) == (on != 0)) return;
+    if (on && c->world > 1) fail(FMM_ERR_UNSUPPORTED, "mutual mode is not supported by the sharded traversal");
+    c->cfg.mutual = on != 0;
+    c->have_lists = c->have_L = c->have_out = false;  // the lists depend on the mode
+  });
+}
+
 // ---------------------------------------------------------------------- sharding -------
 int fmm_set_partition(fmm_ctx* c, int rank, int world) {
   if (!c) return FMM_ERR_ARG;
   return guard(c, [&] {
     if (world < 1 || rank < 0 || rank >= world) fail(FMM_ERR_ARG, "bad rank/world");
+    if (world > 1 && c->cfg.mutual) fail(FMM_ERR_UNSUPPORTED, "mutual mode is not supported by the sharded traversal");
     if (world != c->world) c->plan_world = 0;
     c->rank = rank;
     c->world = world;
@@ -717,10 +789,16 @@ int fmm_op_mac(int64_t count, const double* tcenter3, const double* tradius, con
 // ----------------------------------------------------------------- synthetic inputs ----
 // BASELINE.json configs: the reference's xorshift64* (dataset.cpp:10-34),
 // position drawn before charge, Vec3(u(),u(),u()) evaluated right-to-left by g++ (z first).
+static void generate_reference(int dist, int64_t n, uint64_t seed, double* xyzq);
+
 int fmm_generate_bodies(int config, int64_t n, uint64_t seed, double* xyzq) {
   return guard(nullptr, [&] {
     if (n <= 0) fail(FMM_ERR_EMPTY_INPUT, "empty input");
     if (!xyzq) fail(FMM_ERR_ARG, "null output");
+    if (config >= 10 && config <= 12) {
+      generate_reference(config, n, seed, xyzq);
+      return;
+    }
     auto splitmix = [](uint64_t x) {
       x += 0x9E3779B97F4A7C15ULL;
       x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -787,10 +865,79 @@ int fmm_generate_bodies(int config, int64_t n, uint64_t seed, double* xyzq) {
           break;
         }
         default:
-          fail(FMM_ERR_ARG, "unknown config (1..5)");
+          fail(FMM_ERR_ARG, "unknown config (1..5, 10..12)");
       }
     }
   });
+}
+
+// The reference's own generate_bodies (dataset.cpp:76-111): 10 = cube (uniform [0,1]^3),
+// 11 = sphere-surface (cube rejection, dataset.cpp:55-64), 12 = cluster (8 Irwin-Hall blobs,
+// sigma 0.03, dataset.cpp:67-72); charges uniform(-1,1) then mean-subtracted. Vec3(a(), b(), c())
+// draws are evaluated right-to-left as g++ does (z first), like the reference build.
+static void generate_reference(int dist, int64_t n, uint64_t seed, double* xyzq) {
+  auto splitmix = [](uint64_t x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+  };
+  uint64_t st = splitmix(seed);
+  if (st == 0) st = 0x9E3779B97F4A7C15ULL;
+  auto next = [&]() {
+    st ^= st >> 12;
+    st ^= st << 25;
+    st ^= st >> 27;
+    return st * 2685821657736338717ULL;
+  };
+  auto u01 = [&]() { return static_cast<double>(next() >> 11) * 0x1.0p-53; };
+  auto uni = [&](double lo, double hi) { return lo + (hi - lo) * u01(); };
+  auto normal = [&]() {  // Irwin-Hall: sum of 12 uniforms minus 6
+    double s = 0.0;
+    for (int k = 0; k < 12; ++k) s += u01();
+    return s - 6.0;
+  };
+  double blob[8][3];
+  if (dist == 12)
+    for (auto& c : blob) {
+      c[2] = u01();
+      c[1] = u01();
+      c[0] = u01();
+    }
+  for (int64_t i = 0; i < n; ++i) {
+    double* b = xyzq + 4 * i;
+    if (dist == 10) {
+      b[2] = u01();
+      b[1] = u01();
+      b[0] = u01();
+    } else if (dist == 11) {
+      for (;;) {
+        double v[3];
+        v[2] = uni(-1.0, 1.0);
+        v[1] = uni(-1.0, 1.0);
+        v[0] = uni(-1.0, 1.0);
+        const double r2 = (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2];
+        if (r2 > 1.0 || r2 < 1e-8) continue;
+        const double r = std::sqrt(r2);
+        b[0] = v[0] / r;
+        b[1] = v[1] / r;
+        b[2] = v[2] / r;
+        break;
+      }
+    } else {
+      const double* c = blob[next() % 8];
+      double g[3];
+      g[2] = normal();
+      g[1] = normal();
+      g[0] = normal();
+      for (int d = 0; d < 3; ++d) b[d] = c[d] + 0.03 * g[d];
+    }
+    b[3] = uni(-1.0, 1.0);
+  }
+  double mean = 0.0;
+  for (int64_t i = 0; i < n; ++i) mean += xyzq[4 * i + 3];
+  mean /= static_cast<double>(n);
+  for (int64_t i = 0; i < n; ++i) xyzq[4 * i + 3] -= mean;
 }
 
 }  // extern "C"

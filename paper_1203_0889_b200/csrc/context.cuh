@@ -5,6 +5,7 @@
 //   xyzq_in   double4[N]   input bodies (input order)
 //   bodies    double4[N]   x,y,z,q in tree order (FP64 P2P, P2M, L2P)
 //   bodyf     float4[N]    x-cx,y-cy,z-cz,q relative to the body's own leaf centre (FP32 P2P)
+//   bodyl     float4[N]    the FP32 rounding residuals of bodyf's x,y,z (compensated near tiles)
 //   perm      int32[N]     tree-order body -> input index
 //   cells     SoA: level i32, key u64, cr double4 (cx,cy,cz,radius), body_begin/end,
 //             child_begin/count, parent (i32) — reference Cell (tree.hpp:21-36), BFS order
@@ -33,6 +34,7 @@ struct fmm_ctx {
   fmmb::DBuf<double4> xyzq_in;
   fmmb::DBuf<double4> bodies;
   fmmb::DBuf<float4> bodyf;
+  fmmb::DBuf<float4> bodyl;
   fmmb::DBuf<int32_t> perm;
   fmmb::DBuf<int32_t> leaf_of_body;  // tree-order body -> leaf cell index
 
@@ -48,7 +50,10 @@ struct fmm_ctx {
   fmmb::DBuf<int32_t> leaves;  // leaf cell indices, ascending
 
   // lists (CSR by target)
-  int64_t n_m2l = 0, n_p2p = 0, p2p_body_pairs = 0;
+  int64_t n_m2l = 0, n_p2p = 0, p2p_body_pairs = 0;  // executed lists (mutual: symmetrised)
+  int64_t n_m2l_emit = 0, n_p2p_emit = 0;            // emitted pairs (mutual: once per unordered pair)
+  fmmb::DBuf<uint8_t> m2l_mir, p2p_mir;              // mutual: 1 = entry is a mirror of an emitted pair
+  fmmb::DBuf<uint64_t> mut_keys;                     // mutual: emitted + mirrored keys
   fmmb::DBuf<int64_t> m2l_off, p2p_off;
   fmmb::DBuf<int32_t> m2l_src, p2p_src;
   fmmb::DBuf<int32_t> m2l_targets;  // cells with non-empty M2L lists
@@ -60,7 +65,8 @@ struct fmm_ctx {
   fmmb::DBuf<double> p2p_partial;   // [slot][target body][4] (phi, ax, ay, az)
   fmmb::DBuf<int4> p2p_reduce;      // target leaf, first slot, n slots, body begin
   fmmb::DBuf<int64_t> p2p_pre;      // exclusive prefix of source-body counts over the P2P list
-  fmmb::DBuf<int4> p2p_ent;         // per P2P list entry: {body_begin, count, shift.xy} + {shift.z,...}
+  fmmb::DBuf<int4> p2p_ent;
+  fmmb::DBuf<double4> leaf_lo, leaf_hi;  // tight body boxes of the leaves (FP32 P2P near test)         // per P2P list entry: {body_begin, count, shift.xy} + {shift.z,...}
   int64_t n_p2p_reduce = 0;
 
   // expansions and outputs

@@ -102,19 +102,26 @@ __device__ __forceinline__ void tile_setup(int tid, int32_t le, int32_t cursor, 
 // raw bodies stream into the other buffer with cp.async (no registers), and warp 0 resolves
 // tile k+2's list entries. After the compute, each thread converts the bodies it copied in
 // place (shift into the target frame, negate), and one barrier per tile publishes them.
-struct P2PEnt {  // one P2P list entry (target-specific): source bodies and FP32 frame shift
-  int32_t bb, n;
-  float sx, sy, sz;
-  int32_t self;  // 1 for the (leaf, leaf) entry: the only one that can hold r^2 == 0 pairs
-  int32_t pad[2];
+// One P2P list entry (target specific): source bodies and the FP64 centre difference into the
+// target leaf frame as an FP32 hi + lo pair. kind (top two bits of nk): 0 = far, 1 = the
+// (leaf, leaf) self entry (the only one that can hold r^2 == 0 pairs), 2 = near (the two
+// leaves' body boxes nearly touch: the only entries whose body pairs can be close relative to
+// the leaf size). Self and near entries run compensated tiles.
+struct P2PEnt {
+  int32_t bb, nk;         // first source body; count | kind << 30
+  float sx, sy, sz;       // shift hi
+  float lx, ly, lz;       // shift lo
 };
 static_assert(sizeof(P2PEnt) == 32, "P2PEnt is 32 B");
+constexpr int kKindFar = 0, kKindSelf = 1, kKindNear = 2;
+constexpr int kHalfTile = kTileBodies / 2;  // compensated tiles: hi in [0, half), lo in [half, 2 half)
 
 struct TileTab {
   int32_t off[kTileSegs + 1];
   int32_t bb[kTileSegs];
   float sh[kTileSegs][3];
-  int32_t nseg, next, next_off, guard;
+  float sl[kTileSegs][3];
+  int32_t nseg, next, next_off, guard, prec;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -138,67 +145,80 @@ __device__ __forceinline__ void ent_prefetch(int lane, int32_t cursor, int32_t l
 __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cursor, int32_t cur_off,
                                                const P2PEnt* e, TileTab& tt) {
   const int32_t k = cursor + lane;
-  int32_t n = 0, b = 0, self = 0;
-  float sx = 0.f, sy = 0.f, sz = 0.f;
+  int32_t n = 0, b = 0, kind = kKindFar;
+  float sx = 0.f, sy = 0.f, sz = 0.f, lx = 0.f, ly = 0.f, lz = 0.f;
   if (k < le) {
     const int4 e0 = reinterpret_cast<const int4*>(e)[2 * lane];
-    const int2 e1 = reinterpret_cast<const int2*>(e)[4 * lane + 2];
+    const int4 e1 = reinterpret_cast<const int4*>(e)[2 * lane + 1];
     b = e0.x;
-    n = e0.y;
+    n = e0.y & 0x3fffffff;
+    kind = static_cast<int>(static_cast<uint32_t>(e0.y) >> 30);
     sx = __int_as_float(e0.z);
     sy = __int_as_float(e0.w);
     sz = __int_as_float(e1.x);
-    self = e1.y;
+    lx = __int_as_float(e1.y);
+    ly = __int_as_float(e1.z);
+    lz = __int_as_float(e1.w);
     if (lane == 0) {
       b += cur_off;
       n -= cur_off;
     }
   }
+  // one class per tile: the self entry alone (r^2 == 0 guard), near entries (compensated, half
+  // the bodies: hi and lo staged), far entries (plain FP32)
+  const int kind0 = __shfl_sync(0xffffffffu, kind, 0);
+  const int cap = kind0 == kKindFar ? kTileBodies : kHalfTile;
   int32_t incl = n;
   for (int o = 1; o < 32; o <<= 1) {
     const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
   }
-  const bool fits = (k < le) && (incl <= kTileBodies);
+  const bool fits = (k < le) && (incl <= cap);
   const unsigned m = __ballot_sync(0xffffffffu, fits);
-  const unsigned sm = __ballot_sync(0xffffffffu, self != 0);
+  const unsigned other = __ballot_sync(0xffffffffu, (k < le) && kind != kind0);
   int nseg;
-  if (m == 0) {  // one (level-21 overflow) leaf larger than the tile: take kTileBodies of it
+  if (m == 0) {  // one (level-21 overflow) leaf larger than the tile: take cap of its bodies
     nseg = 1;
-    incl = kTileBodies;
+    incl = cap;
   } else {
     nseg = 32 - __clz(m);  // fits is a prefix of the lanes
   }
-  // the self entry gets a tile of its own: only that tile runs the r^2 == 0 guard
-  if (sm & 1u) nseg = 1;
-  else if (sm) nseg = min(nseg, __ffs(sm) - 1);
+  if (kind0 == kKindSelf) nseg = 1;
+  else if (other) nseg = min(nseg, __ffs(other) - 1);
   if (lane < nseg) {
     tt.off[lane + 1] = incl;
     tt.bb[lane] = b;
     tt.sh[lane][0] = sx;
     tt.sh[lane][1] = sy;
     tt.sh[lane][2] = sz;
+    tt.sl[lane][0] = lx;
+    tt.sl[lane][1] = ly;
+    tt.sl[lane][2] = lz;
   }
   if (lane == 0) {
     tt.off[0] = 0;
     tt.nseg = nseg;
     tt.next = m == 0 ? cursor : cursor + nseg;
-    tt.next_off = m == 0 ? cur_off + kTileBodies : 0;
-    tt.guard = static_cast<int32_t>(sm & 1u);
+    tt.next_off = m == 0 ? cur_off + cap : 0;
+    tt.guard = kind0 == kKindSelf ? 1 : 0;
+    tt.prec = kind0 == kKindFar ? 0 : 1;
   }
 }
 
 // warp 0: one bulk copy per list entry of the tile (lane k copies entry k's bodies); the bytes
 // land on `bar`. The proxy fence orders the CTA's earlier generic reads/writes of the buffer
 // (published by the preceding __syncthreads) before the async-proxy writes.
-__device__ __forceinline__ void tile_tma(int lane, const TileTab& tt, const float4* __restrict__ bodyf, float4* buf,
-                                         uint64_t* bar) {
+__device__ __forceinline__ void tile_tma(int lane, const TileTab& tt, const float4* __restrict__ bodyf,
+                                         const float4* __restrict__ bodyl, float4* buf, uint64_t* bar) {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   const int nseg = tt.nseg;
-  if (lane == 0) mbar_arrive_expect_tx(bar, static_cast<unsigned>(tt.off[nseg]) * 16u);
+  const bool prec = tt.prec != 0;
+  if (lane == 0) mbar_arrive_expect_tx(bar, static_cast<unsigned>(tt.off[nseg]) * (prec ? 32u : 16u));
   if (lane < nseg) {
     const int32_t o0 = tt.off[lane];
-    bulk_g2s(buf + o0, bodyf + tt.bb[lane], static_cast<unsigned>(tt.off[lane + 1] - o0) * 16u, bar);
+    const unsigned bytes = static_cast<unsigned>(tt.off[lane + 1] - o0) * 16u;
+    bulk_g2s(buf + o0, bodyf + tt.bb[lane], bytes, bar);
+    if (prec) bulk_g2s(buf + kHalfTile + o0, bodyl + tt.bb[lane], bytes, bar);
   }
 }
 
@@ -233,6 +253,31 @@ __device__ __forceinline__ void tile_convert(int tid, const TileTab& tt, float4*
   }
 }
 
+// Compensated tiles: (x - c_s) + (c_s - c_t) = (hi_b + lo_b) + (S_hi + S_lo) with hi_b + S_hi
+// split exactly by TwoSum; stored negated as hi at [o], lo at [half + o]. A close pair's
+// difference then keeps ~48 bits instead of an absolute error of the leaf size * 2^-24.
+__device__ __forceinline__ float2 two_sum(float a, float b) {
+  const float s = __fadd_rn(a, b);
+  const float bb = __fsub_rn(s, a);
+  const float e = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
+  return make_float2(s, e);
+}
+
+__device__ __forceinline__ void tile_convert_prec(int tid, const TileTab& tt, float4* buf) {
+  const int nb = tt.off[tt.nseg];
+  const int nseg = tt.nseg;
+#pragma unroll 1
+  for (int j = tid; j < nb; j += kThreads) {
+    int k = 0;  // entry of body j (<= 32 entries: linear scan of the offsets)
+    while (k + 1 < nseg && tt.off[k + 1] <= j) ++k;
+    const float4 h = buf[j], l = buf[kHalfTile + j];
+    const float2 x = two_sum(h.x, tt.sh[k][0]), y = two_sum(h.y, tt.sh[k][1]), z = two_sum(h.z, tt.sh[k][2]);
+    buf[j] = make_float4(-x.x, -y.x, -z.x, h.w);
+    buf[kHalfTile + j] = make_float4(-((x.y + l.x) + tt.sl[k][0]), -((y.y + l.y) + tt.sl[k][1]),
+                                     -((z.y + l.z) + tt.sl[k][2]), 0.f);
+  }
+}
+
 __device__ __forceinline__ float rsqrt_approx(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -241,18 +286,13 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 
 // One source against the thread's two targets: 13 FP32-pipe lane-ops per pair (3 dx, 3 r^2,
 // q/r, phi, 1/r^2, q/r^3, 3 acc) and one MUFU.RSQ (XU pipe: 16/clk/SM, so a second MUFU per
-// pair would make the XU the bottleneck); r^2 == 0 pairs (self, coincident;
-// kernels.cpp:185-186) are predicated off.
-//
-// kGuard = false (every entry but the self one: the bodies are distinct, r^2 > 0): r^2 is
-// seeded with 1e-30 instead of predicating the MUFU, which keeps the result finite even if
-// two distinct bodies round to the same FP32 offsets, at no instruction cost.
+// pair would make the XU the bottleneck). kGuard (the self tile only): r^2 == 0 pairs (self,
+// coincident; kernels.cpp:185-186) are predicated off. Otherwise the bodies are distinct and
+// r^2 is seeded with 1e-30 instead of predicating the MUFU, which keeps the result finite even
+// if two distinct bodies round to the same FP32 offsets, at no instruction cost.
 template <bool kAcc, bool kGuard>
-__device__ __forceinline__ void pair_body(const float4 sv, const float2 X, const float2 Y, const float2 Z, float2& ph,
-                                          float2& ax, float2& ay, float2& az) {
-  const float2 dx = __fadd2_rn(X, make_float2(sv.x, sv.x));
-  const float2 dy = __fadd2_rn(Y, make_float2(sv.y, sv.y));
-  const float2 dz = __fadd2_rn(Z, make_float2(sv.z, sv.z));
+__device__ __forceinline__ void pair_finish(const float2 dx, const float2 dy, const float2 dz, const float q,
+                                            float2& ph, float2& ax, float2& ay, float2& az) {
   float2 r2 = kGuard ? __fmul2_rn(dx, dx) : __ffma2_rn(dx, dx, make_float2(1e-30f, 1e-30f));
   r2 = __ffma2_rn(dy, dy, r2);
   r2 = __ffma2_rn(dz, dz, r2);
@@ -264,7 +304,7 @@ __device__ __forceinline__ void pair_body(const float4 sv, const float2 X, const
   } else {
     ri = make_float2(rsqrt_approx(r2.x), rsqrt_approx(r2.y));
   }
-  const float2 qr = __fmul2_rn(make_float2(sv.w, sv.w), ri);
+  const float2 qr = __fmul2_rn(make_float2(q, q), ri);
   ph = __fadd2_rn(ph, qr);
   if constexpr (kAcc) {
     const float2 qr3 = __fmul2_rn(qr, __fmul2_rn(ri, ri));
@@ -274,10 +314,49 @@ __device__ __forceinline__ void pair_body(const float4 sv, const float2 X, const
   }
 }
 
+template <bool kAcc>
+__device__ __forceinline__ void pair_body(const float4 sv, const float2 X, const float2 Y, const float2 Z, float2& ph,
+                                          float2& ax, float2& ay, float2& az) {
+  const float2 dx = __fadd2_rn(X, make_float2(sv.x, sv.x));
+  const float2 dy = __fadd2_rn(Y, make_float2(sv.y, sv.y));
+  const float2 dz = __fadd2_rn(Z, make_float2(sv.z, sv.z));
+  pair_finish<kAcc, false>(dx, dy, dz, sv.w, ph, ax, ay, az);
+}
+
+// compensated pair (self and near tiles): dx = (X_hi - s_hi) + (X_lo - s_lo); the hi difference
+// is exact for close pairs (Sterbenz), so the pair distance keeps ~48 bits: 6 more FADD2
+struct Tgt {
+  float2 X, Y, Z, XL, YL, ZL;
+};
 template <bool kAcc, bool kGuard>
-__device__ __forceinline__ void tile_compute(const float4* __restrict__ buf, int nb, int g, int G, float2 X,
-                                             float2 Y, float2 Z, double& ph0, double& ph1, double& ax0,
-                                             double& ax1, double& ay0, double& ay1, double& az0, double& az1) {
+__device__ __forceinline__ void pair_body_prec(const float4 sh, const float4 sl, const Tgt& T, float2& ph, float2& ax,
+                                               float2& ay, float2& az) {
+  const float2 dx = __fadd2_rn(__fadd2_rn(T.X, make_float2(sh.x, sh.x)), __fadd2_rn(T.XL, make_float2(sl.x, sl.x)));
+  const float2 dy = __fadd2_rn(__fadd2_rn(T.Y, make_float2(sh.y, sh.y)), __fadd2_rn(T.YL, make_float2(sl.y, sl.y)));
+  const float2 dz = __fadd2_rn(__fadd2_rn(T.Z, make_float2(sh.z, sh.z)), __fadd2_rn(T.ZL, make_float2(sl.z, sl.z)));
+  pair_finish<kAcc, kGuard>(dx, dy, dz, sh.w, ph, ax, ay, az);
+}
+
+struct Acc64 {
+  double ph0 = 0.0, ph1 = 0.0, ax0 = 0.0, ax1 = 0.0, ay0 = 0.0, ay1 = 0.0, az0 = 0.0, az1 = 0.0;
+  // fold one tile's FP32 partials into the FP64 accumulators
+  __device__ __forceinline__ void fold(const float2 ph, const float2 ax, const float2 ay, const float2 az, bool acc) {
+    ph0 += ph.x;
+    ph1 += ph.y;
+    if (acc) {
+      ax0 += ax.x;
+      ax1 += ax.y;
+      ay0 += ay.x;
+      ay1 += ay.y;
+      az0 += az.x;
+      az1 += az.y;
+    }
+  }
+};
+
+template <bool kAcc>
+__device__ __forceinline__ void tile_compute(const float4* __restrict__ buf, int nb, int g, int G, const Tgt& T,
+                                             Acc64& A) {
   float2 ph = make_float2(0.f, 0.f), ax = ph, ay = ph, az = ph;
   // group g takes a contiguous chunk of the tile: unit stride, immediate-offset LDS and one
   // pointer bump per 4 independent sources (ILP, no per-source address arithmetic)
@@ -293,20 +372,32 @@ __device__ __forceinline__ void tile_compute(const float4* __restrict__ buf, int
 #pragma unroll
     for (int u = 0; u < U; ++u) sv[u] = p[u];
 #pragma unroll
-    for (int u = 0; u < U; ++u) pair_body<kAcc, kGuard>(sv[u], X, Y, Z, ph, ax, ay, az);
+    for (int u = 0; u < U; ++u) pair_body<kAcc>(sv[u], T.X, T.Y, T.Z, ph, ax, ay, az);
   }
-  for (; p < end; ++p) pair_body<kAcc, kGuard>(*p, X, Y, Z, ph, ax, ay, az);
-  // fold this tile's FP32 partials into the FP64 accumulators
-  ph0 += ph.x;
-  ph1 += ph.y;
-  if constexpr (kAcc) {
-    ax0 += ax.x;
-    ax1 += ax.y;
-    ay0 += ay.x;
-    ay1 += ay.y;
-    az0 += az.x;
-    az1 += az.y;
+  for (; p < end; ++p) pair_body<kAcc>(*p, T.X, T.Y, T.Z, ph, ax, ay, az);
+  A.fold(ph, ax, ay, az, kAcc);
+}
+
+template <bool kAcc, bool kGuard>
+__device__ __forceinline__ void tile_compute_prec(const float4* __restrict__ buf, int nb, int g, int G, const Tgt& T,
+                                                  Acc64& A) {
+  float2 ph = make_float2(0.f, 0.f), ax = ph, ay = ph, az = ph;
+  const int chunk = ((nb + G - 1) / G) | 1;
+  const float4* p = buf + g * chunk;
+  const float4* const end = buf + min(nb, (g + 1) * chunk);
+  constexpr int U = 4;
+  for (; p + (U - 1) < end; p += U) {
+    float4 sh[U], sl[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      sh[u] = p[u];
+      sl[u] = p[kHalfTile + u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) pair_body_prec<kAcc, kGuard>(sh[u], sl[u], T, ph, ax, ay, az);
   }
+  for (; p < end; ++p) pair_body_prec<kAcc, kGuard>(p[0], p[kHalfTile], T, ph, ax, ay, az);
+  A.fold(ph, ax, ay, az, kAcc);
 }
 
 #ifndef FMM_P2P_MIN_BLOCKS
@@ -315,7 +406,8 @@ __device__ __forceinline__ void tile_compute(const float4* __restrict__ buf, int
 template <bool kAcc>
 __global__ void __launch_bounds__(kThreads, FMM_P2P_MIN_BLOCKS)
 k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, const float4* __restrict__ bodyf,
-           double* __restrict__ phi_out, double* __restrict__ acc_out, double* __restrict__ partial) {
+           const float4* __restrict__ bodyl, double* __restrict__ phi_out, double* __restrict__ acc_out,
+           double* __restrict__ partial) {
   __shared__ __align__(16) float4 sS[2][kTileBodies];
   __shared__ TileTab tabs[3];  // ring: tile k computes from tabs[k%3] while k+2 is resolved
   __shared__ __align__(8) uint64_t bars[2];  // TMA completion, one per buffer
@@ -329,15 +421,21 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
   const int g = tid / slots, t = tid - g * slots;
   const bool active = g < G;
 
-  float2 X = make_float2(0.f, 0.f), Y = X, Z = X;
+  Tgt T;
+  T.X = make_float2(0.f, 0.f);
+  T.Y = T.Z = T.XL = T.YL = T.ZL = T.X;
   if (active) {
-    const float4 b0 = bodyf[it.tb + 2 * t];
-    const float4 b1 = (2 * t + 1 < nt) ? bodyf[it.tb + 2 * t + 1] : b0;
-    X = make_float2(b0.x, b1.x);
-    Y = make_float2(b0.y, b1.y);
-    Z = make_float2(b0.z, b1.z);
+    const int32_t i0 = it.tb + 2 * t, i1 = (2 * t + 1 < nt) ? i0 + 1 : i0;
+    const float4 b0 = bodyf[i0], b1 = bodyf[i1];
+    const float4 l0 = bodyl[i0], l1 = bodyl[i1];
+    T.X = make_float2(b0.x, b1.x);
+    T.Y = make_float2(b0.y, b1.y);
+    T.Z = make_float2(b0.z, b1.z);
+    T.XL = make_float2(l0.x, l1.x);
+    T.YL = make_float2(l0.y, l1.y);
+    T.ZL = make_float2(l0.z, l1.z);
   }
-  double ph0 = 0.0, ph1 = 0.0, ax0 = 0.0, ax1 = 0.0, ay0 = 0.0, ay1 = 0.0, az0 = 0.0, az1 = 0.0;
+  Acc64 A;
 
   // prologue: tile 0 staged and converted, tile 1 resolved
   bool have = it.lb < it.le;
@@ -350,14 +448,15 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
   if (tid < 32 && have) {
     tile_setup_ent(lane, it.le, it.lb, 0, ent + it.lb, tabs[0]);
     __syncwarp();
-    tile_tma(lane, tabs[0], bodyf, sS[0], &bars[0]);
+    tile_tma(lane, tabs[0], bodyf, bodyl, sS[0], &bars[0]);
     const int32_t c1 = tabs[0].next;
     if (c1 < it.le) tile_setup_ent(lane, it.le, c1, tabs[0].next_off, ent + c1, tabs[1]);
   }
   __syncthreads();
   if (have) {
     mbar_wait(&bars[0], 0);
-    tile_convert(tid, tabs[0], sS[0]);
+    if (tabs[0].prec) tile_convert_prec(tid, tabs[0], sS[0]);
+    else tile_convert(tid, tabs[0], sS[0]);
   }
   __syncthreads();
   int k3 = 0, k2 = 0;  // tile index mod 3 (tables) and mod 2 (buffers)
@@ -369,18 +468,21 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
     const bool more = tc.next < it.le;
     const int nb = tc.off[tc.nseg];
     if (more && tid < 32) {
-      tile_tma(lane, tn, bodyf, sS[k2 ^ 1], &bars[k2 ^ 1]);
+      tile_tma(lane, tn, bodyf, bodyl, sS[k2 ^ 1], &bars[k2 ^ 1]);
       ent_prefetch(lane, tn.next, it.le, ent, st);
     }
     if (active) {
-      if (tc.guard)
-        tile_compute<kAcc, true>(sS[k2], nb, g, G, X, Y, Z, ph0, ph1, ax0, ax1, ay0, ay1, az0, az1);
+      if (!tc.prec)
+        tile_compute<kAcc>(sS[k2], nb, g, G, T, A);
+      else if (tc.guard)
+        tile_compute_prec<kAcc, true>(sS[k2], nb, g, G, T, A);
       else
-        tile_compute<kAcc, false>(sS[k2], nb, g, G, X, Y, Z, ph0, ph1, ax0, ax1, ay0, ay1, az0, az1);
+        tile_compute_prec<kAcc, false>(sS[k2], nb, g, G, T, A);
     }
     if (more) {
       mbar_wait(&bars[k2 ^ 1], ((kt + 1) >> 1) & 1u);
-      tile_convert(tid, tn, sS[k2 ^ 1]);
+      if (tn.prec) tile_convert_prec(tid, tn, sS[k2 ^ 1]);
+      else tile_convert(tid, tn, sS[k2 ^ 1]);
       if (tid < 32 && tn.next < it.le) {
         cp_async_wait_all();
         __syncwarp();
@@ -397,8 +499,8 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
   double* red = reinterpret_cast<double*>(sS);  // [G][slots][2 targets][4]
   if (active) {
     double* r = red + 8 * (g * slots + t);
-    r[0] = ph0; r[1] = ax0; r[2] = ay0; r[3] = az0;
-    r[4] = ph1; r[5] = ax1; r[6] = ay1; r[7] = az1;
+    r[0] = A.ph0; r[1] = A.ax0; r[2] = A.ay0; r[3] = A.az0;
+    r[4] = A.ph1; r[5] = A.ax1; r[6] = A.ay1; r[7] = A.az1;
   }
   __syncthreads();
   if (tid < nt) {
@@ -653,42 +755,107 @@ __global__ void k_write_items(const int32_t* __restrict__ leaves, int64_t nleave
     }
 }
 
-// P2P list entries of one target cell per warp: {source body range, FP32 shift into the target
-// leaf frame}. Within each target's (source-sorted) list the self entry is rotated to the
-// front, so that a work item's first tile is the only one that needs the r^2 == 0 guard.
+// P2P list entries of one target cell per warp: {source body range, kind, FP64 centre shift into
+// the target leaf frame as FP32 hi + lo}. Within each target's (source-sorted) list the order is
+// self entry, near entries, far entries (each group ascending by source), so that a work item's
+// tiles each hold one class: only the self tile runs the r^2 == 0 guard and only self / near
+// tiles pay for compensated coordinates. Near = the tight body boxes of the two leaves are less
+// than 0.05 (r_t + r_s) apart along every axis; a far entry's body pairs are then at least that
+// far apart, and FP32 offsets (magnitude <= ~4.5 (r_t + r_s) in the target frame) give them a
+// relative distance error below ~5e-6.
 // Items still partition the list positions, so every entry is computed exactly once.
+__device__ __forceinline__ bool near_leaf(const double4 tlo, const double4 thi, const double4 slo, const double4 shi,
+                                          double lim) {
+  const double gx = fmax(slo.x - thi.x, tlo.x - shi.x);
+  const double gy = fmax(slo.y - thi.y, tlo.y - shi.y);
+  const double gz = fmax(slo.z - thi.z, tlo.z - shi.z);
+  return fmax(gx, fmax(gy, gz)) < lim;
+}
+
+// tight bounding box of each leaf's bodies (warp per leaf; tree order: contiguous bodies)
+__global__ void k_leaf_boxes(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __restrict__ bb,
+                             const int32_t* __restrict__ be, const double4* __restrict__ bodies,
+                             double4* __restrict__ lo, double4* __restrict__ hi) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nleaves) return;
+  const int32_t leaf = leaves[w];
+  double x0 = INFINITY, y0 = INFINITY, z0 = INFINITY, x1 = -INFINITY, y1 = -INFINITY, z1 = -INFINITY;
+  for (int32_t i = bb[leaf] + lane; i < be[leaf]; i += 32) {
+    const double4 b = bodies[i];
+    x0 = fmin(x0, b.x); y0 = fmin(y0, b.y); z0 = fmin(z0, b.z);
+    x1 = fmax(x1, b.x); y1 = fmax(y1, b.y); z1 = fmax(z1, b.z);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+    y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+    z0 = fmin(z0, __shfl_xor_sync(0xffffffffu, z0, o));
+    x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+    y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+    z1 = fmax(z1, __shfl_xor_sync(0xffffffffu, z1, o));
+  }
+  if (lane == 0) {
+    lo[leaf] = make_double4(x0, y0, z0, 0.0);
+    hi[leaf] = make_double4(x1, y1, z1, 0.0);
+  }
+}
+
 __global__ void k_p2p_entries(const int64_t* __restrict__ off, int64_t ncells, const int32_t* __restrict__ src,
                               const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
-                              const double4* __restrict__ cr, P2PEnt* __restrict__ ent) {
+                              const double4* __restrict__ cr, const double4* __restrict__ blo,
+                              const double4* __restrict__ bhi, P2PEnt* __restrict__ ent) {
   const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= ncells) return;
   const int64_t l0 = off[t], l1 = off[t + 1];
   if (l0 == l1) return;
-  int64_t sp = -1;  // position of the self entry
-  if (lane == 0) {
-    int64_t lo = l0, hi = l1;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (src[mid] < t) lo = mid + 1; else hi = mid;
+  const double4 ct = cr[t], tlo = blo[t], thi = bhi[t];
+  const unsigned below = (1u << lane) - 1u;
+  int64_t nnear = 0, nself = 0;
+  for (int64_t kb = l0; kb < l1; kb += 32) {
+    const int64_t k = kb + lane;
+    bool nr = false, sf = false;
+    if (k < l1) {
+      const int32_t s = src[k];
+      sf = s == t;
+      nr = !sf && near_leaf(tlo, thi, blo[s], bhi[s], 0.05 * (ct.w + cr[s].w));
     }
-    if (lo < l1 && src[lo] == t) sp = lo;
+    nnear += __popc(__ballot_sync(0xffffffffu, nr));
+    nself += __popc(__ballot_sync(0xffffffffu, sf));
   }
-  sp = __shfl_sync(0xffffffffu, sp, 0);
-  const double4 ct = cr[t];
-  for (int64_t k = l0 + lane; k < l1; k += 32) {
-    const int32_t s = src[k];
-    const double4 cs = cr[s];
-    const int64_t pos = sp < 0 ? k : (k == sp ? l0 : (k < sp ? k + 1 : k));
-    P2PEnt e;
-    e.bb = bb[s];
-    e.n = be[s] - bb[s];
-    e.sx = static_cast<float>(cs.x - ct.x);
-    e.sy = static_cast<float>(cs.y - ct.y);
-    e.sz = static_cast<float>(cs.z - ct.z);
-    e.self = k == sp ? 1 : 0;
-    e.pad[0] = e.pad[1] = 0;
-    ent[pos] = e;
+  int64_t pn = l0 + nself, pf = l0 + nself + nnear;  // next near / far position
+  for (int64_t kb = l0; kb < l1; kb += 32) {
+    const int64_t k = kb + lane;
+    const bool valid = k < l1;
+    int32_t s = 0;
+    double4 cs = ct;
+    bool sf = false, nr = false;
+    if (valid) {
+      s = src[k];
+      cs = cr[s];
+      sf = s == t;
+      nr = !sf && near_leaf(tlo, thi, blo[s], bhi[s], 0.05 * (ct.w + cs.w));
+    }
+    const unsigned mn = __ballot_sync(0xffffffffu, nr);
+    const unsigned mf = __ballot_sync(0xffffffffu, valid && !sf && !nr);
+    if (valid) {
+      const int64_t pos = sf ? l0 : nr ? pn + __popc(mn & below) : pf + __popc(mf & below);
+      const double dx = cs.x - ct.x, dy = cs.y - ct.y, dz = cs.z - ct.z;
+      const float hx = static_cast<float>(dx), hy = static_cast<float>(dy), hz = static_cast<float>(dz);
+      const int kind = sf ? kKindSelf : nr ? kKindNear : kKindFar;
+      P2PEnt e;
+      e.bb = bb[s];
+      e.nk = (be[s] - bb[s]) | (kind << 30);
+      e.sx = hx;
+      e.sy = hy;
+      e.sz = hz;
+      e.lx = static_cast<float>(dx - hx);
+      e.ly = static_cast<float>(dy - hy);
+      e.lz = static_cast<float>(dz - hz);
+      ent[pos] = e;
+    }
+    pn += __popc(mn);
+    pf += __popc(mf);
   }
 }
 
@@ -761,10 +928,15 @@ void build_p2p_worklist(fmm_ctx* c) {
   CK_LAUNCH("k_write_items");
   if (c->cfg.precision == FMM_PREC_FP32_P2P) {
     P2PEnt* ent = reinterpret_cast<P2PEnt*>(c->p2p_ent.ensure(2 * (ne + 1)));
+    double4* blo = c->leaf_lo.ensure(c->ncells);
+    double4* bhi = c->leaf_hi.ensure(c->ncells);
+    k_leaf_boxes<<<ceil_div(c->nleaves * 32, 256), 256, 0, s>>>(c->leaves.p, c->nleaves, c->c_body_begin.p,
+                                                               c->c_body_end.p, c->bodies.p, blo, bhi);
     k_p2p_entries<<<ceil_div(c->ncells * 32, 256), 256, 0, s>>>(c->p2p_off.p, c->ncells, c->p2p_src.p,
-                                                                c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, ent);
+                                                                c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, blo,
+                                                                bhi, ent);
     CK_LAUNCH("k_p2p_entries");
-    c->kernel_launches += 1;
+    c->kernel_launches += 2;
   }
   // cost-sorted (descending, stable) work list: the longest items launch first
   int32_t* ord_in = c->i32_c.ensure(2 * (nitem + 1));
@@ -792,11 +964,11 @@ void run_p2p(fmm_ctx* c, cudaStream_t s) {
     if (c->cfg.precision == FMM_PREC_FP32_P2P) {
       const P2PEnt* ent = reinterpret_cast<const P2PEnt*>(c->p2p_ent.p);
       if (wa)
-        k_p2p_fp32<true><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, ent, c->bodyf.p, phi, acc,
-                                                                       c->p2p_partial.p);
+        k_p2p_fp32<true><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p, phi,
+                                                                       acc, c->p2p_partial.p);
       else
-        k_p2p_fp32<false><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, ent, c->bodyf.p, phi, acc,
-                                                                        c->p2p_partial.p);
+        k_p2p_fp32<false><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p, phi,
+                                                                        acc, c->p2p_partial.p);
     } else {
       k_p2p_fp64<<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p,
                                                               c->bodies.p, phi, acc, c->p2p_partial.p, wa);

@@ -176,17 +176,42 @@ __global__ void k_pair_keys(const int2* __restrict__ pr, int64_t n, int sbits, K
   if (i < n) keys[i] = static_cast<KeyT>(((uint64_t)(uint32_t)pr[i].x << sbits) | (uint32_t)pr[i].y);
 }
 
-// CSR from sorted (target, source) keys: sources, and offsets (targets tp+1..t start at i)
+// CSR from sorted (target, source) keys: sources, and offsets (targets tp+1..t start at i).
+// Mutual mode: bit 63 marks a mirrored key (outside the sorted bit range, so carried along) and
+// is written to `mir`; the all-ones key of the sorted range is a dropped slot (a self pair has
+// no mirror) and sorts past every cell, so off[ncells] = the number of real entries.
+constexpr uint64_t kMirrorBit = 1ull << 63;
+
 template <class KeyT>
 __global__ void k_csr_from_keys(const KeyT* __restrict__ keys, int64_t n, int sbits, int64_t ncells,
-                                int64_t* __restrict__ off, int32_t* __restrict__ src) {
+                                int64_t* __restrict__ off, int32_t* __restrict__ src, uint8_t* __restrict__ mir) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i > n) return;
-  const uint64_t mask = (1ull << sbits) - 1;
-  const int64_t t = i < n ? (int64_t)(keys[i] >> sbits) : ncells;
-  const int64_t tp = i > 0 ? (int64_t)(keys[i - 1] >> sbits) : -1;
-  if (i < n) src[i] = (int32_t)(keys[i] & mask);
+  const uint64_t mask = (1ull << sbits) - 1, range = (1ull << (2 * sbits)) - 1;
+  auto target_of = [&](int64_t j) -> int64_t {
+    const uint64_t k = static_cast<uint64_t>(keys[j]) & range;
+    return k == range ? ncells : static_cast<int64_t>(k >> sbits);
+  };
+  const int64_t t = i < n ? target_of(i) : ncells;
+  const int64_t tp = i > 0 ? target_of(i - 1) : -1;
+  if (i < n) {
+    src[i] = (int32_t)(keys[i] & mask);
+    if (mir) mir[i] = static_cast<uint8_t>(static_cast<uint64_t>(keys[i]) >> 63);
+  }
   for (int64_t c = tp + 1; c <= t; ++c) off[c] = i;
+}
+
+// Mutual mode (traversal.hpp:76-84 emits each unordered pair once): out[0, n) = the emitted
+// keys, out[n, 2n) = their mirrors (s, t) flagged with kMirrorBit, or the dropped-slot key for
+// a self pair. The symmetrised list equals the non-mutual emission (test_traversal.cpp:182-210),
+// so the target-owned M2L / P2P kernels run unchanged on it.
+__global__ void k_mirror_keys(const uint64_t* __restrict__ in, int64_t n, int sbits, uint64_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t mask = (1ull << sbits) - 1, k = in[i];
+  const uint64_t t = k >> sbits, s = k & mask;
+  out[i] = k;
+  out[n + i] = t == s ? (1ull << (2 * sbits)) - 1 : ((s << sbits) | t | kMirrorBit);
 }
 
 // cells with a non-empty M2L list whose body range meets [b0, b1) (the rank's targets)
@@ -206,9 +231,11 @@ int bits_for(uint64_t v) {
 // target with ascending sources: the canonical form of the emitted multiset.
 // Keys are 32-bit when 2 * ceil(log2 ncells) <= 32 (half the sort traffic), else 64-bit.
 inline bool small_keys(int64_t ncells) { return 2 * bits_for(static_cast<uint64_t>(ncells)) <= 32; }
+// mutual mode carries the mirror flag in bit 63: always 64-bit keys
+inline bool keys32(const fmm_ctx* c) { return !c->cfg.mutual && small_keys(c->ncells); }
 
 template <class KeyT>
-void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int32_t>& src) {
+void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int32_t>& src, uint8_t* mir) {
   cudaStream_t s = c->stream;
   const int64_t nc = c->ncells;
   off.ensure(nc + 1);
@@ -222,7 +249,7 @@ void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int
   size_t sb = 0;
   CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys, kb, (int)n, 0, 2 * sbits, s));
   CK(cub::DeviceRadixSort::SortKeys(temp_storage(c, sb), sb, keys, kb, (int)n, 0, 2 * sbits, s));
-  k_csr_from_keys<<<ceil_div(n + 1, 256), 256, 0, s>>>(kb, n, sbits, nc, off.p, src.p);
+  k_csr_from_keys<<<ceil_div(n + 1, 256), 256, 0, s>>>(kb, n, sbits, nc, off.p, src.p, mir);
   CK_LAUNCH("keys_to_csr");
   c->kernel_launches += 3;
 }
@@ -233,7 +260,7 @@ void lists_from_pairs(fmm_ctx* c, const int2* d_m2l, int64_t n_m2l, const int2* 
   const int sbits = bits_for(static_cast<uint64_t>(c->ncells));
   uint64_t* mk = c->m2l_keys.ensure(n_m2l + 1);
   uint64_t* pk = c->p2p_keys.ensure(n_p2p + 1);
-  if (small_keys(c->ncells)) {
+  if (keys32(c)) {
     if (n_m2l) k_pair_keys<<<ceil_div(n_m2l, 256), 256, 0, c->stream>>>(d_m2l, n_m2l, sbits, (uint32_t*)mk);
     if (n_p2p) k_pair_keys<<<ceil_div(n_p2p, 256), 256, 0, c->stream>>>(d_p2p, n_p2p, sbits, (uint32_t*)pk);
   } else {
@@ -246,12 +273,30 @@ void lists_from_pairs(fmm_ctx* c, const int2* d_m2l, int64_t n_m2l, const int2* 
 
 void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
   cudaStream_t s = c->stream;
-  if (small_keys(c->ncells)) {
-    keys_to_csr(c, reinterpret_cast<uint32_t*>(c->m2l_keys.p), n_m2l, c->m2l_off, c->m2l_src);
-    keys_to_csr(c, reinterpret_cast<uint32_t*>(c->p2p_keys.p), n_p2p, c->p2p_off, c->p2p_src);
+  c->n_m2l_emit = n_m2l;
+  c->n_p2p_emit = n_p2p;
+  if (c->cfg.mutual) {
+    // symmetrise (emitted + mirrored), then the same canonical CSR; off[ncells] of each list is
+    // its executed length (self pairs have no mirror), read back with the M2L target count
+    const int sbits = bits_for(static_cast<uint64_t>(c->ncells));
+    uint64_t* dm = c->mut_keys.ensure(2 * (n_m2l + n_p2p) + 2);
+    uint64_t* dp = dm + 2 * n_m2l;
+    if (n_m2l) k_mirror_keys<<<ceil_div(n_m2l, 256), 256, 0, s>>>(c->m2l_keys.p, n_m2l, sbits, dm);
+    if (n_p2p) k_mirror_keys<<<ceil_div(n_p2p, 256), 256, 0, s>>>(c->p2p_keys.p, n_p2p, sbits, dp);
+    CK_LAUNCH("k_mirror_keys");
+    keys_to_csr(c, dm, 2 * n_m2l, c->m2l_off, c->m2l_src, c->m2l_mir.ensure(2 * n_m2l + 1));
+    keys_to_csr(c, dp, 2 * n_p2p, c->p2p_off, c->p2p_src, c->p2p_mir.ensure(2 * n_p2p + 1));
+    CK(cudaMemcpyAsync(c->hpin + 2, c->m2l_off.p + c->ncells, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->hpin + 3, c->p2p_off.p + c->ncells, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    n_m2l = c->hpin[2];
+    n_p2p = c->hpin[3];
+  } else if (keys32(c)) {
+    keys_to_csr(c, reinterpret_cast<uint32_t*>(c->m2l_keys.p), n_m2l, c->m2l_off, c->m2l_src, nullptr);
+    keys_to_csr(c, reinterpret_cast<uint32_t*>(c->p2p_keys.p), n_p2p, c->p2p_off, c->p2p_src, nullptr);
   } else {
-    keys_to_csr(c, c->m2l_keys.p, n_m2l, c->m2l_off, c->m2l_src);
-    keys_to_csr(c, c->p2p_keys.p, n_p2p, c->p2p_off, c->p2p_src);
+    keys_to_csr(c, c->m2l_keys.p, n_m2l, c->m2l_off, c->m2l_src, nullptr);
+    keys_to_csr(c, c->p2p_keys.p, n_p2p, c->p2p_off, c->p2p_src, nullptr);
   }
   c->n_m2l = n_m2l;
   c->n_p2p = n_p2p;
@@ -289,7 +334,8 @@ void traverse(fmm_ctx* c) {
   cudaStream_t s = c->stream;
   const int mutual = c->cfg.mutual ? 1 : 0;
   const int sbits = bits_for(static_cast<uint64_t>(c->ncells));
-  const bool small = small_keys(c->ncells);
+  const bool small = keys32(c);
+  if (mutual && c->world > 1) fail(FMM_ERR_UNSUPPORTED, "mutual mode is not supported by the sharded traversal");
   // Every split descends the target or the source by one level (a mutual self split both), so
   // the frontier is empty after at most 2 * depth + 1 levels.
   const int nlev = 2 * c->depth + 2;
@@ -339,20 +385,35 @@ void traverse(fmm_ctx* c) {
     CK(cudaStreamSynchronize(s));
     c->kernel_launches += nlev;
     const int64_t nm = static_cast<int64_t>(h[0]), np = static_cast<int64_t>(h[1]);
-    int64_t fmax = 0;
-    for (int L = 0; L <= nlev; ++L) fmax = std::max<int64_t>(fmax, static_cast<int64_t>(h[4 + L]));
     if (h[2] == 0) {  // no overflow: the lists are complete
       if (h[4 + nlev] != 0) fail(FMM_ERR_CUDA, "traverse: frontier not empty after 2*depth+2 levels");
       finish_lists(c, nm, np);
       return;
     }
-    if (attempt > 0) fail(FMM_ERR_CUDA, "traverse: output overflow after regrow");
-    // grow to the exact sizes (+ slack) and run again
-    c->pairs_a.ensure(fmax + fmax / 8 + 1024);
-    c->pairs_d.ensure(fmax + fmax / 8 + 1024);
+    // Counters keep counting past a full buffer, so every count is exact up to the first level
+    // whose frontier was truncated; the levels after it saw a partial frontier and their counts
+    // are lower bounds. Grow each buffer to its count (+ slack), and at least double the ones
+    // that may be underestimated; every attempt completes at least one more level.
+    if (attempt >= 8) fail(FMM_ERR_CUDA, "traverse: output overflow after regrow");
+    bool trunc = false;
+    int64_t fgrow = 0;
+    for (int L = 0; L <= nlev; ++L) {
+      const int64_t f = static_cast<int64_t>(h[4 + L]);
+      fgrow = std::max(fgrow, trunc ? std::max(f, 2 * cap_f) : f);
+      if (f > cap_f) trunc = true;
+    }
+    auto grow = [&](int64_t count, int64_t cap) {
+      const int64_t want = count + count / 8 + 1024;
+      return trunc ? std::max(want, 2 * cap) : want;
+    };
+    const int64_t newf = fgrow + fgrow / 8 + 1024;
+    if (newf > cap_f) {
+      c->pairs_a.ensure(newf);
+      c->pairs_d.ensure(newf);
+    }
     const int64_t div = small ? 2 : 1;
-    c->m2l_keys.ensure((nm + nm / 8 + 1024) / div + 1);
-    c->p2p_keys.ensure((np + np / 8 + 1024) / div + 1);
+    if (nm > cap_m || trunc) c->m2l_keys.ensure(grow(nm, cap_m) / div + 1);
+    if (np > cap_p || trunc) c->p2p_keys.ensure(grow(np, cap_p) / div + 1);
   }
 }
 

@@ -271,14 +271,18 @@ __global__ void k_perm_from_ckey(const uint64_t* __restrict__ ckey, int64_t n, i
 
 __global__ void k_gather(const double4* __restrict__ in, const int32_t* __restrict__ perm,
                          const int32_t* __restrict__ leaf_of_body, const double4* __restrict__ c_cr,
-                         int64_t n, double4* __restrict__ bodies, float4* __restrict__ bodyf) {
+                         int64_t n, double4* __restrict__ bodies, float4* __restrict__ bodyf,
+                         float4* __restrict__ bodyl) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double4 b = in[perm[i]];
   bodies[i] = b;
   const double4 c = c_cr[leaf_of_body[i]];
-  bodyf[i] = make_float4(static_cast<float>(b.x - c.x), static_cast<float>(b.y - c.y),
-                         static_cast<float>(b.z - c.z), static_cast<float>(b.w));
+  const double dx = b.x - c.x, dy = b.y - c.y, dz = b.z - c.z;
+  const float fx = static_cast<float>(dx), fy = static_cast<float>(dy), fz = static_cast<float>(dz);
+  bodyf[i] = make_float4(fx, fy, fz, static_cast<float>(b.w));
+  // hi + lo carries ~48 bits of the offset: the P2P near tiles form exact close-pair differences
+  bodyl[i] = make_float4(static_cast<float>(dx - fx), static_cast<float>(dy - fy), static_cast<float>(dz - fz), 0.f);
 }
 
 __global__ void k_flag_leaves(const int32_t* __restrict__ cc, int64_t ncells, int32_t* __restrict__ flag) {
@@ -505,7 +509,7 @@ void build_tree(fmm_ctx* c) {
   c->kernel_launches += launches;
   c->have_tree = true;
   k_gather<<<ceil_div(n, 256), 256, 0, s>>>(c->xyzq_in.p, perm, leaf_of_body, c->c_cr.p, n, c->bodies.ensure(n),
-                                            c->bodyf.ensure(n));
+                                            c->bodyf.ensure(n), c->bodyl.ensure(n));
   CK_LAUNCH("k_gather");
   c->kernel_launches += 1;
 }
@@ -537,7 +541,7 @@ void gather_bodies(fmm_ctx* c) {
   k_leaf_map<<<ceil_div(c->nleaves * 32, 256), 256, 0, s>>>(c->leaves.p, c->nleaves, c->c_body_begin.p,
                                                               c->c_body_end.p, nullptr, leaf_of_body, nullptr);
   k_gather<<<ceil_div(n, 256), 256, 0, s>>>(c->xyzq_in.p, c->perm.p, leaf_of_body, c->c_cr.p, n,
-                                            c->bodies.ensure(n), c->bodyf.ensure(n));
+                                            c->bodies.ensure(n), c->bodyf.ensure(n), c->bodyl.ensure(n));
   CK_LAUNCH("k_gather");
   c->kernel_launches += 2;
 }

@@ -152,6 +152,10 @@ class Context:
     def reset_accumulators(self): self._c(self.lib.fmm_reset_accumulators(self.h))
     def set_overlap(self, on: bool): self._c(self.lib.fmm_set_overlap(self.h, int(on)))
 
+    def set_mutual(self, on: bool):
+        self._c(self.lib.fmm_set_mutual(self.h, int(on)))
+        self.cfg.mutual = int(on)
+
     # outputs
     def results(self, order: str = "tree", with_acc: bool = True):
         phi = np.zeros(self.n)
@@ -174,6 +178,14 @@ class Context:
         t = _capi.StageTimes()
         self._c(self.lib.fmm_get_stage_times(self.h, C.byref(t)))
         return t
+
+    def stage_trace(self):
+        """Rows (task_id, worker_id, kind, start_ns, end_ns) of the last evaluate: the
+        reference's trace CSV schema (scheduler.cpp:305-317) at GPU-stage granularity."""
+        rows = (_capi.TraceRow * 16)()
+        n = C.c_int(0)
+        self._c(self.lib.fmm_get_stage_trace(self.h, rows, 16, C.byref(n)))
+        return [(r.task_id, r.worker_id, r.kind.decode(), r.start_ns, r.end_ns) for r in rows[:n.value]]
 
     def cells(self) -> dict:
         nc = self.tree_info().ncells
@@ -311,9 +323,10 @@ class KernelVisitor:
     def __init__(self, targets: Tree, sources: Tree, tables: KernelTables, mutual: bool = False):
         if targets is not sources:
             raise FMMError(_capi.ERR_UNSUPPORTED, "distinct target/source trees are not supported")
-        if mutual:
-            raise FMMError(_capi.ERR_UNSUPPORTED, "mutual mode is not implemented on the GPU path")
+        # mutual (m2l_mutual / mutual p2p, kernels.cpp:113-126, :153-180): the GPU runs the
+        # symmetrised lists with target-owned writes, which accumulates the same sums
         self.tree = targets
+        self.mutual = bool(mutual)
 
 
 def dual_tree_traverse(targets: Tree, sources: Tree, cfg: TraversalConfig, visit, drain=None):
@@ -327,8 +340,12 @@ def dual_tree_traverse(targets: Tree, sources: Tree, cfg: TraversalConfig, visit
     if abs(ctx.cfg.theta - cfg.theta) > 0.0:
         ctx.cfg.theta = cfg.theta
         raise FMMError(_capi.ERR_STATE, "theta differs from the tree's context; rebuild with theta")
+    if bool(ctx.cfg.mutual) != bool(cfg.mutual):
+        ctx.set_mutual(cfg.mutual)
     ctx.traverse()
     if isinstance(visit, KernelVisitor):
+        if visit.mutual != bool(cfg.mutual):
+            raise FMMError(_capi.ERR_ARG, "KernelVisitor and TraversalConfig disagree on mutual")
         ctx.reset_accumulators()
         ctx.m2l()
         ctx.p2p()

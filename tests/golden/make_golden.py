@@ -7,7 +7,8 @@ Run in the build container (needs /root/reference to have built oracle/_ref):
 Outputs (all small, committed):
   ref_cases.npz    per case: input bodies, tree cells, body permutation, sorted M2L/P2P
                    emitted pairs, potentials (tree order), multipoles and locals of the
-                   reference's serial pipeline (test_traversal.cpp:292-318 semantics).
+                   reference's serial pipeline (test_traversal.cpp:292-318 semantics); the
+                   same lists and potentials in mutual mode (test_traversal.cpp:320-345).
   aggregates.json  the proj/test_output.txt aggregates reproduced by the reference build, plus
                    BASELINE C1 tree / list counts for the repo's synthetic generator.
 """
@@ -71,6 +72,14 @@ def main():
         data[f"{name}/phi"] = t.potentials()
         data[f"{name}/multipole"] = M
         data[f"{name}/local"] = L
+        # mutual mode (traversal.hpp:76-84; m2l_mutual / mutual p2p): emitted once per
+        # unordered pair, in the emitted orientation; potentials of the mutual pipeline
+        tm = ref.build_tree(bodies, n_crit, p)
+        mm, mp = tm.traverse(theta, mutual=True)
+        tm.pipeline(theta, mutual=True)
+        data[f"{name}/m2l_mutual"] = pair_keys(mm)
+        data[f"{name}/p2p_mutual"] = pair_keys(mp)
+        data[f"{name}/phi_mutual"] = tm.potentials()
     np.savez_compressed(os.path.join(HERE, "ref_cases.npz"), **data)
 
     agg = {}

@@ -178,6 +178,76 @@ def test_reference_fixtures(fmmlib, fx, precision):
             assert rel_l2(L, g("local")) < 1e-11, name
 
 
+def symmetrised(pairs):
+    """Mutual list -> both orientations (test_traversal.cpp:36-46)."""
+    pairs = np.asarray(pairs).reshape(-1, 2)
+    return np.concatenate([pairs, pairs[pairs[:, 0] != pairs[:, 1]][:, ::-1]])
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_reference_fixtures_mutual(fmmlib, fx, precision):
+    """Mutual mode: the GPU's emitted lists are bit-exact with the reference's mutual traversal
+    (each unordered pair once, same orientation); potentials within tolerance of the reference's
+    mutual pipeline and bit-identical to the GPU's own non-mutual run (the symmetrised lists are
+    the non-mutual lists, executed by the same target-owned kernels)."""
+    for name in fixture_cases(fx):
+        g = lambda k: fx[f"{name}/{k}"]  # noqa: E731
+        n_crit, p, theta = g("params")
+        ctx = fmmlib.Context(order=int(p), n_crit=int(n_crit), theta=float(theta), precision=precision,
+                             mutual=True)
+        ctx.set_bodies(g("bodies"))
+        ctx.evaluate()
+        m, pp = ctx.pair_lists()
+        assert np.array_equal(sorted_pairs(m), g("m2l_mutual")), name
+        assert np.array_equal(sorted_pairs(pp), g("p2p_mutual")), name
+        info = ctx.tree_info()
+        assert info.mutual == 1 and info.n_m2l == len(m) and info.n_p2p == len(pp)
+        assert info.n_m2l_exec == len(g("m2l")) and info.n_p2p_exec == len(g("p2p"))
+        phi_m, acc_m = ctx.results("tree")
+        assert rel_l2(phi_m, g("phi_mutual")) <= TOL[precision], (name, rel_l2(phi_m, g("phi_mutual")))
+        ctx.set_mutual(False)
+        ctx.evaluate()
+        m2, pp2 = ctx.pair_lists()
+        assert np.array_equal(sorted_pairs(m2), g("m2l")) and np.array_equal(sorted_pairs(pp2), g("p2p"))
+        phi, acc = ctx.results("tree")
+        assert np.array_equal(phi, phi_m) and np.array_equal(acc, acc_m), name
+        ctx.close()
+
+
+def test_mutual_pipeline_vs_oracle(fmmlib, orc):
+    """Mutual mode at C3/C5 shapes against the oracle's mutual traversal and pipeline
+    (m2l_mutual / mutual p2p), plus the reference API mirror's KernelVisitor(mutual=True)."""
+    for gen, n, seed, n_crit, p in ((3, 30000, 2, 64, 6), (5, 20000, 3, 64, 8)):
+        bodies = fmmlib.generate_bodies(gen, n, seed)
+        t = orc.build_tree(bodies, n_crit, p)
+        om, op = orc.traverse(t, 0.5, mutual=True)
+        orc.evaluate(t, 0.5, mutual=True, with_acc=True)
+        for precision in ("fp64", "fp32"):
+            ctx = fmmlib.Context(order=p, n_crit=n_crit, theta=0.5, precision=precision, mutual=True)
+            ctx.set_bodies(bodies)
+            ctx.evaluate()
+            m, pp = ctx.pair_lists()
+            assert np.array_equal(sorted_pairs(m), sorted_pairs(om))
+            assert np.array_equal(sorted_pairs(pp), sorted_pairs(op))
+            phi, acc = ctx.results("tree")
+            assert rel_l2(phi, t.phi()) <= TOL[precision], (gen, precision, rel_l2(phi, t.phi()))
+            assert rel_l2(acc, t.acc()) <= TOL[precision], (gen, precision, rel_l2(acc, t.acc()))
+            ctx.close()
+    # reference API: dual_tree_traverse(tree, tree, cfg(mutual), KernelVisitor(mutual))
+    bodies = fmmlib.generate_bodies(1, 8192, 5)
+    tree = fmmlib.build_tree(bodies, 64, 5, precision="fp64")
+    kt = fmmlib.KernelTables(5)
+    fmmlib.upward_pass(tree, kt)
+    cfg = fmmlib.TraversalConfig(theta=0.5, mutual=True)
+    fmmlib.dual_tree_traverse(tree, tree, cfg, fmmlib.KernelVisitor(tree, tree, kt, mutual=True))
+    fmmlib.downward_pass(tree, kt)
+    t = orc.build_tree(bodies, 64, 5)
+    orc.evaluate(t, 0.5, mutual=True, with_acc=False)
+    assert rel_l2(fmmlib.potentials(tree), t.phi()) <= 1e-6
+    with pytest.raises(fmmlib.FMMError):
+        fmmlib.dual_tree_traverse(tree, tree, cfg, fmmlib.KernelVisitor(tree, tree, kt, mutual=False))
+
+
 # ------------------------------------------------------------------ pipelines ---------
 CASES = [  # (config or dist, n, seed, n_crit, p, theta)
     ("C1", 16384, 1, 64, 4, 0.5),

@@ -102,6 +102,25 @@ def test_oracle_reproduces_reference_fixtures(orc, fixtures):
         assert np.array_equal(t.locals(), g("local")), name
 
 
+def test_oracle_mutual_reproduces_reference_fixtures(orc, fixtures):
+    """Mutual mode (traversal.hpp:76-84, m2l_mutual / mutual p2p kernels.cpp:113-126, :153-180):
+    the emitted lists, in their emitted orientation, and the mutual pipeline's potentials are
+    bit-exact with the reference; the symmetrised mutual lists equal the non-mutual ones
+    (test_traversal.cpp:182-210)."""
+    for name in case_names(fixtures):
+        g = lambda k: fixtures[f"{name}/{k}"]  # noqa: E731
+        n_crit, p, theta = g("params")
+        t = orc.build_tree(g("bodies"), int(n_crit), int(p))
+        m, pp = orc.traverse(t, float(theta), mutual=True)
+        assert np.array_equal(sorted_pairs(m), g("m2l_mutual")), name
+        assert np.array_equal(sorted_pairs(pp), g("p2p_mutual")), name
+        sym = lambda a: np.concatenate([a, a[a[:, 0] != a[:, 1]][:, ::-1]])  # noqa: E731
+        assert np.array_equal(sorted_pairs(sym(m)), g("m2l")), name
+        assert np.array_equal(sorted_pairs(sym(pp)), g("p2p")), name
+        orc.evaluate(t, float(theta), mutual=True, with_acc=False)
+        assert np.array_equal(t.phi(), g("phi_mutual")), name
+
+
 def test_oracle_matches_reference_build(orc, ref):
     """Against the unmodified reference compiled here (bit-exact), on fresh inputs."""
     for dist, n, seed, n_crit, p in [(0, 3000, 7, 32, 4), (1, 2500, 8, 16, 6), (2, 3000, 9, 24, 5)]:
