@@ -53,10 +53,11 @@ k_p2m(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __rest
       L[P] = 1.0;
       L[2 * P] = 1.0;
 #pragma unroll
-      for (int k = 1; k < P; ++k) {
-        L[k] = L[k - 1] * vx / k;
-        L[P + k] = L[P + k - 1] * vy / k;
-        L[2 * P + k] = L[2 * P + k - 1] * vz / k;
+      for (int k = 1; k < P; ++k) {  // v^k/k! (reciprocals are compile-time constants: no DDIV)
+        const double rk = 1.0 / k;
+        L[k] = L[k - 1] * (vx * rk);
+        L[P + k] = L[P + k - 1] * (vy * rk);
+        L[2 * P + k] = L[2 * P + k - 1] * (vz * rk);
       }
       L[3 * P] = b.w;
     }
@@ -88,110 +89,156 @@ k_p2m(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __rest
   }
 }
 
-// ------------------------------------------------------------------------------ M2M ----
-// One CTA per cell of one level; warp k translates child k (staged multipole + power lines
-// d^k/k! of its shift) into a shared-memory partial, and the partials are summed in child
-// order k = 0..count-1 (the reference's accumulation order, traversal.cpp:44-47).
+// ------------------------------------------------------------- axis line sweeps ------
+// M2M and L2L factorise over the three axes: the 3-D operator is the composition of 1-D
+// operators applied along the "lines" of the coefficient triangle (the exponents on the other
+// two axes fixed). Lane l owns line l of an axis (P(P+1)/2 lines) in a warp-private
+// shared-memory copy of the expansion; the axes are swept in turn with a __syncwarp between.
+// The truncation |alpha| <= P-1 of the reference's term lists (kernels.cpp:25-76) is exactly
+// the lines' lengths, so the result equals the term-list sums up to rounding (parity 1e-12).
+template <int A>
+__device__ __forceinline__ int axis_index(int t, int u, int v) {
+  return A == 0 ? index_of(t, u, v) : (A == 1 ? index_of(u, t, v) : index_of(u, v, t));
+}
+
 template <int P>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ int line_uv(int l, int& u) {  // line l -> (u, v), u + v <= P-1
+  u = 0;
+  while (l >= P - u) {
+    l -= P - u;
+    ++u;
+  }
+  return l;
+}
+
+// L2L along axis A (traversal.cpp:55-57 via l2l, kernels.cpp:128-136): the polynomial
+// sum_t x_t s^t becomes its Taylor shift sum_t x_t (s + d)^t (repeated synthetic division)
+template <int P, int A>
+__device__ __forceinline__ void shift_axis(double* s, double d, int lane) {
+  constexpr int NL = P * (P + 1) / 2;
+  for (int l = lane; l < NL; l += 32) {
+    int u;
+    const int v = line_uv<P>(l, u);
+    const int m = P - u - v;
+    double x[P];
+#pragma unroll
+    for (int t = 0; t < P; ++t) x[t] = t < m ? s[axis_index<A>(t, u, v)] : 0.0;
+#pragma unroll
+    for (int t = 0; t < P - 1; ++t)
+#pragma unroll
+      for (int i = P - 2; i >= t; --i)
+        if (i + 1 < m) x[i] = fma(d, x[i + 1], x[i]);
+#pragma unroll
+    for (int t = 0; t < P; ++t)
+      if (t < m) s[axis_index<A>(t, u, v)] = x[t];
+  }
+}
+
+// M2M along axis A (kernels.cpp:88-96): u_b = sum_{k<=b} x_{b-k} d^k/k!
+template <int P, int A>
+__device__ __forceinline__ void m2m_axis(double* s, const double* D, int lane) {
+  constexpr int NL = P * (P + 1) / 2;
+  for (int l = lane; l < NL; l += 32) {
+    int u;
+    const int v = line_uv<P>(l, u);
+    const int m = P - u - v;
+    double x[P];
+#pragma unroll
+    for (int t = 0; t < P; ++t) x[t] = t < m ? s[axis_index<A>(t, u, v)] : 0.0;
+#pragma unroll
+    for (int b = P - 1; b >= 1; --b) {
+      if (b < m) {
+        double y = x[b];
+#pragma unroll
+        for (int k = 1; k <= b; ++k) y = fma(x[b - k], D[k], y);
+        x[b] = y;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < P; ++t)
+      if (t < m) s[axis_index<A>(t, u, v)] = x[t];
+  }
+}
+
+// ------------------------------------------------------------------------------ M2M ----
+// Warp per cell of one level: each child's multipole (in child order k = 0..count-1, the
+// reference's accumulation order, traversal.cpp:44-47) is translated by three axis sweeps in a
+// warp-private shared-memory copy and added to the lane-owned parent coefficients.
+template <int P>
+__global__ void __launch_bounds__(128)
 k_m2m(int32_t cbeg, int32_t cend, const int32_t* __restrict__ cb, const int32_t* __restrict__ cc,
       const double4* __restrict__ cr, double* __restrict__ M, const int32_t* __restrict__ owner, int32_t want) {
   using T = MI<P>;
   constexpr int N = T::N;
-  __shared__ double sD[8][3 * P];
-  __shared__ double sM[8][N];
-  __shared__ double part[8][N];
+  constexpr int KPL = (N + 31) / 32;
+  __shared__ double sM[4][N];
+  __shared__ double sD[4][3][P];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t ci = cbeg + blockIdx.x;
+  const int32_t ci = cbeg + blockIdx.x * 4 + w;
   if (ci >= cend) return;
   const int32_t nch = cc[ci];
-  if (nch == 0) return;  // uniform over the CTA
+  if (nch == 0) return;
   if (owner && owner[ci] != want) return;  // sharded: only this rank's (or the shared) cells
-  if (w < nch) {
-    const double4 pc = cr[ci];
-    const int32_t child = cb[ci] + w;
+  const double4 pc = cr[ci];
+  double acc[KPL];
+#pragma unroll
+  for (int k = 0; k < KPL; ++k) acc[k] = 0.0;
+  for (int k = 0; k < nch; ++k) {
+    const int32_t child = cb[ci] + k;
     const double4 c4 = cr[child];
     if (lane < 3) {
       const double d = lane == 0 ? c4.x - pc.x : (lane == 1 ? c4.y - pc.y : c4.z - pc.z);
-      double* L = sD[w] + lane * P;
-      L[0] = 1.0;
-      for (int k = 1; k < P; ++k) L[k] = L[k - 1] * d / k;
+      double* D = sD[w][lane];
+      D[0] = 1.0;
+      for (int q = 1; q < P; ++q) D[q] = D[q - 1] * d / q;
     }
     for (int i = lane; i < N; i += 32) sM[w][i] = M[(int64_t)child * N + i];
     __syncwarp();
-    for (int i = lane; i < N; i += 32) {
-      int n = 0;
-      while (n_coef(n + 1) <= i) ++n;
-      int r = i - n_coef(n), a = 0;
-      while (r >= n - a + 1) { r -= n - a + 1; ++a; }
-      const int bb_ = r, cc_ = n - a - r;
-      double s = 0.0;
-      for (int ax = 0; ax <= a; ++ax)
-        for (int ay = 0; ay <= bb_; ++ay) {
-          const double xy = sD[w][a - ax] * sD[w][P + bb_ - ay];
-          for (int az = 0; az <= cc_; ++az) s += sM[w][index_of(ax, ay, az)] * (xy * sD[w][2 * P + cc_ - az]);
-        }
-      part[w][i] = s;
+    m2m_axis<P, 0>(sM[w], sD[w][0], lane);
+    __syncwarp();
+    m2m_axis<P, 1>(sM[w], sD[w][1], lane);
+    __syncwarp();
+    m2m_axis<P, 2>(sM[w], sD[w][2], lane);
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+      const int i = lane + 32 * q;
+      if (i < N) acc[q] += sM[w][i];
     }
+    __syncwarp();
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < nch; ++k) s += part[k][i];
-    M[(int64_t)ci * N + i] = s;
+#pragma unroll
+  for (int q = 0; q < KPL; ++q) {
+    const int i = lane + 32 * q;
+    if (i < N) M[(int64_t)ci * N + i] = acc[q];
   }
 }
 
 // ------------------------------------------------------------------------------ L2L ----
-// Warp per cell of one level (>= 1): child_a += sum_d parent_{a+d} ((a+d)!/a!) d^d/d!,
-// parent local staged in shared memory.
+// Warp per cell of one level (>= 1): the parent local, Taylor-shifted to the child centre by
+// three axis sweeps, is added to the child's local (the M2L result).
 template <int P>
 __global__ void __launch_bounds__(128)
 k_l2l(int32_t cbeg, int32_t cend, const int32_t* __restrict__ par, const double4* __restrict__ cr,
       double* __restrict__ L) {
   using T = MI<P>;
   constexpr int N = T::N;
-  __shared__ double sD[4][3 * P];
   __shared__ double sL[4][N];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t ci = cbeg + blockIdx.x * 4 + w;
   if (ci >= cend) return;
   const int32_t pi = par[ci];
   const double4 c = cr[ci], pc = cr[pi];
-  if (lane < 3) {
-    const double d = lane == 0 ? c.x - pc.x : (lane == 1 ? c.y - pc.y : c.z - pc.z);
-    double* Ld = sD[w] + lane * P;
-    Ld[0] = 1.0;
-    for (int k = 1; k < P; ++k) Ld[k] = Ld[k - 1] * d / k;
-  }
   for (int i = lane; i < N; i += 32) sL[w][i] = L[(int64_t)pi * N + i];
   __syncwarp();
-  __shared__ double sCw[4][P][P];  // (a+d)!/a! (per warp)
-  for (int k = lane; k < P * P; k += 32) {
-    const int a = k / P, d = k % P;
-    double v = 1.0;
-    for (int q = a + 1; q <= a + d; ++q) v *= q;
-    sCw[w][a][d] = v;
-  }
+  shift_axis<P, 0>(sL[w], c.x - pc.x, lane);
   __syncwarp();
-  const auto& sC = sCw[w];
+  shift_axis<P, 1>(sL[w], c.y - pc.y, lane);
+  __syncwarp();
+  shift_axis<P, 2>(sL[w], c.z - pc.z, lane);
+  __syncwarp();
   double* Lc = L + (int64_t)ci * N;
-  for (int i = lane; i < N; i += 32) {
-    int n = 0;
-    while (n_coef(n + 1) <= i) ++n;
-    int r = i - n_coef(n), a = 0;
-    while (r >= n - a + 1) { r -= n - a + 1; ++a; }
-    const int b = r, cz = n - a - r;
-    double s = 0.0;
-    for (int dx = 0; dx + n < P; ++dx)
-      for (int dy = 0; dx + dy + n < P; ++dy) {
-        const double wxy = sC[a][dx] * sC[b][dy];
-        const double pxy = sD[w][dx] * sD[w][P + dy];
-        for (int dz = 0; dx + dy + dz + n < P; ++dz)
-          s += sL[w][index_of(a + dx, b + dy, cz + dz)] * (wxy * sC[cz][dz]) * (pxy * sD[w][2 * P + dz]);
-      }
-    Lc[i] += s;
-  }
+  for (int i = lane; i < N; i += 32) Lc[i] += sL[w][i];
 }
 
 // ------------------------------------------------------------------------------ L2P ----
@@ -216,23 +263,33 @@ k_l2p(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __rest
   const int32_t b0 = bb[leaf], b1 = be[leaf];
   for (int32_t i = b0 + lane; i < b1; i += 32) {
     const double4 b = bodies[i];
-    double X[P], Y[P], Z[P];
-    X[0] = Y[0] = Z[0] = 1.0;
-#pragma unroll
-    for (int k = 1; k < P; ++k) {
-      X[k] = X[k - 1] * (b.x - c.x);
-      Y[k] = Y[k - 1] * (b.y - c.y);
-      Z[k] = Z[k - 1] * (b.z - c.z);
-    }
+    const double x = b.x - c.x, y = b.y - c.y, z = b.z - c.z;
+    // nested Horner: phi = sum_a x^a sum_b y^b sum_c z^c L_abc, derivatives carried along
+    // (dp = dp * x + p before p = p * x + coef); registers only, L broadcast from shared memory
     double ph = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
-    static_for<N>([&](auto I) {
-      constexpr int ii = decltype(I)::value;
-      constexpr int a = T::ea(ii), e = T::eb(ii), f = T::ec(ii);
-      const double l = sL[w][ii];
-      ph = fma(l, X[a] * Y[e] * Z[f], ph);
-      if constexpr (a > 0) gx = fma(l * double(a), X[a - 1] * Y[e] * Z[f], gx);
-      if constexpr (e > 0) gy = fma(l * double(e), X[a] * Y[e - 1] * Z[f], gy);
-      if constexpr (f > 0) gz = fma(l * double(f), X[a] * Y[e] * Z[f - 1], gz);
+    // P >= 8: volatile reads keep the unrolled coefficient loads in order (otherwise they are
+    // hoisted ahead of the FMAs and spill)
+    using LPtr = std::conditional_t<(P >= 8), const volatile double*, const double*>;
+    const LPtr Lw = sL[w];
+    static_for<P>([&](auto AI) {
+      constexpr int a = P - 1 - decltype(AI)::value;
+      double Tv = 0.0, Ty = 0.0, Tz = 0.0;
+      static_for<P - a>([&](auto BI) {
+        constexpr int bb_ = P - 1 - a - decltype(BI)::value;
+        double S = 0.0, Sz = 0.0;
+        static_for<P - a - bb_>([&](auto CI) {
+          constexpr int cc_ = P - 1 - a - bb_ - decltype(CI)::value;
+          Sz = fma(Sz, z, S);
+          S = fma(S, z, Lw[index_of(a, bb_, cc_)]);
+        });
+        Ty = fma(Ty, y, Tv);
+        Tv = fma(Tv, y, S);
+        Tz = fma(Tz, y, Sz);
+      });
+      gx = fma(gx, x, ph);
+      ph = fma(ph, x, Tv);
+      gy = fma(gy, x, Ty);
+      gz = fma(gz, x, Tz);
     });
     phi_out[i] = phi_near[i] + ph;
     if (with_acc) {
@@ -263,7 +320,8 @@ struct Upward {
     for (int l = c->depth - 1; l >= 0; --l) {
       const int32_t b = c->level_start[l], e = c->level_start[l + 1];
       if (e <= b) continue;
-      k_m2m<P><<<e - b, 256, 0, s>>>(b, e, c->c_child_begin.p, c->c_child_count.p, c->c_cr.p, M, owner, want);
+      k_m2m<P><<<ceil_div(e - b, 4), 128, 0, s>>>(b, e, c->c_child_begin.p, c->c_child_count.p, c->c_cr.p, M, owner,
+                                                   want);
       CK_LAUNCH("k_m2m");
       ++launches;
     }

@@ -531,6 +531,180 @@ k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, co
   }
 }
 
+// ------------------------------------------------ FP32 kernel, warp-specialised pipeline ----
+// Same work decomposition and arithmetic as k_p2p_fp32, without per-tile CTA barriers: a fifth
+// (producer) warp resolves each tile's list entries, issues its TMA bulk copies, converts the
+// landed bodies into the target frame and publishes the tile on full[b]; the four consumer
+// warps compute and release the buffer on empty[b] (one arrival per warp). Consumers never wait
+// for each other inside the pipeline, so a warp that finishes its share of a tile early starts
+// on the next one (the producer runs up to one tile ahead: two buffers).
+constexpr int kWsThreads = kThreads + 32;
+
+// producer warp: shift one tile's staged bodies into the target frame and negate
+__device__ __forceinline__ void convert_warp(int lane, const TileTab& tt, float4* buf) {
+  const int nseg = tt.nseg;
+#pragma unroll 1
+  for (int k = 0; k < nseg; k += 4) {
+    int32_t o[4], n[4];
+    float sx[4], sy[4], sz[4];
+    int32_t nm = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool ok = k + q < nseg;
+      o[q] = ok ? tt.off[k + q] : 0;
+      n[q] = ok ? tt.off[k + q + 1] - o[q] : 0;
+      sx[q] = ok ? tt.sh[k + q][0] : 0.f;
+      sy[q] = ok ? tt.sh[k + q][1] : 0.f;
+      sz[q] = ok ? tt.sh[k + q][2] : 0.f;
+      nm = max(nm, n[q]);
+    }
+#pragma unroll 1
+    for (int j = lane; j < nm; j += 32) {
+      float4 a[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (j < n[q]) a[q] = buf[o[q] + j];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (j < n[q]) buf[o[q] + j] = make_float4(-a[q].x - sx[q], -a[q].y - sy[q], -a[q].z - sz[q], a[q].w);
+    }
+  }
+}
+
+__device__ __forceinline__ void convert_prec_warp(int lane, const TileTab& tt, float4* buf) {
+  const int nb = tt.off[tt.nseg];
+  const int nseg = tt.nseg;
+  int k = 0;
+#pragma unroll 1
+  for (int j = lane; j < nb; j += 32) {
+    while (k + 1 < nseg && tt.off[k + 1] <= j) ++k;  // j ascends: the entry index only moves forward
+    const float4 h = buf[j], l = buf[kHalfTile + j];
+    const float2 x = two_sum(h.x, tt.sh[k][0]), y = two_sum(h.y, tt.sh[k][1]), z = two_sum(h.z, tt.sh[k][2]);
+    buf[j] = make_float4(-x.x, -y.x, -z.x, h.w);
+    buf[kHalfTile + j] = make_float4(-((x.y + l.x) + tt.sl[k][0]), -((y.y + l.y) + tt.sl[k][1]),
+                                     -((z.y + l.z) + tt.sl[k][2]), 0.f);
+  }
+}
+
+template <bool kAcc>
+__global__ void __launch_bounds__(kWsThreads, FMM_P2P_MIN_BLOCKS)
+k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, const float4* __restrict__ bodyf,
+              const float4* __restrict__ bodyl, double* __restrict__ phi_out, double* __restrict__ acc_out,
+              double* __restrict__ partial) {
+  __shared__ __align__(16) float4 sS[2][kTileBodies];
+  __shared__ TileTab tabs[2];
+  __shared__ __align__(8) uint64_t full[2], tmab[2], empty[2];
+
+  const P2PItem it = items[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&tmab[b], 1);
+      mbar_init(&empty[b], kThreads / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (tid >= kThreads) {  // ---- producer warp
+    int32_t cursor = it.lb, off = 0;
+    for (unsigned k = 0; cursor < it.le; ++k) {
+      const int b = k & 1;
+      if (k >= 2) mbar_wait(&empty[b], ((k >> 1) - 1) & 1u);
+      tile_setup_ent(lane, it.le, cursor, off, ent + cursor, tabs[b]);
+      __syncwarp();
+      tile_tma(lane, tabs[b], bodyf, bodyl, sS[b], &tmab[b]);
+      mbar_wait(&tmab[b], (k >> 1) & 1u);
+      if (tabs[b].prec) convert_prec_warp(lane, tabs[b], sS[b]);
+      else convert_warp(lane, tabs[b], sS[b]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[b]);
+      cursor = tabs[b].next;
+      off = tabs[b].next_off;
+    }
+    return;
+  }
+
+  // ---- consumer warps
+  const int nt = it.te - it.tb;
+  const int slots = (nt + 1) >> 1;
+  const int G = kThreads / slots;
+  const int g = tid / slots, t = tid - g * slots;
+  const bool active = g < G;
+  Tgt T;
+  T.X = make_float2(0.f, 0.f);
+  T.Y = T.Z = T.XL = T.YL = T.ZL = T.X;
+  if (active) {
+    const int32_t i0 = it.tb + 2 * t, i1 = (2 * t + 1 < nt) ? i0 + 1 : i0;
+    const float4 b0 = bodyf[i0], b1 = bodyf[i1];
+    const float4 l0 = bodyl[i0], l1 = bodyl[i1];
+    T.X = make_float2(b0.x, b1.x);
+    T.Y = make_float2(b0.y, b1.y);
+    T.Z = make_float2(b0.z, b1.z);
+    T.XL = make_float2(l0.x, l1.x);
+    T.YL = make_float2(l0.y, l1.y);
+    T.ZL = make_float2(l0.z, l1.z);
+  }
+  Acc64 A;
+  if (it.lb < it.le) {
+    for (unsigned k = 0;; ++k) {
+      const int b = k & 1;
+      mbar_wait(&full[b], (k >> 1) & 1u);
+      const TileTab& tc = tabs[b];
+      const int nb = tc.off[tc.nseg];
+      const bool prec = tc.prec != 0, guard = tc.guard != 0, more = tc.next < it.le;
+      if (active) {
+        if (!prec)
+          tile_compute<kAcc>(sS[b], nb, g, G, T, A);
+        else if (guard)
+          tile_compute_prec<kAcc, true>(sS[b], nb, g, G, T, A);
+        else
+          tile_compute_prec<kAcc, false>(sS[b], nb, g, G, T, A);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
+      if (!more) break;
+    }
+  }
+  // reduce the G lane groups in fixed order (reusing the tile buffer: the producer is done and
+  // every consumer has released its last tile once this named barrier completes) and write
+  asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads) : "memory");
+  double* red = reinterpret_cast<double*>(sS);  // [G][slots][2 targets][4]
+  if (active) {
+    double* r = red + 8 * (g * slots + t);
+    r[0] = A.ph0; r[1] = A.ax0; r[2] = A.ay0; r[3] = A.az0;
+    r[4] = A.ph1; r[5] = A.ax1; r[6] = A.ay1; r[7] = A.az1;
+  }
+  asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads) : "memory");
+  if (tid < nt) {
+    const int sl = tid >> 1, h = tid & 1;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int gg = 0; gg < G; ++gg) {
+      const double* r = red + 8 * (gg * slots + sl) + 4 * h;
+      v[0] += r[0];
+      v[1] += r[1];
+      v[2] += r[2];
+      v[3] += r[3];
+    }
+    if (it.pbase < 0) {
+      const int32_t i = it.tb + tid;
+      phi_out[i] = v[0];
+      if (kAcc) {
+        acc_out[3 * i] = v[1];
+        acc_out[3 * i + 1] = v[2];
+        acc_out[3 * i + 2] = v[3];
+      }
+    } else {
+      double* p = partial + 4 * ((int64_t)it.pbase + tid);
+      p[0] = v[0];
+      p[1] = v[1];
+      p[2] = v[2];
+      p[3] = v[3];
+    }
+  }
+}
+
 // ------------------------------------------------------------------------ FP64 kernel ----
 // Parity mode: absolute FP64 coordinates and the reference's arithmetic
 // (dx = x_i - y_j, r2 = (dx*dx + dy*dy) + dz*dz, skip r2 == 0, phi += q / sqrt(r2)).
@@ -963,12 +1137,23 @@ void run_p2p(fmm_ctx* c, cudaStream_t s) {
   if (c->n_p2p_items > 0) {
     if (c->cfg.precision == FMM_PREC_FP32_P2P) {
       const P2PEnt* ent = reinterpret_cast<const P2PEnt*>(c->p2p_ent.p);
-      if (wa)
+#ifndef FMM_P2P_WS
+#define FMM_P2P_WS 1
+#endif
+      if (FMM_P2P_WS) {
+        if (wa)
+          k_p2p_fp32_ws<true><<<(unsigned)c->n_p2p_items, kWsThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p,
+                                                                              phi, acc, c->p2p_partial.p);
+        else
+          k_p2p_fp32_ws<false><<<(unsigned)c->n_p2p_items, kWsThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p,
+                                                                               phi, acc, c->p2p_partial.p);
+      } else if (wa) {
         k_p2p_fp32<true><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p, phi,
                                                                        acc, c->p2p_partial.p);
-      else
+      } else {
         k_p2p_fp32<false><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p, phi,
                                                                         acc, c->p2p_partial.p);
+      }
     } else {
       k_p2p_fp64<<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p,
                                                               c->bodies.p, phi, acc, c->p2p_partial.p, wa);
