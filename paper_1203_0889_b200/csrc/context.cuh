@@ -56,6 +56,7 @@ struct fmm_ctx {
   fmmb::DBuf<uint64_t> mut_keys;                     // mutual: emitted + mirrored keys
   fmmb::DBuf<int64_t> m2l_off, p2p_off;
   fmmb::DBuf<int32_t> m2l_src, p2p_src;
+  fmmb::DBuf<int32_t> p2p_tgt;  // target cell of each P2P CSR entry
   fmmb::DBuf<int32_t> m2l_targets;  // cells with non-empty M2L lists
   int64_t n_m2l_targets = 0;
 
@@ -66,7 +67,9 @@ struct fmm_ctx {
   fmmb::DBuf<int4> p2p_reduce;      // target leaf, first slot, n slots, body begin
   fmmb::DBuf<int64_t> p2p_pre;      // exclusive prefix of source-body counts over the P2P list
   fmmb::DBuf<int4> p2p_ent;
-  fmmb::DBuf<double4> leaf_lo, leaf_hi;  // tight body boxes of the leaves (FP32 P2P near test)         // per P2P list entry: {body_begin, count, shift.xy} + {shift.z,...}
+  fmmb::DBuf<double4> leaf_lo, leaf_hi;  // tight body boxes of the leaves (FP32 P2P near test)
+  fmmb::DBuf<int64_t> ent_cls, ent_pre;  // entry class counters (near | far << 32) and their scan
+  fmmb::DBuf<int32_t> self_pos;          // per cell: CSR position of its self entry, -1 = none         // per P2P list entry: {body_begin, count, shift.xy} + {shift.z,...}
   int64_t n_p2p_reduce = 0;
 
   // expansions and outputs

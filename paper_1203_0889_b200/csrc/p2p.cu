@@ -929,8 +929,8 @@ __global__ void k_write_items(const int32_t* __restrict__ leaves, int64_t nleave
     }
 }
 
-// P2P list entries of one target cell per warp: {source body range, kind, FP64 centre shift into
-// the target leaf frame as FP32 hi + lo}. Within each target's (source-sorted) list the order is
+// P2P list entries: {source body range, kind, FP64 centre shift into the target leaf frame as
+// FP32 hi + lo}. Within each target's (source-sorted) list the order is
 // self entry, near entries, far entries (each group ascending by source), so that a work item's
 // tiles each hold one class: only the self tile runs the r^2 == 0 guard and only self / near
 // tiles pay for compensated coordinates. Near = the tight body boxes of the two leaves are less
@@ -974,63 +974,71 @@ __global__ void k_leaf_boxes(const int32_t* __restrict__ leaves, int64_t nleaves
   }
 }
 
-__global__ void k_p2p_entries(const int64_t* __restrict__ off, int64_t ncells, const int32_t* __restrict__ src,
-                              const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
-                              const double4* __restrict__ cr, const double4* __restrict__ blo,
-                              const double4* __restrict__ bhi, P2PEnt* __restrict__ ent) {
-  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= ncells) return;
+// Entry-parallel (C3's halo leaf alone has 57 K entries): pass 1 classifies every entry
+// (self / near / far) and records each target's self position; an exclusive scan of the packed
+// per-class indicators (near in the low, far in the high 32 bits) gives every entry its rank
+// within its target's class; pass 2 writes the entry at
+//   self: l0 | near: l0 + has_self + near rank | far: l0 + has_self + n_near + far rank.
+__global__ void k_ent_class(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src, int64_t ne,
+                            const double4* __restrict__ cr, const double4* __restrict__ blo,
+                            const double4* __restrict__ bhi, int64_t* __restrict__ cls,
+                            int32_t* __restrict__ self_pos) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k > ne) return;
+  if (k == ne) {
+    cls[k] = 0;
+    return;
+  }
+  const int32_t t = tgt[k], s = src[k];
+  int64_t v;
+  if (s == t) {
+    self_pos[t] = static_cast<int32_t>(k);
+    v = 0;
+  } else {
+    const bool nr = near_leaf(blo[t], bhi[t], blo[s], bhi[s], 0.05 * (cr[t].w + cr[s].w));
+    v = nr ? 1ll : (1ll << 32);
+  }
+  cls[k] = v;
+}
+
+__global__ void k_ent_write(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src, int64_t ne,
+                            const int64_t* __restrict__ off, const int64_t* __restrict__ cls,
+                            const int64_t* __restrict__ pre, const int32_t* __restrict__ self_pos,
+                            const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
+                            const double4* __restrict__ cr, P2PEnt* __restrict__ ent) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= ne) return;
+  const int32_t t = tgt[k], s = src[k];
   const int64_t l0 = off[t], l1 = off[t + 1];
-  if (l0 == l1) return;
-  const double4 ct = cr[t], tlo = blo[t], thi = bhi[t];
-  const unsigned below = (1u << lane) - 1u;
-  int64_t nnear = 0, nself = 0;
-  for (int64_t kb = l0; kb < l1; kb += 32) {
-    const int64_t k = kb + lane;
-    bool nr = false, sf = false;
-    if (k < l1) {
-      const int32_t s = src[k];
-      sf = s == t;
-      nr = !sf && near_leaf(tlo, thi, blo[s], bhi[s], 0.05 * (ct.w + cr[s].w));
-    }
-    nnear += __popc(__ballot_sync(0xffffffffu, nr));
-    nself += __popc(__ballot_sync(0xffffffffu, sf));
+  const int64_t hs = self_pos[t] >= 0 ? 1 : 0;
+  const int64_t v = cls[k], P0 = pre[l0], Pk = pre[k];
+  const int64_t lo0 = P0 & 0xffffffffll, hi0 = P0 >> 32;
+  int64_t pos;
+  int kind;
+  if (s == t) {
+    pos = l0;
+    kind = kKindSelf;
+  } else if (v == 1) {
+    pos = l0 + hs + ((Pk & 0xffffffffll) - lo0);
+    kind = kKindNear;
+  } else {
+    const int64_t nnear = (pre[l1] & 0xffffffffll) - lo0;
+    pos = l0 + hs + nnear + ((Pk >> 32) - hi0);
+    kind = kKindFar;
   }
-  int64_t pn = l0 + nself, pf = l0 + nself + nnear;  // next near / far position
-  for (int64_t kb = l0; kb < l1; kb += 32) {
-    const int64_t k = kb + lane;
-    const bool valid = k < l1;
-    int32_t s = 0;
-    double4 cs = ct;
-    bool sf = false, nr = false;
-    if (valid) {
-      s = src[k];
-      cs = cr[s];
-      sf = s == t;
-      nr = !sf && near_leaf(tlo, thi, blo[s], bhi[s], 0.05 * (ct.w + cs.w));
-    }
-    const unsigned mn = __ballot_sync(0xffffffffu, nr);
-    const unsigned mf = __ballot_sync(0xffffffffu, valid && !sf && !nr);
-    if (valid) {
-      const int64_t pos = sf ? l0 : nr ? pn + __popc(mn & below) : pf + __popc(mf & below);
-      const double dx = cs.x - ct.x, dy = cs.y - ct.y, dz = cs.z - ct.z;
-      const float hx = static_cast<float>(dx), hy = static_cast<float>(dy), hz = static_cast<float>(dz);
-      const int kind = sf ? kKindSelf : nr ? kKindNear : kKindFar;
-      P2PEnt e;
-      e.bb = bb[s];
-      e.nk = (be[s] - bb[s]) | (kind << 30);
-      e.sx = hx;
-      e.sy = hy;
-      e.sz = hz;
-      e.lx = static_cast<float>(dx - hx);
-      e.ly = static_cast<float>(dy - hy);
-      e.lz = static_cast<float>(dz - hz);
-      ent[pos] = e;
-    }
-    pn += __popc(mn);
-    pf += __popc(mf);
-  }
+  const double4 ct = cr[t], cs = cr[s];
+  const double dx = cs.x - ct.x, dy = cs.y - ct.y, dz = cs.z - ct.z;
+  const float hx = static_cast<float>(dx), hy = static_cast<float>(dy), hz = static_cast<float>(dz);
+  P2PEnt e;
+  e.bb = bb[s];
+  e.nk = (be[s] - bb[s]) | (kind << 30);
+  e.sx = hx;
+  e.sy = hy;
+  e.sz = hz;
+  e.lx = static_cast<float>(dx - hx);
+  e.ly = static_cast<float>(dy - hy);
+  e.lz = static_cast<float>(dz - hz);
+  ent[pos] = e;
 }
 
 __global__ void k_iota(int32_t* __restrict__ v, int64_t n) {
@@ -1106,10 +1114,20 @@ void build_p2p_worklist(fmm_ctx* c) {
     double4* bhi = c->leaf_hi.ensure(c->ncells);
     k_leaf_boxes<<<ceil_div(c->nleaves * 32, 256), 256, 0, s>>>(c->leaves.p, c->nleaves, c->c_body_begin.p,
                                                                c->c_body_end.p, c->bodies.p, blo, bhi);
-    k_p2p_entries<<<ceil_div(c->ncells * 32, 256), 256, 0, s>>>(c->p2p_off.p, c->ncells, c->p2p_src.p,
-                                                                c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, blo,
-                                                                bhi, ent);
-    CK_LAUNCH("k_p2p_entries");
+    int64_t* cls = c->ent_cls.ensure(ne + 1);
+    int64_t* epre = c->ent_pre.ensure(ne + 1);
+    int32_t* spos = c->self_pos.ensure(c->ncells);
+    CK(cudaMemsetAsync(spos, 0xff, sizeof(int32_t) * c->ncells, s));
+    k_ent_class<<<ceil_div(ne + 1, 256), 256, 0, s>>>(c->p2p_tgt.p, c->p2p_src.p, ne, c->c_cr.p, blo, bhi, cls, spos);
+    {
+      size_t sb = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, cls, epre, (int)(ne + 1), s));
+      CK(cub::DeviceScan::ExclusiveSum(temp_storage(c, sb), sb, cls, epre, (int)(ne + 1), s));
+    }
+    k_ent_write<<<ceil_div(ne, 256), 256, 0, s>>>(c->p2p_tgt.p, c->p2p_src.p, ne, c->p2p_off.p, cls, epre, spos,
+                                                  c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, ent);
+    CK_LAUNCH("k_ent_write");
+    c->kernel_launches += 3;
     c->kernel_launches += 2;
   }
   // cost-sorted (descending, stable) work list: the longest items launch first

@@ -184,7 +184,8 @@ constexpr uint64_t kMirrorBit = 1ull << 63;
 
 template <class KeyT>
 __global__ void k_csr_from_keys(const KeyT* __restrict__ keys, int64_t n, int sbits, int64_t ncells,
-                                int64_t* __restrict__ off, int32_t* __restrict__ src, uint8_t* __restrict__ mir) {
+                                int64_t* __restrict__ off, int32_t* __restrict__ src, uint8_t* __restrict__ mir,
+                                int32_t* __restrict__ tgt) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i > n) return;
   const uint64_t mask = (1ull << sbits) - 1, range = (1ull << (2 * sbits)) - 1;
@@ -197,6 +198,7 @@ __global__ void k_csr_from_keys(const KeyT* __restrict__ keys, int64_t n, int sb
   if (i < n) {
     src[i] = (int32_t)(keys[i] & mask);
     if (mir) mir[i] = static_cast<uint8_t>(static_cast<uint64_t>(keys[i]) >> 63);
+    if (tgt) tgt[i] = static_cast<int32_t>(t);  // ncells for a dropped slot (past off[ncells])
   }
   for (int64_t c = tp + 1; c <= t; ++c) off[c] = i;
 }
@@ -235,7 +237,8 @@ inline bool small_keys(int64_t ncells) { return 2 * bits_for(static_cast<uint64_
 inline bool keys32(const fmm_ctx* c) { return !c->cfg.mutual && small_keys(c->ncells); }
 
 template <class KeyT>
-void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int32_t>& src, uint8_t* mir) {
+void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int32_t>& src, uint8_t* mir,
+                 int32_t* tgt = nullptr) {
   cudaStream_t s = c->stream;
   const int64_t nc = c->ncells;
   off.ensure(nc + 1);
@@ -249,7 +252,7 @@ void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int
   size_t sb = 0;
   CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys, kb, (int)n, 0, 2 * sbits, s));
   CK(cub::DeviceRadixSort::SortKeys(temp_storage(c, sb), sb, keys, kb, (int)n, 0, 2 * sbits, s));
-  k_csr_from_keys<<<ceil_div(n + 1, 256), 256, 0, s>>>(kb, n, sbits, nc, off.p, src.p, mir);
+  k_csr_from_keys<<<ceil_div(n + 1, 256), 256, 0, s>>>(kb, n, sbits, nc, off.p, src.p, mir, tgt);
   CK_LAUNCH("keys_to_csr");
   c->kernel_launches += 3;
 }
@@ -285,7 +288,8 @@ void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
     if (n_p2p) k_mirror_keys<<<ceil_div(n_p2p, 256), 256, 0, s>>>(c->p2p_keys.p, n_p2p, sbits, dp);
     CK_LAUNCH("k_mirror_keys");
     keys_to_csr(c, dm, 2 * n_m2l, c->m2l_off, c->m2l_src, c->m2l_mir.ensure(2 * n_m2l + 1));
-    keys_to_csr(c, dp, 2 * n_p2p, c->p2p_off, c->p2p_src, c->p2p_mir.ensure(2 * n_p2p + 1));
+    keys_to_csr(c, dp, 2 * n_p2p, c->p2p_off, c->p2p_src, c->p2p_mir.ensure(2 * n_p2p + 1),
+                c->p2p_tgt.ensure(2 * n_p2p + 1));
     CK(cudaMemcpyAsync(c->hpin + 2, c->m2l_off.p + c->ncells, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->hpin + 3, c->p2p_off.p + c->ncells, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -293,10 +297,11 @@ void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
     n_p2p = c->hpin[3];
   } else if (keys32(c)) {
     keys_to_csr(c, reinterpret_cast<uint32_t*>(c->m2l_keys.p), n_m2l, c->m2l_off, c->m2l_src, nullptr);
-    keys_to_csr(c, reinterpret_cast<uint32_t*>(c->p2p_keys.p), n_p2p, c->p2p_off, c->p2p_src, nullptr);
+    keys_to_csr(c, reinterpret_cast<uint32_t*>(c->p2p_keys.p), n_p2p, c->p2p_off, c->p2p_src, nullptr,
+                c->p2p_tgt.ensure(n_p2p + 1));
   } else {
     keys_to_csr(c, c->m2l_keys.p, n_m2l, c->m2l_off, c->m2l_src, nullptr);
-    keys_to_csr(c, c->p2p_keys.p, n_p2p, c->p2p_off, c->p2p_src, nullptr);
+    keys_to_csr(c, c->p2p_keys.p, n_p2p, c->p2p_off, c->p2p_src, nullptr, c->p2p_tgt.ensure(n_p2p + 1));
   }
   c->n_m2l = n_m2l;
   c->n_p2p = n_p2p;
