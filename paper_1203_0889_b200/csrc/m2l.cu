@@ -5,6 +5,14 @@
 #include "expansions.cuh"
 #include "tma.cuh"
 
+// A/B switches (tools/m2l_ab.sh): split recurrence sums, next-chunk centre prefetch
+#ifndef FMM_M2L_TWOACC
+#define FMM_M2L_TWOACC 0
+#endif
+#ifndef FMM_M2L_PREFETCH
+#define FMM_M2L_PREFETCH 0
+#endif
+
 namespace fmmb {
 namespace {
 
@@ -118,14 +126,25 @@ __device__ __forceinline__ void derivs_reg(double rx, double ry, double rz, doub
     constexpr int a = T::ea(i), b = T::eb(i), c = T::ec(i), n = T::deg(i);
     if constexpr (i > 0 && c <= 2) {
       constexpr double cn = double(n - 1) / double(2 * n - 1);
-      double acc = 0.0;
-      if constexpr (a >= 1) acc = fma(double(a) * rx, D[H::g_of(index_of(a - 1, b, c))], acc);
-      if constexpr (b >= 1) acc = fma(double(b) * ry, D[H::g_of(index_of(a, b - 1, c))], acc);
-      if constexpr (c >= 1) acc = fma(double(c) * rz, D[H::g_of(index_of(a, b, c - 1))], acc);
-      if constexpr (a >= 2) acc = fma(double(a * (a - 1)) * cn, D[H::g_of(index_of(a - 2, b, c))], acc);
-      if constexpr (b >= 2) acc = fma(double(b * (b - 1)) * cn, D[H::g_of(index_of(a, b - 2, c))], acc);
-      if constexpr (c >= 2) acc = fma(double(c * (c - 1)) * cn, D[H::g_of(index_of(a, b, c - 2))], acc);
-      D[H::g_of(i)] = an[n] * acc;
+      // two independent partial sums (first- and second-order terms): half the dependent-FMA
+      // chain of the degree recurrence (it is latency-bound at the register kernels' occupancy)
+      double acc1 = 0.0;
+#if FMM_M2L_TWOACC
+      double acc2 = 0.0;
+#else
+      double& acc2 = acc1;
+#endif
+      if constexpr (a >= 1) acc1 = fma(double(a) * rx, D[H::g_of(index_of(a - 1, b, c))], acc1);
+      if constexpr (b >= 1) acc1 = fma(double(b) * ry, D[H::g_of(index_of(a, b - 1, c))], acc1);
+      if constexpr (c >= 1) acc1 = fma(double(c) * rz, D[H::g_of(index_of(a, b, c - 1))], acc1);
+      if constexpr (a >= 2) acc2 = fma(double(a * (a - 1)) * cn, D[H::g_of(index_of(a - 2, b, c))], acc2);
+      if constexpr (b >= 2) acc2 = fma(double(b * (b - 1)) * cn, D[H::g_of(index_of(a, b - 2, c))], acc2);
+      if constexpr (c >= 2) acc2 = fma(double(c * (c - 1)) * cn, D[H::g_of(index_of(a, b, c - 2))], acc2);
+#if FMM_M2L_TWOACC
+      D[H::g_of(i)] = an[n] * (acc1 + acc2);
+#else
+      D[H::g_of(i)] = an[n] * acc1;
+#endif
     }
   });
 }
@@ -177,6 +196,9 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
 #pragma unroll
   for (int i = 0; i < NA; ++i) lam[i] = 0.0;
   int32_t s_next = (l0 + lane < l1) ? src[l0 + lane] : t;
+#if FMM_M2L_PREFETCH
+  double4 cs_next = cr[s_next];
+#endif
   for (int64_t base = l0; base < l1; base += 32) {
     const int64_t k = base + lane;
     const bool valid = k < l1;
@@ -202,10 +224,18 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
     } else {
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
+#if FMM_M2L_PREFETCH
+    const double4 cs = cs_next;
+    if (base + 32 + lane < l1) {
+      s_next = src[base + 32 + lane];
+      cs_next = cr[s_next];  // next chunk's centre: its L2 latency hides behind this chunk
+    }
+#else
     if (base + 32 + lane < l1) s_next = src[base + 32 + lane];
+    const double4 cs = valid ? cr[s] : ct;
+#endif
     double rx = 1.0, ry = 0.0, rz = 0.0;
     if (valid) {
-      const double4 cs = cr[s];
       rx = cs.x - ct.x;  // R = source centre - target centre (traversal.hpp:146)
       ry = cs.y - ct.y;
       rz = cs.z - ct.z;
@@ -447,6 +477,153 @@ k_m2l_big(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
   }
 }
 
+// ------------------------------------------------- staged-row M2L (p >= 7), v2 ----
+// Lane = source, warp = target, like k_m2l_reg, with the per-lane state split by size:
+//  * Dt (g_c <= 2; p = 10: 136 values) in registers (derivs_reg, no shared-memory row);
+//  * the detraced source row M' (100 values) staged in the warp's shared memory by one TMA
+//    bulk copy per lane, read back as broadcast-free own-row loads (16-B stride with an odd
+//    half: conflict-free);
+//  * the lane's partial Lambda (100 values) in a shared-memory row (odd stride), streamed
+//    through registers in blocks of kBlk coefficients: per block and source, kBlk loads and
+//    stores against ~2035 / (NA / kBlk) FMAs.
+// No L2 scratch, no global gathers inside the contraction. The 32 Lambda rows are reduced
+// once per target, then the c >= 2 entries follow from the trace identity.
+template <int P>
+struct BigCfg2 {
+  static constexpr int NA = HM<P>::NA, NG = HM<P>::NG;
+  static constexpr int SA = m2l_row_stride(NA);  // staged M' rows (TMA: 16-B multiples)
+  static constexpr int SL = odd_stride(NA);      // Lambda rows
+#ifndef FMM_BIG2_BLK
+#define FMM_BIG2_BLK 20
+#endif
+  static constexpr int kBlk = FMM_BIG2_BLK;
+  static constexpr int kBlocks = (NA + kBlk - 1) / kBlk;
+  static constexpr size_t kSmemPerWarp = sizeof(double) * 32 * (SA + SL);
+};
+
+template <int P>
+__global__ void __launch_bounds__(32, 1)
+k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* __restrict__ off,
+           const int32_t* __restrict__ src, const double4* __restrict__ cr, const double* __restrict__ Mt,
+           double* __restrict__ L) {
+  using T = MI<P>;
+  using H = HM<P>;
+  using C = BigCfg2<P>;
+  constexpr int N = T::N, NA = C::NA, NG = C::NG, SA = C::SA, SL = C::SL;
+  constexpr bool kBulk = (NA * 8) % 16 == 0;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) uint64_t bar;
+  const int lane = threadIdx.x;
+  double* rowsM = smem;            // [32][SA]
+  double* rowsL = smem + 32 * SA;  // [32][SL]
+  double* myM = rowsM + lane * SA;
+  double* myL = rowsL + lane * SL;
+  if (kBulk && lane == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  unsigned phase = 0;
+  const int64_t wid = blockIdx.x;
+  if (wid >= ntargets) return;
+  const int32_t t = targets[wid];
+  const double4 ct = cr[t];
+  const int64_t l0 = off[t], l1 = off[t + 1];
+  for (int i = 0; i < NA; ++i) myL[i] = 0.0;
+  int32_t s_next = (l0 + lane < l1) ? src[l0 + lane] : t;
+#if FMM_M2L_PREFETCH
+  double4 cs_next = cr[s_next];
+#endif
+  for (int64_t base = l0; base < l1; base += 32) {
+    const int64_t k = base + lane;
+    const bool valid = k < l1;
+    const int32_t s = s_next;
+    if (!valid) {
+      for (int e = 0; e < NA; ++e) myM[e] = 0.0;  // tail lanes contribute nothing
+    } else if constexpr (kBulk) {
+      fence_proxy_async_smem();
+      bulk_g2s(myM, Mt + (int64_t)s * NA, NA * 8, &bar);
+    } else {
+      const char* row = reinterpret_cast<const char*>(Mt + (int64_t)s * NA);
+      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(myM));
+#pragma unroll 1
+      for (int e = 0; e < NA * 8; e += 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + e), "l"(row + e));
+    }
+    if constexpr (kBulk) {
+      if (lane == 0) {
+        const int64_t nv = l1 - base < 32 ? l1 - base : 32;
+        mbar_arrive_expect_tx(&bar, static_cast<unsigned>(nv * NA * 8));
+      }
+    } else {
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+#if FMM_M2L_PREFETCH
+    const double4 cs = cs_next;
+    if (base + 32 + lane < l1) {
+      s_next = src[base + 32 + lane];
+      cs_next = cr[s_next];  // next chunk's centre: its L2 latency hides behind this chunk
+    }
+#else
+    if (base + 32 + lane < l1) s_next = src[base + 32 + lane];
+    const double4 cs = valid ? cr[s] : ct;
+#endif
+    double rx = 1.0, ry = 0.0, rz = 0.0;
+    if (valid) {
+      rx = cs.x - ct.x;  // R = source centre - target centre (traversal.hpp:146)
+      ry = cs.y - ct.y;
+      rz = cs.z - ct.z;
+    }
+    double D[NG];
+    derivs_reg<P>(rx, ry, rz, D);
+    if constexpr (kBulk) {
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+    } else {
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+    }
+    __syncwarp();
+    const volatile double* vM = myM;
+    static_for<C::kBlocks>([&](auto BI) {
+      constexpr int b0 = decltype(BI)::value * C::kBlk;
+      constexpr int b1 = (b0 + C::kBlk < NA) ? b0 + C::kBlk : NA;
+      double lam[b1 - b0];
+#pragma unroll
+      for (int j = 0; j < b1 - b0; ++j) lam[j] = myL[b0 + j];
+      static_for<NA>([&](auto KA) {
+        constexpr int ka = decltype(KA)::value;
+        constexpr int ia = H::a_full(ka);
+        constexpr int aa = T::ea(ia), ab = T::eb(ia), ac = T::ec(ia), da = T::deg(ia);
+        if constexpr (da + T::deg(H::a_full(b0)) <= P - 1) {
+          // volatile: reloaded in every block (the smem load is cheap); otherwise the compiler
+          // keeps all NA values live across the blocks and spills the Dt registers
+          const double m = vM[ka];
+          static_for<b1 - b0>([&](auto J) {
+            constexpr int ib = H::a_full(b0 + decltype(J)::value);
+            if constexpr (da + T::deg(ib) <= P - 1) {
+              constexpr int ig = H::g_of(index_of(aa + T::ea(ib), ab + T::eb(ib), ac + T::ec(ib)));
+              lam[decltype(J)::value] = fma(m, D[ig], lam[decltype(J)::value]);
+            }
+          });
+        }
+      });
+#pragma unroll
+      for (int j = 0; j < b1 - b0; ++j) myL[b0 + j] = lam[j];
+    });
+    __syncwarp();  // every lane done with its M' row before the next chunk's copies land
+  }
+  // reduce the 32 lane rows (column sums, fixed order) ...
+  double* cmp = rowsM;            // NA reduced values
+  double* full = rowsM + NA + 1;  // N values (32 * SA >= NA + N + 1)
+  for (int kk = lane; kk < NA; kk += 32) {
+    double acc = 0.0;
+    for (int j = 0; j < 32; ++j) acc += rowsL[j * SL + kk];
+    cmp[kk] = acc;
+  }
+  __syncwarp();
+  trace_fill_store<P>(lane, cmp, full, L + (int64_t)t * N);
+}
+
 template <int P>
 struct M2L {
   static void run(fmm_ctx* c, cudaStream_t s) {
@@ -464,6 +641,25 @@ struct M2L {
       k_m2l_reg<P><<<ceil_div(c->n_m2l_targets, kM2LWarps), 32 * kM2LWarps, smem, s>>>(c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p,
                                                                     c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
       CK_LAUNCH("k_m2l_reg");
+      c->kernel_launches += 2;
+      return;
+    }
+#ifndef FMM_M2L_BIG_V2
+#define FMM_M2L_BIG_V2 1
+#endif
+    if (FMM_M2L_BIG_V2) {
+      using C2 = BigCfg2<P>;
+      static bool attr2 = false;
+      if (!attr2) {
+        CK(cudaFuncSetAttribute(k_m2l_big2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C2::kSmemPerWarp));
+        attr2 = true;
+      }
+      if (c->n_m2l_targets == 0) return;
+      double* Mt = c->m2l_mt.ensure(c->ncells * C2::NA + 1);
+      launch_detrace<P>(c, Mt, s);
+      k_m2l_big2<P><<<(unsigned)c->n_m2l_targets, 32, C2::kSmemPerWarp, s>>>(
+          c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p, c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
+      CK_LAUNCH("k_m2l_big2");
       c->kernel_launches += 2;
       return;
     }
