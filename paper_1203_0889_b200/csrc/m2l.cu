@@ -5,7 +5,11 @@
 #include "expansions.cuh"
 #include "tma.cuh"
 
-// A/B switches (tools/m2l_ab.sh): split recurrence sums, next-chunk centre prefetch
+// A/B switches (tools/m2l_ab.sh): split recurrence sums, next-chunk centre prefetch, volatile
+// source-row reads in k_m2l_big2
+#ifndef FMM_BIG2_VOLATILE
+#define FMM_BIG2_VOLATILE 0
+#endif
 #ifndef FMM_M2L_TWOACC
 #define FMM_M2L_TWOACC 0
 #endif
@@ -145,6 +149,35 @@ __device__ __forceinline__ void derivs_reg(double rx, double ry, double rz, doub
 #else
       D[H::g_of(i)] = an[n] * acc1;
 #endif
+    }
+  });
+}
+
+// Same recurrence restricted to g_c <= 1 (the compact a-order HM::a_of, NA values): the set is
+// closed under the recurrence. Used when the g_c = 2 entries are folded by the trace identity
+// Dt_{x,y,2} = -Dt_{x+2,y,0} - Dt_{x,y+2,0} (k_m2l_big2 at p = 10: 100 registers instead of 136).
+template <int P>
+__device__ __forceinline__ void derivs_reg1(double rx, double ry, double rz, double (&D)[HM<P>::NA]) {
+  using T = MI<P>;
+  using H = HM<P>;
+  const double r2 = (rx * rx + ry * ry) + rz * rz;
+  D[0] = rsqrt(r2);
+  const double inv_r2 = D[0] * D[0];
+  double an[P];
+#pragma unroll
+  for (int n = 1; n < P; ++n) an[n] = (-double(2 * n - 1) / double(n)) * inv_r2;
+  static_for<T::N>([&](auto I) {
+    constexpr int i = decltype(I)::value;
+    constexpr int a = T::ea(i), b = T::eb(i), c = T::ec(i), n = T::deg(i);
+    if constexpr (i > 0 && c <= 1) {
+      constexpr double cn = double(n - 1) / double(2 * n - 1);
+      double acc = 0.0;
+      if constexpr (a >= 1) acc = fma(double(a) * rx, D[H::a_of(index_of(a - 1, b, c))], acc);
+      if constexpr (b >= 1) acc = fma(double(b) * ry, D[H::a_of(index_of(a, b - 1, c))], acc);
+      if constexpr (c >= 1) acc = fma(double(c) * rz, D[H::a_of(index_of(a, b, c - 1))], acc);
+      if constexpr (a >= 2) acc = fma(double(a * (a - 1)) * cn, D[H::a_of(index_of(a - 2, b, c))], acc);
+      if constexpr (b >= 2) acc = fma(double(b * (b - 1)) * cn, D[H::a_of(index_of(a, b - 2, c))], acc);
+      D[H::a_of(i)] = an[n] * acc;
     }
   });
 }
@@ -498,7 +531,20 @@ struct BigCfg2 {
 #endif
   static constexpr int kBlk = FMM_BIG2_BLK;
   static constexpr int kBlocks = (NA + kBlk - 1) / kBlk;
-  static constexpr size_t kSmemPerWarp = sizeof(double) * 32 * (SA + SL);
+#ifndef FMM_BIG2_C1_MIN_P
+#define FMM_BIG2_C1_MIN_P 10
+#endif
+  static constexpr bool kC1 = P >= FMM_BIG2_C1_MIN_P;  // Dt over g_c <= 1 only (register budget)
+#ifndef FMM_BIG2_LR_MIN_P
+#define FMM_BIG2_LR_MIN_P 10
+#endif
+  // kLR: the lanes' block partials are reduced after every block (transpose through a 32 x kBlk
+  // buffer) into lane-owned target accumulators, instead of a Lambda row per lane: 5 KB instead
+  // of 26 KB of shared memory per warp (p = 10), so 7 instead of 4 warps per SM (C5 M2L
+  // 24.5 -> 19.6 ms; at p = 8 the extra reductions cost more than the occupancy gains)
+  static constexpr bool kLR = P >= FMM_BIG2_LR_MIN_P;
+  static constexpr int SB = odd_stride(kBlk);
+  static constexpr size_t kSmemPerWarp = sizeof(double) * 32 * (SA + (kLR ? SB : SL));
 };
 
 template <int P>
@@ -529,7 +575,12 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
   const int32_t t = targets[wid];
   const double4 ct = cr[t];
   const int64_t l0 = off[t], l1 = off[t + 1];
-  for (int i = 0; i < NA; ++i) myL[i] = 0.0;
+  constexpr bool kLR = C::kLR;
+  double accT[C::kBlocks];  // kLR: Lambda_{q kBlk + lane} of the target (lanes < block width)
+#pragma unroll
+  for (int q = 0; q < C::kBlocks; ++q) accT[q] = 0.0;
+  if constexpr (!kLR)
+    for (int i = 0; i < NA; ++i) myL[i] = 0.0;
   int32_t s_next = (l0 + lane < l1) ? src[l0 + lane] : t;
 #if FMM_M2L_PREFETCH
   double4 cs_next = cr[s_next];
@@ -574,8 +625,10 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
       ry = cs.y - ct.y;
       rz = cs.z - ct.z;
     }
-    double D[NG];
-    derivs_reg<P>(rx, ry, rz, D);
+    constexpr bool kC1 = C::kC1;
+    double D[kC1 ? NA : NG];
+    if constexpr (kC1) derivs_reg1<P>(rx, ry, rz, D);
+    else derivs_reg<P>(rx, ry, rz, D);
     if constexpr (kBulk) {
       mbar_wait(&bar, phase);
       phase ^= 1u;
@@ -583,42 +636,76 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
       asm volatile("cp.async.wait_all;\n" ::: "memory");
     }
     __syncwarp();
+    // the source row is re-read in every block: a compiler memory barrier between blocks keeps
+    // the loads from being merged across blocks (all NA values live: the Dt registers spill)
+    // while leaving them free to be scheduled early within a block
+#if FMM_BIG2_VOLATILE
     const volatile double* vM = myM;
+#else
+    const double* vM = myM;
+#endif
     static_for<C::kBlocks>([&](auto BI) {
       constexpr int b0 = decltype(BI)::value * C::kBlk;
+      asm volatile("" ::: "memory");
       constexpr int b1 = (b0 + C::kBlk < NA) ? b0 + C::kBlk : NA;
       double lam[b1 - b0];
 #pragma unroll
-      for (int j = 0; j < b1 - b0; ++j) lam[j] = myL[b0 + j];
+      for (int j = 0; j < b1 - b0; ++j) lam[j] = kLR ? 0.0 : myL[b0 + j];
       static_for<NA>([&](auto KA) {
         constexpr int ka = decltype(KA)::value;
         constexpr int ia = H::a_full(ka);
         constexpr int aa = T::ea(ia), ab = T::eb(ia), ac = T::ec(ia), da = T::deg(ia);
         if constexpr (da + T::deg(H::a_full(b0)) <= P - 1) {
-          // volatile: reloaded in every block (the smem load is cheap); otherwise the compiler
-          // keeps all NA values live across the blocks and spills the Dt registers
           const double m = vM[ka];
           static_for<b1 - b0>([&](auto J) {
             constexpr int ib = H::a_full(b0 + decltype(J)::value);
             if constexpr (da + T::deg(ib) <= P - 1) {
-              constexpr int ig = H::g_of(index_of(aa + T::ea(ib), ab + T::eb(ib), ac + T::ec(ib)));
-              lam[decltype(J)::value] = fma(m, D[ig], lam[decltype(J)::value]);
+              constexpr int gx = aa + T::ea(ib), gy = ab + T::eb(ib), gz = ac + T::ec(ib);
+              if constexpr (!kC1) {
+                constexpr int ig = H::g_of(index_of(gx, gy, gz));
+                lam[decltype(J)::value] = fma(m, D[ig], lam[decltype(J)::value]);
+              } else if constexpr (gz <= 1) {
+                lam[decltype(J)::value] = fma(m, D[H::a_of(index_of(gx, gy, gz))], lam[decltype(J)::value]);
+              } else {  // gz == 2: trace identity
+                lam[decltype(J)::value] = fma(-m, D[H::a_of(index_of(gx + 2, gy, 0))], lam[decltype(J)::value]);
+                lam[decltype(J)::value] = fma(-m, D[H::a_of(index_of(gx, gy + 2, 0))], lam[decltype(J)::value]);
+              }
             }
           });
         }
       });
+      if constexpr (kLR) {
+        double* red = rowsL;  // [32][SB]
 #pragma unroll
-      for (int j = 0; j < b1 - b0; ++j) myL[b0 + j] = lam[j];
+        for (int j = 0; j < b1 - b0; ++j) red[lane * C::SB + j] = lam[j];
+        __syncwarp();
+        if (lane < b1 - b0) {
+          double sum = 0.0;
+#pragma unroll 8
+          for (int j = 0; j < 32; ++j) sum += red[j * C::SB + lane];
+          accT[decltype(BI)::value] += sum;
+        }
+        __syncwarp();
+      } else {
+#pragma unroll
+        for (int j = 0; j < b1 - b0; ++j) myL[b0 + j] = lam[j];
+      }
     });
     __syncwarp();  // every lane done with its M' row before the next chunk's copies land
   }
   // reduce the 32 lane rows (column sums, fixed order) ...
   double* cmp = rowsM;            // NA reduced values
   double* full = rowsM + NA + 1;  // N values (32 * SA >= NA + N + 1)
-  for (int kk = lane; kk < NA; kk += 32) {
-    double acc = 0.0;
-    for (int j = 0; j < 32; ++j) acc += rowsL[j * SL + kk];
-    cmp[kk] = acc;
+  if constexpr (kLR) {
+#pragma unroll
+    for (int q = 0; q < C::kBlocks; ++q)
+      if (q * C::kBlk + lane < NA && lane < C::kBlk) cmp[q * C::kBlk + lane] = accT[q];
+  } else {
+    for (int kk = lane; kk < NA; kk += 32) {
+      double acc = 0.0;
+      for (int j = 0; j < 32; ++j) acc += rowsL[j * SL + kk];
+      cmp[kk] = acc;
+    }
   }
   __syncwarp();
   trace_fill_store<P>(lane, cmp, full, L + (int64_t)t * N);
