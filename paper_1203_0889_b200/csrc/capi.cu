@@ -54,20 +54,19 @@ float ms_between(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-void do_m2l(fmm_ctx* c) {
-  CK(cudaMemsetAsync(c->L.ensure((size_t)c->ncells * c->ncoef), 0, sizeof(double) * c->ncells * c->ncoef,
-                     c->stream));
-  CK(cudaEventRecord(c->ev[EV_M2LK0], c->stream));
-  fmmb::run_m2l(c, c->stream);
-  CK(cudaEventRecord(c->ev[EV_M2LK1], c->stream));
+void do_m2l(fmm_ctx* c, cudaStream_t st) {
+  CK(cudaMemsetAsync(c->L.ensure((size_t)c->ncells * c->ncoef), 0, sizeof(double) * c->ncells * c->ncoef, st));
+  CK(cudaEventRecord(c->ev[EV_M2LK0], st));
+  fmmb::run_m2l(c, st);
+  CK(cudaEventRecord(c->ev[EV_M2LK1], st));
 }
 
-void do_p2p(fmm_ctx* c) {
-  CK(cudaMemsetAsync(c->phi_p2p.ensure(c->N), 0, sizeof(double) * c->N, c->stream));
-  CK(cudaMemsetAsync(c->acc_p2p.ensure(3 * c->N), 0, sizeof(double) * 3 * c->N, c->stream));
-  CK(cudaEventRecord(c->ev[EV_P2PK0], c->stream));
-  fmmb::run_p2p(c, c->stream);
-  CK(cudaEventRecord(c->ev[EV_P2PK1], c->stream));
+void do_p2p(fmm_ctx* c, cudaStream_t st) {
+  CK(cudaMemsetAsync(c->phi_p2p.ensure(c->N), 0, sizeof(double) * c->N, st));
+  CK(cudaMemsetAsync(c->acc_p2p.ensure(3 * c->N), 0, sizeof(double) * 3 * c->N, st));
+  CK(cudaEventRecord(c->ev[EV_P2PK0], st));
+  fmmb::run_p2p(c, st);
+  CK(cudaEventRecord(c->ev[EV_P2PK1], st));
 }
 
 void set_device(fmm_ctx* c) { CK(cudaSetDevice(c->cfg.device)); }
@@ -185,7 +184,7 @@ int fmm_m2l(fmm_ctx* c) {
   if (!c) return FMM_ERR_ARG;
   return guard(c, [&] {
     set_device(c);
-    do_m2l(c);
+    do_m2l(c, c->stream);
     CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
   });
 }
@@ -194,7 +193,7 @@ int fmm_p2p(fmm_ctx* c) {
   if (!c) return FMM_ERR_ARG;
   return guard(c, [&] {
     set_device(c);
-    do_p2p(c);
+    do_p2p(c, c->stream);
     CK(cudaEventRecord(c->ev[EV_P2P1], c->stream));
   });
 }
@@ -243,10 +242,21 @@ int fmm_evaluate(fmm_ctx* c) {
       CK(cudaEventRecord(c->ev[EV_UP1], c->stream));
       CK(cudaEventRecord(c->ev[EV_FORK], c->stream));
     }
-    do_m2l(c);
-    CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
-    do_p2p(c);
-    CK(cudaEventRecord(c->ev[EV_P2P1], c->stream));
+    if (c->overlap >= 2) {
+      // M2L (FP64 pipe) on the high-priority stream and P2P (FP32 pipe) on the low-priority
+      // one, concurrently: P2P CTAs fill what the M2L CTAs leave of each SM
+      CK(cudaStreamWaitEvent(c->stream2, c->ev[EV_FORK], 0));
+      do_p2p(c, c->stream2);
+      CK(cudaEventRecord(c->ev[EV_P2P1], c->stream2));
+      do_m2l(c, c->stream);
+      CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
+      CK(cudaStreamWaitEvent(c->stream, c->ev[EV_P2P1], 0));
+    } else {
+      do_m2l(c, c->stream);
+      CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
+      do_p2p(c, c->stream);
+      CK(cudaEventRecord(c->ev[EV_P2P1], c->stream));
+    }
     fmmb::run_downward(c, c->stream);
     CK(cudaEventRecord(c->ev[EV_DOWN1], c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -256,8 +266,11 @@ int fmm_evaluate(fmm_ctx* c) {
     // overlap: upward ran concurrently with the traversal (BUILD1 -> UP1 on the second stream)
     t.upward_ms = c->overlap ? ms_between(c->ev[EV_BUILD1], c->ev[EV_UP1]) : ms_between(c->ev[EV_TRAV1], c->ev[EV_UP1]);
     t.m2l_ms = ms_between(c->ev[EV_FORK], c->ev[EV_M2L1]);
-    t.p2p_ms = ms_between(c->ev[EV_M2L1], c->ev[EV_P2P1]);
-    t.downward_ms = ms_between(c->ev[EV_P2P1], c->ev[EV_DOWN1]);
+    // overlap 2: P2P ran from the fork alongside M2L; downward starts when both are done
+    t.p2p_ms = c->overlap >= 2 ? ms_between(c->ev[EV_FORK], c->ev[EV_P2P1]) : ms_between(c->ev[EV_M2L1], c->ev[EV_P2P1]);
+    t.downward_ms = c->overlap >= 2 ? ms_between(c->ev[EV_FORK], c->ev[EV_DOWN1]) -
+                                          std::max(t.m2l_ms, t.p2p_ms)
+                                    : ms_between(c->ev[EV_P2P1], c->ev[EV_DOWN1]);
     t.total_ms = ms_between(c->ev[EV_BUILD0], c->ev[EV_DOWN1]);
     t.p2p_kernel_ms = ms_between(c->ev[EV_P2PK0], c->ev[EV_P2PK1]);
     t.m2l_kernel_ms = ms_between(c->ev[EV_M2LK0], c->ev[EV_M2LK1]);
@@ -281,7 +294,7 @@ int fmm_get_stage_trace(fmm_ctx* c, fmm_trace_row* rows, int max_rows, int* n_ro
         {"traversal", 0, EV_BUILD1, EV_TRAV1},
         {"upward", c->overlap ? 1 : 0, c->overlap ? EV_BUILD1 : EV_TRAV1, EV_UP1},
         {"m2l", 0, EV_FORK, EV_M2L1},
-        {"p2p", 0, EV_M2L1, EV_P2P1},
+        {"p2p", c->overlap >= 2 ? 1 : 0, c->overlap >= 2 ? EV_FORK : EV_M2L1, EV_P2P1},
         {"downward", 0, EV_P2P1, EV_DOWN1},
     };
     const int n = static_cast<int>(sizeof(spans) / sizeof(spans[0]));
@@ -294,6 +307,10 @@ int fmm_get_stage_trace(fmm_ctx* c, fmm_trace_row* rows, int max_rows, int* n_ro
       std::strncpy(r.kind, spans[i].kind, sizeof(r.kind) - 1);
       r.start_ns = static_cast<int64_t>(1e6 * ms_between(c->ev[EV_BUILD0], c->ev[spans[i].a]));
       r.end_ns = static_cast<int64_t>(1e6 * ms_between(c->ev[EV_BUILD0], c->ev[spans[i].b]));
+    }
+    if (c->overlap >= 2 && n > 5 && max_rows > 5) {  // downward waits for both M2L and P2P
+      const int64_t m2l_end = static_cast<int64_t>(1e6 * ms_between(c->ev[EV_BUILD0], c->ev[EV_M2L1]));
+      rows[5].start_ns = std::max(rows[5].start_ns, m2l_end);
     }
   });
 }
@@ -582,7 +599,7 @@ int fmm_reset_accumulators(fmm_ctx* c) {
 
 int fmm_set_overlap(fmm_ctx* c, int on) {
   if (!c) return FMM_ERR_ARG;
-  c->overlap = on != 0;
+  c->overlap = on < 0 ? 0 : (on > 2 ? 2 : on);
   return FMM_OK;
 }
 

@@ -120,7 +120,9 @@ struct fmm_ctx {
   fmmb::DBuf<int64_t> shard_bounds;        // device copy of the world + 1 body bounds
   int64_t trav_b0 = 0, trav_b1 = 0;        // traversal target filter [b0, b1)
 
-  bool overlap = true;  // fmm_evaluate: upward pass on stream2 concurrently with the traversal
+  // fmm_evaluate: 1 = upward pass on stream2 concurrently with the traversal; 2 = also M2L and
+  // P2P concurrently (M2L on the high-priority stream)
+  int overlap = 1;
 
   // state
   bool have_bodies = false, have_tree = false, have_lists = false, have_M = false,

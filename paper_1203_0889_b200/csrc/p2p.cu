@@ -17,6 +17,7 @@
 // coincident; kernels.cpp:185-186) are removed by a select. Each tile's FP32 partial sums are
 // folded into FP64 per-target accumulators ("FP64-checked accumulation").
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "context.cuh"
 #include "tma.cuh"
@@ -1159,12 +1160,23 @@ void run_p2p(fmm_ctx* c, cudaStream_t s) {
 #define FMM_P2P_WS 1
 #endif
       if (FMM_P2P_WS) {
+        // optional dynamic shared-memory pad: caps the P2P CTAs per SM (room for concurrent M2L)
+        static const int pad = [] {
+          const char* e = std::getenv("FMM_P2P_PAD_KB");
+          return e ? std::atoi(e) * 1024 : 0;
+        }();
+        static bool attr = false;
+        if (!attr && pad > 0) {
+          CK(cudaFuncSetAttribute(k_p2p_fp32_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad));
+          CK(cudaFuncSetAttribute(k_p2p_fp32_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad));
+          attr = true;
+        }
         if (wa)
-          k_p2p_fp32_ws<true><<<(unsigned)c->n_p2p_items, kWsThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p,
-                                                                              phi, acc, c->p2p_partial.p);
+          k_p2p_fp32_ws<true><<<(unsigned)c->n_p2p_items, kWsThreads, pad, s>>>(items, ent, c->bodyf.p, c->bodyl.p,
+                                                                                phi, acc, c->p2p_partial.p);
         else
-          k_p2p_fp32_ws<false><<<(unsigned)c->n_p2p_items, kWsThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p,
-                                                                               phi, acc, c->p2p_partial.p);
+          k_p2p_fp32_ws<false><<<(unsigned)c->n_p2p_items, kWsThreads, pad, s>>>(items, ent, c->bodyf.p, c->bodyl.p,
+                                                                                 phi, acc, c->p2p_partial.p);
       } else if (wa) {
         k_p2p_fp32<true><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p, phi,
                                                                        acc, c->p2p_partial.p);

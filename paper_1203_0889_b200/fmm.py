@@ -150,7 +150,10 @@ class Context:
     def evaluate(self): self._c(self.lib.fmm_evaluate(self.h))
     def synchronize(self): self._c(self.lib.fmm_synchronize(self.h))
     def reset_accumulators(self): self._c(self.lib.fmm_reset_accumulators(self.h))
-    def set_overlap(self, on: bool): self._c(self.lib.fmm_set_overlap(self.h, int(on)))
+    def set_overlap(self, on):
+        """0 = serial stages, 1 = upward concurrent with the traversal (default), 2 = also M2L
+        concurrent with P2P."""
+        self._c(self.lib.fmm_set_overlap(self.h, int(on)))
 
     def set_mutual(self, on: bool):
         self._c(self.lib.fmm_set_mutual(self.h, int(on)))

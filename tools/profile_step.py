@@ -16,6 +16,7 @@ ap.add_argument("--precision", default="fp32")
 ap.add_argument("--n", type=int, default=0, help="override the body count")
 ap.add_argument("--serial", action="store_true", help="stages serialised on one stream")
 ap.add_argument("--overlap", action="store_true", help="upward pass concurrent with the traversal")
+ap.add_argument("--overlap-level", type=int, default=-1, help="fmm_set_overlap level (0, 1, 2)")
 a = ap.parse_args()
 gen, n, p, n_crit, theta = CONFIGS[a.config]
 if a.n:
@@ -26,11 +27,18 @@ ctx.set_bodies(b)
 if a.serial:
     ctx.set_overlap(False)
 if a.overlap:
-    ctx.set_overlap(True)
-for _ in range(a.warmup + a.steps):
+    ctx.set_overlap(1)
+if a.overlap_level >= 0:
+    ctx.set_overlap(a.overlap_level)
+for _ in range(a.warmup):
     ctx.evaluate()
-t = ctx.stage_times()
-print({k: round(getattr(t, k), 3) for k, _ in t._fields_})
+acc = {}
+for _ in range(a.steps):  # stage times averaged over the timed steps
+    ctx.evaluate()
+    t = ctx.stage_times()
+    for k, _ in t._fields_:
+        acc[k] = acc.get(k, 0.0) + getattr(t, k) / a.steps
+print({k: round(v, 3) for k, v in acc.items()})
 info = ctx.tree_info()
 print("cells", info.ncells, "leaves", info.nleaves, "depth", info.depth, "m2l", info.n_m2l,
       "p2p", info.n_p2p, "pairs", info.p2p_body_pairs)
