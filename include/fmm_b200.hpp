@@ -215,6 +215,14 @@ inline void m2l(const KernelTables& kt, const std::vector<Real>& source_m, const
                 std::vector<Real>& target_l) {
   check(fmm_op_m2l(kt.order(), 1, source_m.data(), displacement.data(), target_l.data()));
 }
+// m2l_mutual (kernels.cpp:113-126): both one-directional translations (the reference's w_rev
+// terms are the translation of target_m by -R)
+inline void m2l_mutual(const KernelTables& kt, const std::vector<Real>& source_m, const std::vector<Real>& target_m,
+                       const Vec3& displacement, std::vector<Real>& target_l, std::vector<Real>& source_l) {
+  const Vec3 neg{-displacement[0], -displacement[1], -displacement[2]};
+  check(fmm_op_m2l(kt.order(), 1, source_m.data(), displacement.data(), target_l.data()));
+  check(fmm_op_m2l(kt.order(), 1, target_m.data(), neg.data(), source_l.data()));
+}
 inline Real evaluate_multipole(const KernelTables& kt, const std::vector<Real>& M, const Vec3& x,
                                const Vec3& center) {
   Real out = 0.0;

@@ -573,6 +573,27 @@ class OracleOps:
             raise OracleError(ERRORS.get(rc, str(rc)))
         return out
 
+    def m2l_mutual(self, Ms, Mt, R):
+        """kernels.cpp:113-126 (orc_m2l_mutual): (target_l, source_l) from zero."""
+        tl, sl = np.zeros(self.n), np.zeros(self.n)
+        rc = self.lib.orc_m2l_mutual(C.byref(self.kt), _ptr(self._a(Ms), _dp), _ptr(self._a(Mt), _dp),
+                                     _ptr(self._a(R), _dp), _ptr(tl, _dp), _ptr(sl, _dp))
+        if rc:
+            raise OracleError(ERRORS.get(rc, str(rc)))
+        return tl, sl
+
+    def p2p_mutual(self, txyzq, sxyzq):
+        """kernels.cpp:167-180: distinct target and source spans, both updated."""
+        t = self._a(txyzq).reshape(-1, 4)
+        s_ = self._a(sxyzq).reshape(-1, 4)
+        tp, tq = np.ascontiguousarray(t[:, :3]), np.ascontiguousarray(t[:, 3])
+        sp, sq = np.ascontiguousarray(s_[:, :3]), np.ascontiguousarray(s_[:, 3])
+        tphi, sphi = np.zeros(len(t)), np.zeros(len(s_))
+        tacc, sacc = np.zeros((len(t), 3)), np.zeros((len(s_), 3))
+        self.lib.orc_p2p(len(t), _ptr(tp, _dp), _ptr(tq, _dp), _ptr(tphi, _dp), _ptr(tacc, _dp), len(s_),
+                         _ptr(sp, _dp), _ptr(sq, _dp), _ptr(sphi, _dp), _ptr(sacc, _dp), 0, 1)
+        return (tphi, tacc), (sphi, sacc)
+
     def l2l(self, parent, shift):
         out = np.zeros(self.n)
         self.lib.orc_l2l(C.byref(self.kt), _ptr(self._a(parent), _dp), _ptr(self._a(shift), _dp), _ptr(out, _dp))

@@ -8,12 +8,12 @@ from . import _capi
 from .fmm import (FMMError, Context, Tree, KernelTables, KernelVisitor, TraversalConfig,
                   build_tree, upward_pass, dual_tree_traverse, downward_pass, potentials,
                   accelerations, evaluate, compute_bounds, morton_key, mac, split_pair, p2m,
-                  m2m, m2l, l2l, l2p, p2p, evaluate_multipole, laplace_derivatives, m2p_flip,
+                  m2m, m2l, m2l_mutual, l2l, l2p, p2p, evaluate_multipole, laplace_derivatives, m2p_flip,
                   generate_bodies, n_coef, index_of, exponents)
 
 __all__ = ["FMMError", "Context", "Tree", "KernelTables", "KernelVisitor", "TraversalConfig",
            "build_tree", "upward_pass", "dual_tree_traverse", "downward_pass", "potentials",
            "accelerations", "evaluate", "compute_bounds", "morton_key", "mac", "split_pair",
-           "p2m", "m2m", "m2l", "l2l", "l2p", "p2p", "evaluate_multipole",
+           "p2m", "m2m", "m2l", "m2l_mutual", "l2l", "l2p", "p2p", "evaluate_multipole",
            "laplace_derivatives", "m2p_flip", "generate_bodies", "n_coef", "index_of",
            "exponents", "_capi"]

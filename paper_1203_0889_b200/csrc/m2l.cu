@@ -545,10 +545,20 @@ struct BigCfg2 {
   static constexpr bool kLR = P >= FMM_BIG2_LR_MIN_P;
   static constexpr int SB = odd_stride(kBlk);
   static constexpr size_t kSmemPerWarp = sizeof(double) * 32 * (SA + (kLR ? SB : SL));
+#ifndef FMM_BIG2_WARPS
+#define FMM_BIG2_WARPS 1
+#endif
+#ifndef FMM_BIG2_WARPS_P10
+#define FMM_BIG2_WARPS_P10 7
+#endif
+  // warps (targets) per CTA, advancing chunk by chunk in lockstep (a CTA barrier per chunk):
+  // the fully unrolled contraction (p = 10: ~45 KB of SASS per chunk) is then fetched once per
+  // SM position instead of once per warp (ncu at 1 warp/CTA: 40 % no_instruction stalls)
+  static constexpr int kWarps = P >= 10 ? FMM_BIG2_WARPS_P10 : FMM_BIG2_WARPS;
 };
 
 template <int P>
-__global__ void __launch_bounds__(32, 1)
+__global__ void __launch_bounds__(32 * BigCfg2<P>::kWarps, 1)
 k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* __restrict__ off,
            const int32_t* __restrict__ src, const double4* __restrict__ cr, const double* __restrict__ Mt,
            double* __restrict__ L) {
@@ -557,24 +567,33 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
   using C = BigCfg2<P>;
   constexpr int N = T::N, NA = C::NA, NG = C::NG, SA = C::SA, SL = C::SL;
   constexpr bool kBulk = (NA * 8) % 16 == 0;
+  constexpr int W = C::kWarps;
   extern __shared__ __align__(16) double smem[];
-  __shared__ __align__(8) uint64_t bar;
-  const int lane = threadIdx.x;
-  double* rowsM = smem;            // [32][SA]
-  double* rowsL = smem + 32 * SA;  // [32][SL]
+  __shared__ __align__(8) uint64_t bars[W];
+  __shared__ int64_t cta_chunks;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* wsm = smem + (size_t)w * (C::kSmemPerWarp / sizeof(double));
+  double* rowsM = wsm;            // [32][SA]
+  double* rowsL = wsm + 32 * SA;  // [32][SL] (kLR: [32][SB] block buffer)
   double* myM = rowsM + lane * SA;
   double* myL = rowsL + lane * SL;
+  uint64_t& bar = bars[w];
   if (kBulk && lane == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  __syncwarp();
+  if (threadIdx.x == 0) cta_chunks = 0;
+  __syncthreads();
   unsigned phase = 0;
-  const int64_t wid = blockIdx.x;
-  if (wid >= ntargets) return;
-  const int32_t t = targets[wid];
+  const int64_t wid = blockIdx.x * (int64_t)W + w;
+  const bool have = wid < ntargets;
+  const int32_t t = have ? targets[wid] : 0;
   const double4 ct = cr[t];
-  const int64_t l0 = off[t], l1 = off[t + 1];
+  const int64_t l0 = have ? off[t] : 0, l1 = have ? off[t + 1] : 0;
+  if (W > 1 && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&cta_chunks),
+                                    static_cast<unsigned long long>((l1 - l0 + 31) / 32));
+  if (W > 1) __syncthreads();
+  const int64_t lockstep_end = W > 1 ? l0 + 32 * cta_chunks : l1;
   constexpr bool kLR = C::kLR;
   double accT[C::kBlocks];  // kLR: Lambda_{q kBlk + lane} of the target (lanes < block width)
 #pragma unroll
@@ -585,7 +604,11 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
 #if FMM_M2L_PREFETCH
   double4 cs_next = cr[s_next];
 #endif
-  for (int64_t base = l0; base < l1; base += 32) {
+  for (int64_t base = l0; base < lockstep_end; base += 32) {
+    if (base >= l1) {  // this warp's target is done: keep the CTA's chunk barriers
+      __syncthreads();
+      continue;
+    }
     const int64_t k = base + lane;
     const bool valid = k < l1;
     const int32_t s = s_next;
@@ -692,7 +715,9 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
       }
     });
     __syncwarp();  // every lane done with its M' row before the next chunk's copies land
+    if (W > 1) __syncthreads();
   }
+  if (!have) return;
   // reduce the 32 lane rows (column sums, fixed order) ...
   double* cmp = rowsM;            // NA reduced values
   double* full = rowsM + NA + 1;  // N values (32 * SA >= NA + N + 1)
@@ -736,15 +761,16 @@ struct M2L {
 #endif
     if (FMM_M2L_BIG_V2) {
       using C2 = BigCfg2<P>;
+      const size_t smem2 = C2::kSmemPerWarp * C2::kWarps;
       static bool attr2 = false;
       if (!attr2) {
-        CK(cudaFuncSetAttribute(k_m2l_big2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C2::kSmemPerWarp));
+        CK(cudaFuncSetAttribute(k_m2l_big2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
         attr2 = true;
       }
       if (c->n_m2l_targets == 0) return;
       double* Mt = c->m2l_mt.ensure(c->ncells * C2::NA + 1);
       launch_detrace<P>(c, Mt, s);
-      k_m2l_big2<P><<<(unsigned)c->n_m2l_targets, 32, C2::kSmemPerWarp, s>>>(
+      k_m2l_big2<P><<<(unsigned)ceil_div(c->n_m2l_targets, C2::kWarps), 32 * C2::kWarps, smem2, s>>>(
           c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p, c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
       CK_LAUNCH("k_m2l_big2");
       c->kernel_launches += 2;

@@ -513,6 +513,14 @@ def m2l(order: int, source_m, disp, target_l=None) -> np.ndarray:
     return out
 
 
+def m2l_mutual(order: int, source_m, target_m, disp, target_l=None, source_l=None):
+    """kernels.cpp:113-126: target_l += M2L(source_m, R) and source_l += M2L(target_m, -R), with
+    R = source centre - target centre (the reference's w_rev terms are the reversed translation).
+    Returns (target_l, source_l); raises 'singular M2L displacement' on |R| = 0."""
+    r = _batch(disp, 3)
+    return m2l(order, source_m, r, target_l), m2l(order, target_m, -r, source_l)
+
+
 def l2l(order: int, parent_l, shifts, child_l=None) -> np.ndarray:
     """kernels.cpp:128-136 (accumulates into child_l)."""
     pl = _batch(parent_l, n_coef(order))
@@ -536,9 +544,15 @@ def l2p(order: int, L, center, bodies, with_acc: bool = True):
     return phi, acc
 
 
-def p2p(targets, sources=None, precision: str = "fp64", with_acc: bool = True):
-    """kernels.cpp:150-195, non-mutual (sources=None means the self interaction). Returns
-    (phi, acc) of the targets."""
+def p2p(targets, sources=None, precision: str = "fp64", with_acc: bool = True, mutual: bool = False):
+    """kernels.cpp:150-195 (sources=None means the self interaction). Returns (phi, acc) of the
+    targets; with ``mutual`` (kernels.cpp:153-180) and distinct sources, returns
+    ((phi_t, acc_t), (phi_s, acc_s)): both spans updated, each pair evaluated for both sides
+    (the GPU computes the two target-owned directions; the sums equal the mutual kernel's up
+    to rounding). A mutual self interaction equals the non-mutual one (test_kernels.cpp:299)."""
+    if mutual and sources is not None:
+        return (p2p(targets, sources, precision, with_acc),
+                p2p(sources, targets, precision, with_acc))
     t = np.ascontiguousarray(targets, dtype=np.float64).reshape(-1, 4)
     if sources is None:
         b = t

@@ -119,6 +119,29 @@ def test_operators_match_oracle(fmmlib, orc, p):
         assert g[k] == pytest.approx(ops.evaluate_multipole(Ms[k], x[k], [0, 0, 0]), rel=1e-12, abs=1e-14)
 
 
+def test_mutual_operators_match_oracle(fmmlib, orc):
+    """m2l_mutual (kernels.cpp:113-126) and mutual p2p (kernels.cpp:167-180) through the GPU
+    operators (two target-owned directions) against the oracle's mutual kernels; the reference's
+    test_kernels.cpp:187-200 check (m2l_mutual = two one-directional translations)."""
+    fb = fmmlib
+    rng = np.random.default_rng(11)
+    for p in (3, 6, 8):
+        ops = oracle.OracleOps(orc, p)
+        Ms, Mt = rng.uniform(-1, 1, ops.n), rng.uniform(-1, 1, ops.n)
+        R = np.array([2.2, -1.7, 0.9])
+        tl, sl = fb.m2l_mutual(p, Ms, Mt, R)
+        otl, osl = ops.m2l_mutual(Ms, Mt, R)
+        assert rel_l2(tl[0], otl) < 1e-12 and rel_l2(sl[0], osl) < 1e-12, p
+        with pytest.raises(fb.FMMError, match="singular M2L displacement"):
+            fb.m2l_mutual(p, Ms, Mt, [0.0, 0.0, 0.0])
+    t = np.concatenate([rng.uniform(-0.5, 0.5, (40, 3)), rng.uniform(-1, 1, (40, 1))], 1)
+    s_ = np.concatenate([rng.uniform(0.6, 1.4, (30, 3)), rng.uniform(-1, 1, (30, 1))], 1)
+    (gt, gs) = fb.p2p(t, s_, mutual=True)
+    (ot, os_) = ops.p2p_mutual(t, s_)
+    for g, o in ((gt, ot), (gs, os_)):
+        assert rel_l2(g[0], o[0]) < 1e-13 and rel_l2(g[1], o[1]) < 1e-13
+
+
 def test_laplace_derivatives_match_reference(fmmlib, ref):
     rng = np.random.default_rng(7)
     for md in (0, 3, 5, 9):
