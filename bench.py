@@ -384,7 +384,7 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f)["k_p2p_fp32"]["dram_bytes_per_launch"]
+            traffic = json.load(f)["k_p2p_fp32_ws"]["dram_bytes_per_launch"]
     except Exception:
         traffic = None
 
@@ -457,7 +457,7 @@ def main():
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                          "frac": achieved / fp32_peak, "traffic": traffic,
                          "traffic_unit": "bytes per launch (dram read + write, ncu --set full, C2)",
-                         "kernel": "k_p2p_fp32", "flops_per_unit": FLOPS_PER_PAIR,
+                         "kernel": "k_p2p_fp32_ws", "flops_per_unit": FLOPS_PER_PAIR,
                          "timing": "CUDA events around the P2P launch in the timed steps (no other kernel runs concurrently with it), L2 flushed",
                          "peak_source": f"derived: {sms} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz "
                                         "(sm_max_mhz of MEASURED_PEAKS.json; FFMA microbenchmark "
