@@ -104,6 +104,15 @@ int fmm_m2l(fmm_ctx* ctx);          /* KernelVisitor::m2l_pair over the M2L list
 int fmm_p2p(fmm_ctx* ctx);          /* KernelVisitor::p2p_pair over the P2P list */
 int fmm_downward(fmm_ctx* ctx);     /* downward_pass       traversal.cpp:52-63 (+ output) */
 int fmm_evaluate(fmm_ctx* ctx);     /* all of the above */
+/* Time stepping with tree reuse (extension; the reference rebuilds every run; the
+ * paper's motivating use). fmm_update_bodies replaces the positions/charges of
+ * the same N bodies (input order) and keeps the tree and lists; fmm_evaluate_reuse then checks on
+ * the device that every body still lies in its previous leaf's cube and, if so, re-gathers the
+ * bodies in the kept tree order and runs upward / M2L / P2P / downward on the kept lists
+ * (*reused = 1): the exact FMM of the kept tree (cell geometry, MAC decisions and lists depend
+ * only on the cells). Otherwise it runs the full fmm_evaluate (*reused = 0). */
+int fmm_update_bodies(fmm_ctx* ctx, const double* xyzq, int64_t n);
+int fmm_evaluate_reuse(fmm_ctx* ctx, int* reused);
 int fmm_synchronize(fmm_ctx* ctx);
 /* 1 (default): fmm_evaluate runs the upward pass (P2M/M2M, needs only the tree) on a second
  * stream concurrently with the dual tree traversal and its list building; M2L joins both.

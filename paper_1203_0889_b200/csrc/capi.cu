@@ -216,27 +216,32 @@ int fmm_downward(fmm_ctx* c) {
   });
 }
 
-int fmm_evaluate(fmm_ctx* c) {
-  if (!c) return FMM_ERR_ARG;
-  return guard(c, [&] {
-    if (c->world > 1) fail(FMM_ERR_STATE, "evaluate: sharded contexts run the staged sequence (see fmm_b200.h)");
-    set_device(c);
-    c->kernel_launches = 0;
-    CK(cudaEventRecord(c->ev[EV_BUILD0], c->stream));
-    fmmb::build_tree(c);
+// The step of fmm_evaluate; with `reuse` (a time step on the kept tree, the bodies already
+// re-gathered by refit_bodies) the build is replaced by the refit and the traversal by the
+// rebuild of the FP32 P2P entries (their near test depends on the bodies).
+void evaluate_impl(fmm_ctx* c, bool reuse) {
+  {
+    if (!reuse) {
+      CK(cudaEventRecord(c->ev[EV_BUILD0], c->stream));
+      fmmb::build_tree(c);
+    }
     CK(cudaEventRecord(c->ev[EV_BUILD1], c->stream));
+    auto lists = [&] {
+      if (!reuse) fmmb::traverse(c);
+      else if (c->cfg.precision == FMM_PREC_FP32_P2P) fmmb::build_p2p_entries(c);
+    };
     if (c->overlap) {
       // The upward pass needs only the tree: it runs on the second stream while the traversal
       // (and its host round trips) proceeds on the first; M2L joins both.
       CK(cudaStreamWaitEvent(c->stream2, c->ev[EV_BUILD1], 0));
       fmmb::run_upward(c, c->stream2);
       CK(cudaEventRecord(c->ev[EV_UP1], c->stream2));
-      fmmb::traverse(c);
+      lists();
       CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
       CK(cudaStreamWaitEvent(c->stream, c->ev[EV_UP1], 0));
       CK(cudaEventRecord(c->ev[EV_FORK], c->stream));
     } else {
-      fmmb::traverse(c);
+      lists();
       CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
       fmmb::run_upward(c, c->stream);
       CK(cudaEventRecord(c->ev[EV_UP1], c->stream));
@@ -277,7 +282,7 @@ int fmm_evaluate(fmm_ctx* c) {
     t.p2p_launches = 1;
     t.m2l_launches = 1;
     t.kernel_launches = c->kernel_launches;
-  });
+  }
 }
 
 int fmm_get_stage_trace(fmm_ctx* c, fmm_trace_row* rows, int max_rows, int* n_rows) {
@@ -312,6 +317,49 @@ int fmm_get_stage_trace(fmm_ctx* c, fmm_trace_row* rows, int max_rows, int* n_ro
       const int64_t m2l_end = static_cast<int64_t>(1e6 * ms_between(c->ev[EV_BUILD0], c->ev[EV_M2L1]));
       rows[5].start_ns = std::max(rows[5].start_ns, m2l_end);
     }
+  });
+}
+
+int fmm_evaluate(fmm_ctx* c) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (c->world > 1) fail(FMM_ERR_STATE, "evaluate: sharded contexts run the staged sequence (see fmm_b200.h)");
+    set_device(c);
+    c->kernel_launches = 0;
+    evaluate_impl(c, false);
+  });
+}
+
+int fmm_update_bodies(fmm_ctx* c, const double* xyzq, int64_t n) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (n <= 0) fail(FMM_ERR_EMPTY_INPUT, "empty input");
+    if (!xyzq) fail(FMM_ERR_ARG, "null bodies");
+    set_device(c);
+    const bool keep = c->have_tree && c->have_lists && n == c->N;
+    c->N = n;
+    c->kernel_launches = 0;
+    CK(cudaMemcpyAsync(c->xyzq_in.ensure(n), xyzq, n * sizeof(double4), cudaMemcpyHostToDevice, c->stream));
+    c->have_bodies = true;
+    c->have_M = c->have_L = c->have_out = false;
+    if (!keep) c->have_tree = c->have_lists = false;
+  });
+}
+
+int fmm_evaluate_reuse(fmm_ctx* c, int* reused) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_bodies) fail(FMM_ERR_STATE, "evaluate_reuse: no bodies");
+    if (c->world > 1) fail(FMM_ERR_UNSUPPORTED, "evaluate_reuse: sharded contexts rebuild every step");
+    set_device(c);
+    c->kernel_launches = 0;
+    bool ok = false;
+    if (c->have_tree && c->have_lists) {
+      CK(cudaEventRecord(c->ev[EV_BUILD0], c->stream));
+      ok = fmmb::refit_bodies(c);
+    }
+    if (reused) *reused = ok ? 1 : 0;
+    evaluate_impl(c, ok);
   });
 }
 

@@ -140,6 +140,7 @@ namespace fmmb {
 void build_tree(fmm_ctx* c);
 void unpermute_results(fmm_ctx* c, double* phi_in, double* acc_in);  // tree -> input order
 void gather_bodies(fmm_ctx* c);  // bodies/bodyf/leaf_of_body from perm + tree
+bool refit_bodies(fmm_ctx* c);   // tree reuse: false if a body left its leaf cube, else re-gather
 // traverse.cu
 void traverse(fmm_ctx* c);
 void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p);  // lists from c->m2l_keys/p2p_keys
@@ -155,6 +156,7 @@ void plan_partition_host(int64_t ncells, const int32_t* bb, const int32_t* be, c
                          const double* cell_cost, int world, int64_t* bounds, int32_t* owner);
 // p2p.cu
 void build_p2p_worklist(fmm_ctx* c);
+void build_p2p_entries(fmm_ctx* c);  // FP32 entries (near test on the current bodies)
 void run_p2p(fmm_ctx* c, cudaStream_t s);
 // expansions.cu
 void run_upward(fmm_ctx* c, cudaStream_t s, int mode = 0);  // 0 all, 1 own cells, 2 shared cells

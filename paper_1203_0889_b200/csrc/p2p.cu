@@ -1055,6 +1055,33 @@ void exclusive_scan_i32(fmm_ctx* c, const int32_t* in, int32_t* out, int64_t n) 
 
 }  // namespace
 
+// FP32 P2P list entries (self / near / far order, FP32 hi + lo shifts): depend on the lists and,
+// through the near test, on the bodies' tight leaf boxes (rebuilt by a tree-reuse step)
+void build_p2p_entries(fmm_ctx* c) {
+  cudaStream_t s = c->stream;
+  const int64_t ne = c->n_p2p;
+  P2PEnt* ent = reinterpret_cast<P2PEnt*>(c->p2p_ent.ensure(2 * (ne + 1)));
+  double4* blo = c->leaf_lo.ensure(c->ncells);
+  double4* bhi = c->leaf_hi.ensure(c->ncells);
+  k_leaf_boxes<<<ceil_div(c->nleaves * 32, 256), 256, 0, s>>>(c->leaves.p, c->nleaves, c->c_body_begin.p,
+                                                             c->c_body_end.p, c->bodies.p, blo, bhi);
+  int64_t* cls = c->ent_cls.ensure(ne + 1);
+  int64_t* epre = c->ent_pre.ensure(ne + 1);
+  int32_t* spos = c->self_pos.ensure(c->ncells);
+  CK(cudaMemsetAsync(spos, 0xff, sizeof(int32_t) * c->ncells, s));
+  k_ent_class<<<ceil_div(ne + 1, 256), 256, 0, s>>>(c->p2p_tgt.p, c->p2p_src.p, ne, c->c_cr.p, blo, bhi, cls, spos);
+  {
+    size_t sb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, cls, epre, (int)(ne + 1), s));
+    CK(cub::DeviceScan::ExclusiveSum(temp_storage(c, sb), sb, cls, epre, (int)(ne + 1), s));
+  }
+  if (ne > 0)
+    k_ent_write<<<ceil_div(ne, 256), 256, 0, s>>>(c->p2p_tgt.p, c->p2p_src.p, ne, c->p2p_off.p, cls, epre, spos,
+                                                  c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, ent);
+  CK_LAUNCH("k_ent_write");
+  c->kernel_launches += 5;
+}
+
 void build_p2p_worklist(fmm_ctx* c) {
   cudaStream_t s = c->stream;
   const int64_t nl = c->nwl, ne = c->n_p2p;
@@ -1109,28 +1136,7 @@ void build_p2p_worklist(fmm_ctx* c) {
                                                    c->c_body_end.p, sum_ns, nitems, item_off, red_off, part_off,
                                                    items_raw, costs, red);
   CK_LAUNCH("k_write_items");
-  if (c->cfg.precision == FMM_PREC_FP32_P2P) {
-    P2PEnt* ent = reinterpret_cast<P2PEnt*>(c->p2p_ent.ensure(2 * (ne + 1)));
-    double4* blo = c->leaf_lo.ensure(c->ncells);
-    double4* bhi = c->leaf_hi.ensure(c->ncells);
-    k_leaf_boxes<<<ceil_div(c->nleaves * 32, 256), 256, 0, s>>>(c->leaves.p, c->nleaves, c->c_body_begin.p,
-                                                               c->c_body_end.p, c->bodies.p, blo, bhi);
-    int64_t* cls = c->ent_cls.ensure(ne + 1);
-    int64_t* epre = c->ent_pre.ensure(ne + 1);
-    int32_t* spos = c->self_pos.ensure(c->ncells);
-    CK(cudaMemsetAsync(spos, 0xff, sizeof(int32_t) * c->ncells, s));
-    k_ent_class<<<ceil_div(ne + 1, 256), 256, 0, s>>>(c->p2p_tgt.p, c->p2p_src.p, ne, c->c_cr.p, blo, bhi, cls, spos);
-    {
-      size_t sb = 0;
-      CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, cls, epre, (int)(ne + 1), s));
-      CK(cub::DeviceScan::ExclusiveSum(temp_storage(c, sb), sb, cls, epre, (int)(ne + 1), s));
-    }
-    k_ent_write<<<ceil_div(ne, 256), 256, 0, s>>>(c->p2p_tgt.p, c->p2p_src.p, ne, c->p2p_off.p, cls, epre, spos,
-                                                  c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, ent);
-    CK_LAUNCH("k_ent_write");
-    c->kernel_launches += 3;
-    c->kernel_launches += 2;
-  }
+  if (c->cfg.precision == FMM_PREC_FP32_P2P) build_p2p_entries(c);
   // cost-sorted (descending, stable) work list: the longest items launch first
   int32_t* ord_in = c->i32_c.ensure(2 * (nitem + 1));
   int32_t* ord_out = ord_in + (nitem + 1);

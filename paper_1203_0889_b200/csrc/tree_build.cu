@@ -534,6 +534,37 @@ void unpermute_results(fmm_ctx* c, double* phi_in, double* acc_in) {
   CK_LAUNCH("k_unpermute");
 }
 
+namespace {
+// tree reuse: every body (new position, kept permutation) must lie in its leaf's closed cube
+__global__ void k_check_inside(const double4* __restrict__ in, const int32_t* __restrict__ perm,
+                               const int32_t* __restrict__ leaf_of_body, const double4* __restrict__ cr, int64_t n,
+                               int* __restrict__ outside) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 b = in[perm[i]], c = cr[leaf_of_body[i]];
+  if (!(fabs(b.x - c.x) <= c.w && fabs(b.y - c.y) <= c.w && fabs(b.z - c.z) <= c.w)) *outside = 1;
+}
+}  // namespace
+
+bool refit_bodies(fmm_ctx* c) {
+  cudaStream_t s = c->stream;
+  const int64_t n = c->N;
+  int* flag = reinterpret_cast<int*>(c->d_counters.p + 8);
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), s));
+  k_check_inside<<<ceil_div(n, 256), 256, 0, s>>>(c->xyzq_in.p, c->perm.p, c->leaf_of_body.p, c->c_cr.p, n, flag);
+  CK_LAUNCH("k_check_inside");
+  int* h = reinterpret_cast<int*>(c->hpin + 8);
+  CK(cudaMemcpyAsync(h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  c->kernel_launches += 1;
+  if (*h) return false;
+  k_gather<<<ceil_div(n, 256), 256, 0, s>>>(c->xyzq_in.p, c->perm.p, c->leaf_of_body.p, c->c_cr.p, n, c->bodies.p,
+                                            c->bodyf.p, c->bodyl.p);
+  CK_LAUNCH("k_gather");
+  c->kernel_launches += 1;
+  return true;
+}
+
 void gather_bodies(fmm_ctx* c) {
   cudaStream_t s = c->stream;
   const int64_t n = c->N;

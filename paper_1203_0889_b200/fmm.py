@@ -148,6 +148,19 @@ class Context:
     def p2p(self): self._c(self.lib.fmm_p2p(self.h))
     def downward(self): self._c(self.lib.fmm_downward(self.h))
     def evaluate(self): self._c(self.lib.fmm_evaluate(self.h))
+
+    def update_bodies(self, xyzq: np.ndarray) -> None:
+        """New positions/charges of the same bodies (input order); keeps the tree and lists."""
+        xyzq = np.ascontiguousarray(xyzq, dtype=np.float64).reshape(-1, 4)
+        self.n = len(xyzq)
+        self._c(self.lib.fmm_update_bodies(self.h, _ptr(xyzq, _dp), len(xyzq)))
+
+    def evaluate_reuse(self) -> bool:
+        """Time step on the kept tree when every body stayed in its leaf cube (returns True),
+        else a full rebuild (False). See fmm_b200.h."""
+        r = C.c_int(0)
+        self._c(self.lib.fmm_evaluate_reuse(self.h, C.byref(r)))
+        return bool(r.value)
     def synchronize(self): self._c(self.lib.fmm_synchronize(self.h))
     def reset_accumulators(self): self._c(self.lib.fmm_reset_accumulators(self.h))
     def set_overlap(self, on):

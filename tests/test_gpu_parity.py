@@ -309,6 +309,57 @@ def test_pipeline_vs_oracle(fmmlib, orc, case):
         assert info.p2p_body_pairs == int((nb[op[:, 0]] * nb[op[:, 1]]).sum())
 
 
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_time_step_tree_reuse(fmmlib, orc, precision):
+    """fmm_update_bodies + fmm_evaluate_reuse (time stepping on the kept tree): bodies moved
+    inside their leaf cubes reuse the tree and lists, and the result is bit-identical to the
+    same tree loaded and evaluated stage by stage (fmm_load_tree) and within FMM accuracy of a
+    fresh build; a body leaving its leaf falls back to the full rebuild (bit-identical to a
+    fresh context)."""
+    fb = fmmlib
+    b0 = fb.generate_bodies(3, 20000, 5)
+    ctx = fb.Context(order=6, n_crit=64, theta=0.5, precision=precision)
+    ctx.set_bodies(b0)
+    ctx.evaluate()
+    cells, perm = ctx.cells(), ctx.permutation()
+    # move every body toward its leaf centre (stays inside the cube) and change the charges
+    leaf = np.zeros(len(b0), np.int64)
+    for c in np.nonzero(cells["child_count"] == 0)[0]:
+        leaf[cells["body_begin"][c]:cells["body_end"][c]] = c
+    b1 = b0.copy()
+    ctr = cells["center"][leaf]
+    b1[perm, :3] = ctr + 0.9 * (b0[perm, :3] - ctr)
+    b1[:, 3] = b0[:, 3] * np.random.default_rng(1).uniform(0.5, 1.5, len(b0))
+    ctx.update_bodies(b1)
+    assert ctx.evaluate_reuse()
+    phi, acc = ctx.results("input")
+    ref = fb.Context(order=6, n_crit=64, theta=0.5, precision=precision)
+    ref.set_bodies(b1)
+    ref.load_tree(cells, perm)
+    ref.traverse()
+    ref.upward()
+    ref.m2l()
+    ref.p2p()
+    ref.downward()
+    rphi, racc = ref.results("input")
+    assert np.array_equal(phi, rphi) and np.array_equal(acc, racc)
+    fresh = fb.Context(order=6, n_crit=64, theta=0.5, precision=precision)
+    fresh.set_bodies(b1)
+    fresh.evaluate()
+    fphi, facc = fresh.results("input")
+    assert rel_l2(phi, fphi) < 1e-4 and rel_l2(acc, facc) < 1e-3
+    # a body leaves its leaf: full rebuild
+    b2 = b1.copy()
+    b2[0, :3] += 0.5
+    ctx.update_bodies(b2)
+    assert not ctx.evaluate_reuse()
+    fresh.set_bodies(b2)
+    fresh.evaluate()
+    assert np.array_equal(ctx.results("input")[0], fresh.results("input")[0])
+    for x in (ctx, ref, fresh):
+        x.close()
+
+
 def test_tree_reuse_across_distributions(fmmlib, orc):
     """One context, successive body sets of growing depth: the partial-digit sort keyed on the
     previous depth must fall back to the full sort (and the level batches must continue) so that
