@@ -109,6 +109,48 @@ __global__ void k_mixed(float* out, const float* ab) {
   if (s == 12345.f) out[0] = s;
 }
 
+// operand-form variants of the packed ops used by the P2P pair (register-read pressure)
+__global__ void k_fadd2_bc(float* out, const float* ab) {  // pair + broadcast scalar
+  float2 x[CHAINS];
+  float c[CHAINS];
+  for (int i = 0; i < CHAINS; ++i) { x[i] = make_float2(threadIdx.x * 1e-3f + i, i); c[i] = ab[4 + i] * 1e-6f; }
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < CHAINS; ++i) x[i] = __fadd2_rn(x[i], make_float2(c[i], c[i]));
+  }
+  float s = 0;
+  for (int i = 0; i < CHAINS; ++i) s += x[i].x + x[i].y;
+  if (s == 12345.f) out[0] = s;
+}
+
+__global__ void k_fmul2_pp(float* out, const float* ab) {  // pair x pair
+  float2 x[CHAINS], c[CHAINS];
+  for (int i = 0; i < CHAINS; ++i) { x[i] = make_float2(threadIdx.x * 1e-3f + i, i); c[i] = make_float2(ab[4 + i], ab[5 + i]); }
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < CHAINS; ++i) x[i] = __fmul2_rn(x[i], c[i]);
+  }
+  float s = 0;
+  for (int i = 0; i < CHAINS; ++i) s += x[i].x + x[i].y;
+  if (s == 12345.f) out[0] = s;
+}
+
+__global__ void k_ffma2_3p(float* out, const float* ab) {  // three distinct pairs (acc update)
+  float2 x[CHAINS], y[CHAINS], c[CHAINS];
+  for (int i = 0; i < CHAINS; ++i) {
+    x[i] = make_float2(threadIdx.x * 1e-3f + i, i);
+    y[i] = make_float2(ab[6 + i] * 1e-3f, ab[7 + i] * 1e-3f);
+    c[i] = make_float2(ab[4 + i], ab[5 + i]);
+  }
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < CHAINS; ++i) x[i] = __ffma2_rn(y[i], c[i], x[i]);
+  }
+  float s = 0;
+  for (int i = 0; i < CHAINS; ++i) s += x[i].x + x[i].y;
+  if (s == 12345.f) out[0] = s;
+}
+
 template <class F>
 float time_it(F f, int reps = 5) {
   cudaEvent_t e0, e1;
@@ -157,6 +199,12 @@ int main() {
   report("ffma2", ms, double(ITERS) * CHAINS * 2);
   ms = time_it([&] { k_ffma2_reg<<<blocks, threads>>>(d, d); });
   report("ffma2_reg", ms, double(ITERS) * CHAINS * 2);
+  ms = time_it([&] { k_fadd2_bc<<<blocks, threads>>>(d, d); });
+  report("fadd2_bcast", ms, double(ITERS) * CHAINS * 2);
+  ms = time_it([&] { k_fmul2_pp<<<blocks, threads>>>(d, d); });
+  report("fmul2_pair", ms, double(ITERS) * CHAINS * 2);
+  ms = time_it([&] { k_ffma2_3p<<<blocks, threads>>>(d, d); });
+  report("ffma2_3pair", ms, double(ITERS) * CHAINS * 2);
   ms = time_it([&] { k_mixed<<<blocks, threads>>>(d, d); });
   report("ffma2+ffma", ms, double(ITERS) * CHAINS * 3);
   ms = time_it([&] { k_rsq<<<blocks, threads>>>(d, 1.f); });
