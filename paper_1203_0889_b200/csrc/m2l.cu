@@ -2,6 +2,8 @@
 // by KernelVisitor::m2l_pair, traversal.hpp:143-152). See expansions.cu for the conventions.
 #include <algorithm>
 
+#include <cub/cub.cuh>
+
 #include "expansions.cuh"
 #include "tma.cuh"
 
@@ -736,6 +738,14 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
   trace_fill_store<P>(lane, cmp, full, L + (int64_t)t * N);
 }
 
+// lockstep CTAs: targets ordered by descending chunk count (stable), so the warps of a CTA carry
+// similar list lengths and few idle through the chunk barriers
+__global__ void k_target_chunks(const int32_t* __restrict__ targets, int64_t n, const int64_t* __restrict__ off,
+                                uint32_t* __restrict__ chunks) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) chunks[i] = static_cast<uint32_t>((off[targets[i] + 1] - off[targets[i]] + 31) / 32);
+}
+
 template <int P>
 struct M2L {
   static void run(fmm_ctx* c, cudaStream_t s) {
@@ -770,8 +780,25 @@ struct M2L {
       if (c->n_m2l_targets == 0) return;
       double* Mt = c->m2l_mt.ensure(c->ncells * C2::NA + 1);
       launch_detrace<P>(c, Mt, s);
+      const int32_t* tg = c->m2l_targets.p;
+#ifndef FMM_BIG2_SORT
+#define FMM_BIG2_SORT 1
+#endif
+      if (C2::kWarps > 1 && FMM_BIG2_SORT) {
+        const int64_t nt = c->n_m2l_targets;
+        uint32_t* kin = reinterpret_cast<uint32_t*>(c->keys_a.ensure(nt + 1));
+        uint32_t* kout = reinterpret_cast<uint32_t*>(c->keys_b.ensure(nt + 1));
+        int32_t* tout = c->i32_b.ensure(nt + 1);
+        k_target_chunks<<<ceil_div(nt, 256), 256, 0, s>>>(c->m2l_targets.p, nt, c->m2l_off.p, kin);
+        size_t sb = 0;
+        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, kin, kout, c->m2l_targets.p, tout, (int)nt, 0, 16, s));
+        CK(cub::DeviceRadixSort::SortPairsDescending(temp_storage(c, sb), sb, kin, kout, c->m2l_targets.p, tout,
+                                                     (int)nt, 0, 16, s));
+        tg = tout;
+        c->kernel_launches += 4;
+      }
       k_m2l_big2<P><<<(unsigned)ceil_div(c->n_m2l_targets, C2::kWarps), 32 * C2::kWarps, smem2, s>>>(
-          c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p, c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
+          tg, c->n_m2l_targets, c->m2l_off.p, c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
       CK_LAUNCH("k_m2l_big2");
       c->kernel_launches += 2;
       return;
