@@ -4,6 +4,7 @@
 // engine.hpp:38-49, measured on the device).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -490,12 +491,24 @@ int fmm_get_lists(fmm_ctx* c, int64_t* m2l_offsets, int32_t* m2l_sources, int64_
     auto cp = [&](void* dst, const void* src, size_t bytes) {
       if (dst && bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
     };
+    // the device CSR keeps each target's sources in (deterministic) emission order; the export
+    // is canonical: ascending sources within each target
+    auto sort_segments = [&](const int64_t* o_off, int32_t* o_src) {
+      for (int64_t t = 0; t < c->ncells; ++t) std::sort(o_src + o_off[t], o_src + o_off[t + 1]);
+    };
     if (!c->cfg.mutual) {
-      cp(m2l_offsets, c->m2l_off.p, (c->ncells + 1) * 8);
+      std::vector<int64_t> mo, po;
+      const int64_t* mo_p = m2l_offsets;
+      const int64_t* po_p = p2p_offsets;
+      if (m2l_sources && !m2l_offsets) { mo.resize(c->ncells + 1); mo_p = mo.data(); }
+      if (p2p_sources && !p2p_offsets) { po.resize(c->ncells + 1); po_p = po.data(); }
+      cp(const_cast<int64_t*>(mo_p), c->m2l_off.p, (mo_p ? (c->ncells + 1) * 8 : 0));
       cp(m2l_sources, c->m2l_src.p, c->n_m2l * 4);
-      cp(p2p_offsets, c->p2p_off.p, (c->ncells + 1) * 8);
+      cp(const_cast<int64_t*>(po_p), c->p2p_off.p, (po_p ? (c->ncells + 1) * 8 : 0));
       cp(p2p_sources, c->p2p_src.p, c->n_p2p * 4);
       CK(cudaStreamSynchronize(c->stream));
+      if (m2l_sources) sort_segments(mo_p, m2l_sources);
+      if (p2p_sources) sort_segments(po_p, p2p_sources);
       return;
     }
     // mutual: the emitted list (once per unordered pair, in its emitted orientation) = the
@@ -520,6 +533,7 @@ int fmm_get_lists(fmm_ctx* c, int64_t* m2l_offsets, int32_t* m2l_sources, int64_
           }
       }
       if (o_off) o_off[c->ncells] = k;
+      if (o_off && o_src) sort_segments(o_off, o_src);
     };
     emitted(c->m2l_off, c->m2l_src, c->m2l_mir, c->n_m2l, m2l_offsets, m2l_sources);
     emitted(c->p2p_off, c->p2p_src, c->p2p_mir, c->n_p2p, p2p_offsets, p2p_sources);

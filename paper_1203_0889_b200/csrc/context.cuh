@@ -91,7 +91,10 @@ struct fmm_ctx {
   fmmb::DBuf<double> small;
   fmmb::DBuf<int2> pairs_d;         // second traversal frontier
   fmmb::DBuf<uint64_t> m2l_keys, p2p_keys;  // emitted (target << sbits | source)
-  fmmb::DBuf<uint64_t> trav_ctr;            // traversal level counters
+  fmmb::DBuf<uint64_t> trav_ctr;            // traversal level counters + chunk tickets
+  fmmb::DBuf<uint32_t> lb_flag;             // traversal look-back: per-chunk status (epoch tagged)
+  fmmb::DBuf<uint64_t> lb_val;              // traversal look-back: per-chunk aggregate / prefix
+  uint32_t trav_epoch = 0;                  // one epoch per k_step launch
   fmmb::DBuf<int32_t> bnd;           // child boundaries of one level (9 per cell)
   fmmb::DBuf<int32_t> bnd_lev;       // device level table (tree build)
   int last_depth = 6;                // depth of the previous build (level batch, sorted digits)

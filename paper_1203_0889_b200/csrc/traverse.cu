@@ -62,17 +62,34 @@ __device__ __forceinline__ void classify(const int2 pr, const double4* __restric
 // One frontier step (frontier level L): every pair is classified (process_pair) and emits an
 // M2L or P2P key or pushes its child pairs to level L+1. The launch does not know the frontier
 // size: it reads it from the level counters written by the previous launch, so all levels are
-// queued back to back without a host round trip. Each block takes chunks of kStepChunk pairs
-// (kStepPer per thread) and reserves its output slots with one atomic per counter (block-level
-// aggregation: the per-warp variant was bound by same-address atomic throughput). Output that
-// would exceed a buffer's capacity is dropped and flagged; the host then grows the buffers and
-// reruns the traversal. Emission order is not deterministic; the lists are canonicalised
-// afterwards by a radix sort on (target, source), so everything downstream is deterministic.
+// queued back to back without a host round trip. A persistent grid takes chunks of pairs in
+// ticket order. With 64-bit keys (more than 2^16 cells, or mutual mode) each chunk's output
+// offsets come from a chained (decoupled look-back, warp-wide) scan over the chunks of the level,
+// so the emission order is a pure function of the frontier order: deterministic, level by level,
+// and the lists only need a STABLE sort on the target bits to become deterministic CSR (3
+// instead of 5 radix passes at C3-C5). With 32-bit keys the slots are reserved by one atomic per
+// chunk and counter, and the full (target, source) sort canonicalises the lists (cheaper at C2:
+// 4 passes of 4-byte keys against the look-back's latency). Output that would exceed a buffer's
+// capacity is dropped and flagged; the host then grows the buffers and reruns the traversal.
 // Counters (ctr): [0] M2L total, [1] P2P total, [2] overflow flag, [4 + L] frontier size of
-// level L (level 0 = the root pair).
+// level L (level 0 = the root pair), [64 + L] chunk tickets of level L.
 constexpr int kStepThreads = 256;
-constexpr int kStepPer = 4;
-constexpr int kStepChunk = kStepThreads * kStepPer;
+// pairs per thread: 4 with atomic slot reservation (32-bit keys), 8 with the ordered look-back
+// (fewer, larger chunks amortise the look-back)
+template <class KeyT>
+constexpr int step_per() { return sizeof(KeyT) == 8 ? 8 : 4; }
+template <class KeyT>
+constexpr int step_chunk() { return kStepThreads * step_per<KeyT>(); }
+constexpr int kTicketBase = 64;
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 
 template <class KeyT>
 __global__ void __launch_bounds__(kStepThreads)
@@ -80,14 +97,29 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
        const int32_t* __restrict__ cb, double theta, double theta2, int mutual, int sbits, KeyT* __restrict__ m2l_keys,
        KeyT* __restrict__ p2p_keys, int2* __restrict__ next, unsigned long long* __restrict__ ctr, int64_t cap_m,
        int64_t cap_p, int64_t cap_f, const int32_t* __restrict__ bb, const int32_t* __restrict__ be, int32_t tb0,
-       int32_t tb1, int filter) {
+       int32_t tb1, int filter, uint32_t epoch, uint32_t* __restrict__ lb_flag,
+       unsigned long long* __restrict__ lb_val) {
   using Scan = cub::BlockScan<unsigned long long, kStepThreads>;
+  // 64-bit keys (more than 2^16 cells, or mutual mode): ordered emission by look-back, and the
+  // lists only need a stable sort on the target bits; 32-bit keys: atomic slot reservation (the
+  // full (target, source) sort canonicalises them; measured cheaper at C2)
+  constexpr bool kOrdered = sizeof(KeyT) == 8;
+  constexpr int kStepPer = step_per<KeyT>();
+  constexpr int kStepChunk = step_chunk<KeyT>();
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ unsigned long long sbase[3];
+  __shared__ int64_t s_chunk;
   // a frontier that overflowed its buffer is only partially written (the run is flagged and
   // repeated with larger buffers): read no further than the capacity
   const int64_t n = min(static_cast<int64_t>(ctr[4 + level]), cap_f);
-  for (int64_t c0 = static_cast<int64_t>(blockIdx.x) * kStepChunk; c0 < n; c0 += static_cast<int64_t>(gridDim.x) * kStepChunk) {
+  const unsigned long long base_m = ctr[0], base_p = ctr[1];  // totals of the previous levels
+  const uint32_t f_agg = 2u * epoch, f_inc = 2u * epoch + 1u;
+  for (;;) {
+    if (threadIdx.x == 0) s_chunk = static_cast<int64_t>(atomicAdd(&ctr[kTicketBase + level], 1ull));
+    __syncthreads();
+    const int64_t ch = s_chunk;
+    const int64_t c0 = ch * kStepChunk;
+    if (c0 >= n) break;  // uniform over the block
     int kind[kStepPer], nch[kStepPer];
     int2 pr[kStepPer];
     // packed per-thread counts: M2L (bits 0..20) | P2P (21..41) | children (42..63)
@@ -112,11 +144,68 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
     }
     unsigned long long excl, tot;
     Scan(scan_tmp).ExclusiveSum(mine, excl, tot);
-    if (threadIdx.x == 0) {
-      const unsigned long long tm = tot & 0x1fffffull, tp = (tot >> 21) & 0x1fffffull, tc = tot >> 42;
-      sbase[0] = tm ? atomicAdd(&ctr[0], tm) : 0ull;
-      sbase[1] = tp ? atomicAdd(&ctr[1], tp) : 0ull;
-      sbase[2] = tc ? atomicAdd(&ctr[4 + level + 1], tc) : 0ull;
+    if (!kOrdered) {
+      if (threadIdx.x == 0) {
+        const unsigned long long tm = tot & 0x1fffffull, tp = (tot >> 21) & 0x1fffffull, tc = tot >> 42;
+        sbase[0] = tm ? atomicAdd(&ctr[0], tm) : 0ull;
+        sbase[1] = tp ? atomicAdd(&ctr[1], tp) : 0ull;
+        sbase[2] = tc ? atomicAdd(&ctr[4 + level + 1], tc) : 0ull;
+      }
+    } else if (threadIdx.x < 32) {
+      // chunk aggregate: (M2L | P2P << 32) and children; the exclusive prefix over the earlier
+      // chunks of this level by a warp-wide decoupled look-back, 32 predecessors per step
+      // (chunk ch only waits for chunks with lower tickets, all running or done: no deadlock)
+      const int lane = threadIdx.x;
+      unsigned long long tot_b = __shfl_sync(0xffffffffu, tot, 0);
+      const unsigned long long a01 = (tot_b & 0x1fffffull) | (((tot_b >> 21) & 0x1fffffull) << 32);
+      const unsigned long long a2 = tot_b >> 42;
+      unsigned long long p01 = 0, p2 = 0;
+      if (ch > 0) {
+        if (lane == 0) {
+          lb_val[4 * ch + 0] = a01;
+          lb_val[4 * ch + 1] = a2;
+          st_release(&lb_flag[ch], f_agg);
+        }
+        for (int64_t top = ch - 1;; top -= 32) {
+          const int64_t j = top - lane;
+          uint32_t f = f_inc;  // lanes before chunk 0 count as an empty inclusive prefix
+          if (j >= 0) {
+            do {
+              f = ld_acquire(&lb_flag[j]);
+            } while (f != f_agg && f != f_inc);
+          }
+          const unsigned inc = __ballot_sync(0xffffffffu, f == f_inc);
+          const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest lane holding an inclusive prefix
+          unsigned long long v01 = 0, v2 = 0;
+          if (j >= 0 && lane <= stop) {
+            const int o = f == f_inc ? 2 : 0;
+            v01 = __ldcg(&lb_val[4 * j + o]);
+            v2 = __ldcg(&lb_val[4 * j + o + 1]);
+          }
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) {
+            v01 += __shfl_xor_sync(0xffffffffu, v01, d);
+            v2 += __shfl_xor_sync(0xffffffffu, v2, d);
+          }
+          p01 += v01;
+          p2 += v2;
+          if (inc) break;
+        }
+      }
+      if (lane == 0) {
+        lb_val[4 * ch + 2] = p01 + a01;
+        lb_val[4 * ch + 3] = p2 + a2;
+        st_release(&lb_flag[ch], f_inc);
+        sbase[0] = base_m + (p01 & 0xffffffffull);
+        sbase[1] = base_p + (p01 >> 32);
+        sbase[2] = p2;
+        if (c0 + kStepChunk >= n) {  // the level's last chunk: totals for the next launch
+          const unsigned long long i01 = p01 + a01;
+          ctr[0] = base_m + (i01 & 0xffffffffull);
+          ctr[1] = base_p + (i01 >> 32);
+          ctr[4 + level + 1] = p2 + a2;
+        }
+      }
     }
     __syncthreads();
     int64_t om = static_cast<int64_t>(sbase[0] + (excl & 0x1fffffull));
@@ -166,7 +255,7 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
       }
     }
     if (over) ctr[2] = 1ull;
-    __syncthreads();  // sbase / scan storage reuse
+    __syncthreads();  // sbase / scan storage / s_chunk reuse
   }
 }
 
@@ -250,8 +339,11 @@ void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int
   const int sbits = bits_for(static_cast<uint64_t>(nc));
   KeyT* kb = reinterpret_cast<KeyT*>(c->keys_b.ensure(n));
   size_t sb = 0;
-  CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys, kb, (int)n, 0, 2 * sbits, s));
-  CK(cub::DeviceRadixSort::SortKeys(temp_storage(c, sb), sb, keys, kb, (int)n, 0, 2 * sbits, s));
+  // 64-bit keys come in a deterministic order (ordered emission / given pairs): a stable sort on
+  // the target bits keeps it within each target; 32-bit keys: the full (target, source) sort
+  const int b0 = sizeof(KeyT) == 8 ? sbits : 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys, kb, (int)n, b0, 2 * sbits, s));
+  CK(cub::DeviceRadixSort::SortKeys(temp_storage(c, sb), sb, keys, kb, (int)n, b0, 2 * sbits, s));
   k_csr_from_keys<<<ceil_div(n + 1, 256), 256, 0, s>>>(kb, n, sbits, nc, off.p, src.p, mir, tgt);
   CK_LAUNCH("keys_to_csr");
   c->kernel_launches += 3;
@@ -345,7 +437,7 @@ void traverse(fmm_ctx* c) {
   // the frontier is empty after at most 2 * depth + 1 levels.
   const int nlev = 2 * c->depth + 2;
   if (4 + nlev + 1 > 60) fail(FMM_ERR_UNSUPPORTED, "traverse: tree too deep");
-  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(c->trav_ctr.ensure(64));
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(c->trav_ctr.ensure(128));
   unsigned long long* h = reinterpret_cast<unsigned long long*>(c->hpin);
   // first call: capacities from the cell count; afterwards the buffers keep their size
   const int64_t want_f = std::max<int64_t>(c->ncells * 256, 1 << 16);
@@ -367,23 +459,33 @@ void traverse(fmm_ctx* c) {
     // KeyT buffers are uint64_t arrays; 32-bit keys use twice the count
     const int64_t cap_m = static_cast<int64_t>(c->m2l_keys.cap) * (small ? 2 : 1);
     const int64_t cap_p = static_cast<int64_t>(c->p2p_keys.cap) * (small ? 2 : 1);
-    CK(cudaMemsetAsync(ctr, 0, 64 * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(ctr, 0, 128 * sizeof(unsigned long long), s));
+    // look-back state: one flag + 4 values per chunk of the largest frontier (flags zeroed on
+    // (re)allocation only: every launch uses a fresh epoch)
+    const int64_t nchunk = cap_f / step_chunk<uint32_t>() + 2;
+    if (c->lb_flag.cap < static_cast<size_t>(nchunk)) {
+      c->lb_flag.ensure(nchunk);
+      CK(cudaMemsetAsync(c->lb_flag.p, 0, sizeof(uint32_t) * c->lb_flag.cap, s));
+    }
+    unsigned long long* lbv = reinterpret_cast<unsigned long long*>(c->lb_val.ensure(4 * nchunk));
     const unsigned long long one = 1;
     CK(cudaMemcpyAsync(ctr + 4, &one, sizeof(one), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(c->pairs_a.p, &root, sizeof(int2), cudaMemcpyHostToDevice, s));
     for (int L = 0; L < nlev; ++L) {
       const int2* fr = (L & 1) ? c->pairs_d.p : c->pairs_a.p;
       int2* nx = (L & 1) ? c->pairs_a.p : c->pairs_d.p;
+      const uint32_t epoch = ++c->trav_epoch;
       if (small)
         k_step<<<grid, kStepThreads, 0, s>>>(L, fr, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
                                              theta * theta, mutual, sbits, (uint32_t*)c->m2l_keys.p,
                                              (uint32_t*)c->p2p_keys.p, nx, ctr, cap_m, cap_p, cap_f,
-                                             c->c_body_begin.p, c->c_body_end.p, tb0, tb1, filter);
+                                             c->c_body_begin.p, c->c_body_end.p, tb0, tb1, filter, epoch,
+                                             c->lb_flag.p, lbv);
       else
         k_step<<<grid, kStepThreads, 0, s>>>(L, fr, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
                                              theta * theta, mutual, sbits, c->m2l_keys.p, c->p2p_keys.p, nx, ctr,
                                              cap_m, cap_p, cap_f, c->c_body_begin.p, c->c_body_end.p, tb0, tb1,
-                                             filter);
+                                             filter, epoch, c->lb_flag.p, lbv);
       CK_LAUNCH("k_step");
     }
     CK(cudaMemcpyAsync(h, ctr, (4 + nlev + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
