@@ -196,6 +196,9 @@ constexpr int m2l_row_stride(int n) {
 // lane's detraced source row arrives by one TMA bulk copy (8-byte cp.async when the row is not
 // a 16-byte multiple) on a per-warp mbarrier while the recurrence runs; one shared-memory
 // transpose reduction per target, then the c >= 2 entries of Lambda by the trace identity.
+#ifndef FMM_M2L_DB
+#define FMM_M2L_DB 0  // measured slower at p = 6 (1.07 -> 1.14 ms): register pressure
+#endif
 #ifndef FMM_M2L_MINB
 #define FMM_M2L_MINB 10
 #endif
@@ -211,17 +214,19 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
   using T = MI<P>;
   using H = HM<P>;
   constexpr int N = T::N, NA = H::NA, NG = H::NG, S = m2l_row_stride(NA);
+  constexpr bool kBulk = (NA * 8) % 16 == 0;
+  // kBulk: the rows of chunk k+1 are copied (TMA) into the other buffer while chunk k computes
+  constexpr int kBufs = kBulk && FMM_M2L_DB ? 2 : 1;
   extern __shared__ double smem[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* sR = smem + (size_t)w * 32 * S;  // per-warp source rows, then reduction rows
-  constexpr bool kBulk = (NA * 8) % 16 == 0;
-  __shared__ __align__(8) uint64_t bars[kM2LWarps];
+  double* sR = smem + (size_t)w * kBufs * 32 * S;  // per-warp source rows, then reduction rows
+  __shared__ __align__(8) uint64_t bars[kM2LWarps][2];
   if (kBulk && lane == 0) {
-    mbar_init(&bars[w], 1);
+    mbar_init(&bars[w][0], 1);
+    mbar_init(&bars[w][1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncwarp();
-  unsigned phase = 0;
   const int64_t wid = blockIdx.x * (int64_t)kM2LWarps + w;
   if (wid >= ntargets) return;
   const int32_t t = targets[wid];
@@ -230,45 +235,44 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
   double lam[NA];
 #pragma unroll
   for (int i = 0; i < NA; ++i) lam[i] = 0.0;
-  int32_t s_next = (l0 + lane < l1) ? src[l0 + lane] : t;
-#if FMM_M2L_PREFETCH
-  double4 cs_next = cr[s_next];
-#endif
-  for (int64_t base = l0; base < l1; base += 32) {
-    const int64_t k = base + lane;
-    const bool valid = k < l1;
-    const int32_t s = s_next;
-    // stage this lane's detraced source multipole (async; hidden behind the Dt recurrence)
-    if (!valid) {
-      for (int e = 0; e < NA; ++e) sR[lane * S + e] = 0.0;  // tail lanes contribute nothing
+  // stage the lane's detraced source row of chunk `cbase` into buffer b (async)
+  auto stage = [&](int b, int64_t cbase, int32_t s_lane) {
+    double* row = sR + (size_t)b * 32 * S + lane * S;
+    if (cbase + lane >= l1) {
+      for (int e = 0; e < NA; ++e) row[e] = 0.0;  // tail lanes contribute nothing
     } else if constexpr (kBulk) {
       fence_proxy_async_smem();  // earlier generic reads of this row before the async write
-      bulk_g2s(sR + lane * S, Mt + (int64_t)s * NA, NA * 8, &bars[w]);
+      bulk_g2s(row, Mt + (int64_t)s_lane * NA, NA * 8, &bars[w][b]);
     } else {
-      const char* row = reinterpret_cast<const char*>(Mt + (int64_t)s * NA);
-      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(sR + lane * S));
+      const char* g = reinterpret_cast<const char*>(Mt + (int64_t)s_lane * NA);
+      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(row));
 #pragma unroll
       for (int e = 0; e < NA * 8; e += 8)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + e), "l"(row + e));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + e), "l"(g + e));
     }
     if constexpr (kBulk) {
       if (lane == 0) {
-        const int64_t nv = l1 - base < 32 ? l1 - base : 32;
-        mbar_arrive_expect_tx(&bars[w], static_cast<unsigned>(nv * NA * 8));
+        const int64_t nv = l1 - cbase < 32 ? l1 - cbase : 32;
+        mbar_arrive_expect_tx(&bars[w][b], static_cast<unsigned>(nv * NA * 8));
       }
     } else {
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
-#if FMM_M2L_PREFETCH
-    const double4 cs = cs_next;
-    if (base + 32 + lane < l1) {
-      s_next = src[base + 32 + lane];
-      cs_next = cr[s_next];  // next chunk's centre: its L2 latency hides behind this chunk
+  };
+  int32_t s_cur = (l0 + lane < l1) ? src[l0 + lane] : t;
+  int32_t s_nxt = (l0 + 32 + lane < l1) ? src[l0 + 32 + lane] : t;
+  if (kBufs == 2) stage(0, l0, s_cur);
+  unsigned k = 0;
+  for (int64_t base = l0; base < l1; base += 32, ++k) {
+    const int b = kBufs == 2 ? (k & 1) : 0;
+    const bool valid = base + lane < l1;
+    if (kBufs == 2) {
+      if (base + 32 < l1) stage(b ^ 1, base + 32, s_nxt);  // next chunk, behind this one
+    } else {
+      stage(0, base, s_cur);  // hidden behind the Dt recurrence only
     }
-#else
-    if (base + 32 + lane < l1) s_next = src[base + 32 + lane];
-    const double4 cs = valid ? cr[s] : ct;
-#endif
+    const int32_t s_nn = (base + 64 + lane < l1) ? src[base + 64 + lane] : t;
+    const double4 cs = valid ? cr[s_cur] : ct;
     double rx = 1.0, ry = 0.0, rz = 0.0;
     if (valid) {
       rx = cs.x - ct.x;  // R = source centre - target centre (traversal.hpp:146)
@@ -278,13 +282,12 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
     double D[NG];
     derivs_reg<P>(rx, ry, rz, D);
     if constexpr (kBulk) {
-      mbar_wait(&bars[w], phase);
-      phase ^= 1u;
+      mbar_wait(&bars[w][b], kBufs == 2 ? ((k >> 1) & 1u) : (k & 1u));
     } else {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
     }
     __syncwarp();
-    const double* Ms = sR + lane * S;
+    const double* Ms = sR + (size_t)b * 32 * S + lane * S;
     auto contract = [&](auto KA, const double m) {
       constexpr int ia = H::a_full(decltype(KA)::value);
       constexpr int aa = T::ea(ia), ab = T::eb(ia), ac = T::ec(ia), da = T::deg(ia);
@@ -305,7 +308,9 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
       contract(std::integral_constant<int, i0 + 1>{}, mm.y);
     });
     if constexpr (NA & 1) contract(std::integral_constant<int, NA - 1>{}, Ms[NA - 1]);
-    __syncwarp();  // every lane done reading sR before the next chunk's copies land
+    __syncwarp();  // every lane done reading this buffer before it is refilled
+    s_cur = s_nxt;
+    s_nxt = s_nn;
   }
   // reduce the 32 lane partials (shared-memory transpose) ...
 #pragma unroll
@@ -751,7 +756,8 @@ struct M2L {
   static void run(fmm_ctx* c, cudaStream_t s) {
     if constexpr (P <= 6) {
       constexpr int S = m2l_row_stride(HM<P>::NA);
-      const size_t smem = sizeof(double) * kM2LWarps * 32 * S;
+      constexpr int kBufs = (HM<P>::NA * 8) % 16 == 0 && FMM_M2L_DB ? 2 : 1;
+      const size_t smem = sizeof(double) * kM2LWarps * kBufs * 32 * S;
       static bool attr = false;
       if (!attr) {
         CK(cudaFuncSetAttribute(k_m2l_reg<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
