@@ -7,15 +7,16 @@
 // cost exceeds a per-SM share are split into source chunks whose partial sums are reduced in
 // a fixed order afterwards (deterministic, no atomics). Writes are target-owned.
 //
-// Inside a CTA the 128 threads form G = floor(128 / n_t) lane groups; thread (g, t) owns
-// target body t and every G-th source pair of each shared-memory tile. Source tiles hold up to
-// 32 list entries (1024 bodies) converted to coordinates relative to the TARGET leaf centre:
-// bodies are stored in HBM as FP32 offsets from their own leaf centre and shifted by the
-// FP64-computed centre difference, so FP32 only ever sees leaf-scale magnitudes. Tiles are
-// pair-interleaved {-x0,-x1,-y0,-y1},{-z0,-z1,q0,q1} so the inner loop runs on the packed
-// f32x2 pipe (FFMA2/FADD2/FMUL2) with one MUFU.RSQ per pair; r^2 == 0 pairs (self,
-// coincident; kernels.cpp:185-186) are removed by a select. Each tile's FP32 partial sums are
-// folded into FP64 per-target accumulators ("FP64-checked accumulation").
+// Inside a CTA four consumer warps (128 threads) form G = floor(128 / ceil(n_t / 2)) lane groups;
+// thread (g, t) owns the target pair (2t, 2t+1) packed in f32x2 lanes and a contiguous chunk of
+// each shared-memory tile; a fifth (producer) warp stages the tiles (k_p2p_fp32_ws). Tiles hold
+// up to 64 list entries (1 024 bodies) converted to coordinates relative to the TARGET leaf
+// centre: bodies are stored in HBM as FP32 offsets from their own leaf centre and shifted by
+// the FP64-computed centre difference, so FP32 only ever sees leaf-scale magnitudes; the inner
+// loop runs on the packed f32x2 pipe (FFMA2/FADD2/FMUL2) with one MUFU.RSQ per pair; r^2 == 0
+// pairs (self, coincident; kernels.cpp:185-186) are removed by a predicate in the self tile.
+// Each tile's FP32 partial sums are folded into FP64 per-target accumulators ("FP64-checked
+// accumulation").
 #include <cub/cub.cuh>
 #include <cstdlib>
 
@@ -26,7 +27,7 @@ namespace fmmb {
 namespace {
 
 constexpr int kThreads = 128;   // threads per P2P CTA (max target bodies per item)
-constexpr int kTileSegs = 32;   // list entries staged per tile
+constexpr int kTileSegs = 64;   // list entries per FP32 tile (two per producer lane)
 #ifndef FMM_P2P_TILE
 #define FMM_P2P_TILE 1024
 #endif
@@ -93,16 +94,6 @@ __device__ __forceinline__ void tile_setup(int tid, int32_t le, int32_t cursor, 
   }
 }
 
-// ------------------------------------------------------------------------ FP32 kernel ----
-// Thread (g, t) owns the target pair (2t, 2t+1) of the item, packed in f32x2 lanes, and every
-// G-th source of each tile (G = 128 / ceil(n_t/2) lane groups). Sources are staged as float4
-// {-x, -y, -z, q} in the target leaf's frame; the packed ops take the source component as a
-// broadcast scalar operand, so one LDS.128 feeds two pair evaluations.
-//
-// Tiles are software-pipelined: while tile k is computed from one shared buffer, tile k+1's
-// raw bodies stream into the other buffer with cp.async (no registers), and warp 0 resolves
-// tile k+2's list entries. After the compute, each thread converts the bodies it copied in
-// place (shift into the target frame, negate), and one barrier per tile publishes them.
 // One P2P list entry (target specific): source bodies and the FP64 centre difference into the
 // target leaf frame as an FP32 hi + lo pair. kind (top two bits of nk): 0 = far, 1 = the
 // (leaf, leaf) self entry (the only one that can hold r^2 == 0 pairs), 2 = near (the two
@@ -125,132 +116,112 @@ struct TileTab {
   int32_t nseg, next, next_off, guard, prec;
 };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-// warp 0: stage list entries [cursor, cursor + 32) into shared memory ahead of tile_setup_ent,
-// so that the global-load latency overlaps a tile's compute instead of the tile barrier
-__device__ __forceinline__ void ent_prefetch(int lane, int32_t cursor, int32_t le, const P2PEnt* __restrict__ ent,
-                                             P2PEnt* st) {
-  if (cursor + lane < le) {
-    cp_async16(&st[lane], &ent[cursor + lane]);
-    cp_async16(reinterpret_cast<char*>(&st[lane]) + 16, reinterpret_cast<const char*>(&ent[cursor + lane]) + 16);
-  }
-}
-
-// warp 0: take the list entries from (cursor, cur_off) that fit in one tile; e[lane] is list
-// entry cursor + lane (global memory, or the shared staging copy)
+// producer warp: take the list entries from (cursor, cur_off) that fit in one tile; e[i] is list
+// entry cursor + i, lane l holds entries l and l + 32 (small leaves, e.g. C5's median of 18
+// bodies, fill a 1 024-body tile only with ~60 entries)
 __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cursor, int32_t cur_off,
                                                const P2PEnt* e, TileTab& tt) {
-  const int32_t k = cursor + lane;
-  int32_t n = 0, b = 0, kind = kKindFar;
-  float sx = 0.f, sy = 0.f, sz = 0.f, lx = 0.f, ly = 0.f, lz = 0.f;
-  if (k < le) {
-    const int4 e0 = reinterpret_cast<const int4*>(e)[2 * lane];
-    const int4 e1 = reinterpret_cast<const int4*>(e)[2 * lane + 1];
-    b = e0.x;
-    n = e0.y & 0x3fffffff;
-    kind = static_cast<int>(static_cast<uint32_t>(e0.y) >> 30);
-    sx = __int_as_float(e0.z);
-    sy = __int_as_float(e0.w);
-    sz = __int_as_float(e1.x);
-    lx = __int_as_float(e1.y);
-    ly = __int_as_float(e1.z);
-    lz = __int_as_float(e1.w);
-    if (lane == 0) {
-      b += cur_off;
-      n -= cur_off;
+  constexpr int H = kTileSegs / 32;
+  int32_t n[H], b[H], kind[H], incl[H];
+  float sh[H][3], sl[H][3];
+  bool valid[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    const int32_t k = cursor + h * 32 + lane;
+    valid[h] = k < le;
+    n[h] = 0;
+    b[h] = 0;
+    kind[h] = kKindFar;
+    sh[h][0] = sh[h][1] = sh[h][2] = sl[h][0] = sl[h][1] = sl[h][2] = 0.f;
+    if (valid[h]) {
+      const int4 e0 = reinterpret_cast<const int4*>(e)[2 * (h * 32 + lane)];
+      const int4 e1 = reinterpret_cast<const int4*>(e)[2 * (h * 32 + lane) + 1];
+      b[h] = e0.x;
+      n[h] = e0.y & 0x3fffffff;
+      kind[h] = static_cast<int>(static_cast<uint32_t>(e0.y) >> 30);
+      sh[h][0] = __int_as_float(e0.z);
+      sh[h][1] = __int_as_float(e0.w);
+      sh[h][2] = __int_as_float(e1.x);
+      sl[h][0] = __int_as_float(e1.y);
+      sl[h][1] = __int_as_float(e1.z);
+      sl[h][2] = __int_as_float(e1.w);
+      if (h == 0 && lane == 0) {
+        b[h] += cur_off;
+        n[h] -= cur_off;
+      }
     }
   }
   // one class per tile: the self entry alone (r^2 == 0 guard), near entries (compensated, half
   // the bodies: hi and lo staged), far entries (plain FP32)
-  const int kind0 = __shfl_sync(0xffffffffu, kind, 0);
+  const int kind0 = __shfl_sync(0xffffffffu, kind[0], 0);
   const int cap = kind0 == kKindFar ? kTileBodies : kHalfTile;
-  int32_t incl = n;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
+  int32_t running = 0;
+  unsigned m[H], other[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    incl[h] = n[h];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t v = __shfl_up_sync(0xffffffffu, incl[h], o);
+      if (lane >= o) incl[h] += v;
+    }
+    incl[h] += running;
+    running = __shfl_sync(0xffffffffu, incl[h], 31);
+    m[h] = __ballot_sync(0xffffffffu, valid[h] && incl[h] <= cap);
+    other[h] = __ballot_sync(0xffffffffu, valid[h] && kind[h] != kind0);
   }
-  const bool fits = (k < le) && (incl <= cap);
-  const unsigned m = __ballot_sync(0xffffffffu, fits);
-  const unsigned other = __ballot_sync(0xffffffffu, (k < le) && kind != kind0);
-  int nseg;
-  if (m == 0) {  // one (level-21 overflow) leaf larger than the tile: take cap of its bodies
+  int nseg = 0;  // the fitting entries are a prefix of the 64
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    if (nseg == 32 * h) nseg += 32 - __clz(m[h]);
+  }
+  const bool huge = m[0] == 0;  // one (level-21 overflow) leaf larger than the tile: take cap of it
+  if (huge) {
     nseg = 1;
-    incl = cap;
-  } else {
-    nseg = 32 - __clz(m);  // fits is a prefix of the lanes
+    incl[0] = cap;
   }
+  int first_other = kTileSegs;
+#pragma unroll
+  for (int h = H - 1; h >= 0; --h)
+    if (other[h]) first_other = 32 * h + __ffs(other[h]) - 1;
   if (kind0 == kKindSelf) nseg = 1;
-  else if (other) nseg = min(nseg, __ffs(other) - 1);
-  if (lane < nseg) {
-    tt.off[lane + 1] = incl;
-    tt.bb[lane] = b;
-    tt.sh[lane][0] = sx;
-    tt.sh[lane][1] = sy;
-    tt.sh[lane][2] = sz;
-    tt.sl[lane][0] = lx;
-    tt.sl[lane][1] = ly;
-    tt.sl[lane][2] = lz;
+  else nseg = min(nseg, first_other);
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    const int idx = h * 32 + lane;
+    if (idx < nseg) {
+      tt.off[idx + 1] = incl[h];
+      tt.bb[idx] = b[h];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        tt.sh[idx][d] = sh[h][d];
+        tt.sl[idx][d] = sl[h][d];
+      }
+    }
   }
   if (lane == 0) {
     tt.off[0] = 0;
     tt.nseg = nseg;
-    tt.next = m == 0 ? cursor : cursor + nseg;
-    tt.next_off = m == 0 ? cur_off + cap : 0;
+    tt.next = huge ? cursor : cursor + nseg;
+    tt.next_off = huge ? cur_off + cap : 0;
     tt.guard = kind0 == kKindSelf ? 1 : 0;
     tt.prec = kind0 == kKindFar ? 0 : 1;
   }
 }
 
-// warp 0: one bulk copy per list entry of the tile (lane k copies entry k's bodies); the bytes
-// land on `bar`. The proxy fence orders the CTA's earlier generic reads/writes of the buffer
-// (published by the preceding __syncthreads) before the async-proxy writes.
+// producer warp: one bulk copy per list entry of the tile (lane k copies entries k, k + 32);
+// the bytes land on `bar`. The proxy fence orders earlier generic reads/writes of the buffer
+// (released to the producer through the empty barrier) before the async-proxy writes.
 __device__ __forceinline__ void tile_tma(int lane, const TileTab& tt, const float4* __restrict__ bodyf,
                                          const float4* __restrict__ bodyl, float4* buf, uint64_t* bar) {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   const int nseg = tt.nseg;
   const bool prec = tt.prec != 0;
   if (lane == 0) mbar_arrive_expect_tx(bar, static_cast<unsigned>(tt.off[nseg]) * (prec ? 32u : 16u));
-  if (lane < nseg) {
-    const int32_t o0 = tt.off[lane];
-    const unsigned bytes = static_cast<unsigned>(tt.off[lane + 1] - o0) * 16u;
-    bulk_g2s(buf + o0, bodyf + tt.bb[lane], bytes, bar);
-    if (prec) bulk_g2s(buf + kHalfTile + o0, bodyl + tt.bb[lane], bytes, bar);
-  }
-}
-
-// all threads: shift the staged bodies into the target frame and negate (warp w converts list
-// entries w, w+4, ..., two entries per pass for memory-level parallelism)
-__device__ __forceinline__ void tile_convert(int tid, const TileTab& tt, float4* buf) {
-  const int w = tid >> 5, lane = tid & 31;
-  const int nseg = tt.nseg;
-#pragma unroll 1
-  for (int k = w; k < nseg; k += 8) {
-    const int k1 = k + 4;
-    const int32_t o0 = tt.off[k], n0 = tt.off[k + 1] - o0;
-    int32_t o1 = 0, n1 = 0;
-    float tx = 0.f, ty = 0.f, tz = 0.f;
-    if (k1 < nseg) {
-      o1 = tt.off[k1];
-      n1 = tt.off[k1 + 1] - o1;
-      tx = tt.sh[k1][0];
-      ty = tt.sh[k1][1];
-      tz = tt.sh[k1][2];
-    }
-    const float sx = tt.sh[k][0], sy = tt.sh[k][1], sz = tt.sh[k][2];
-    const int32_t nm = max(n0, n1);
-#pragma unroll 1
-    for (int j = lane; j < nm; j += 32) {
-      float4 a, b;
-      if (j < n0) a = buf[o0 + j];
-      if (j < n1) b = buf[o1 + j];
-      if (j < n0) buf[o0 + j] = make_float4(-a.x - sx, -a.y - sy, -a.z - sz, a.w);
-      if (j < n1) buf[o1 + j] = make_float4(-b.x - tx, -b.y - ty, -b.z - tz, b.w);
-    }
+  for (int idx = lane; idx < nseg; idx += 32) {
+    const int32_t o0 = tt.off[idx];
+    const unsigned bytes = static_cast<unsigned>(tt.off[idx + 1] - o0) * 16u;
+    bulk_g2s(buf + o0, bodyf + tt.bb[idx], bytes, bar);
+    if (prec) bulk_g2s(buf + kHalfTile + o0, bodyl + tt.bb[idx], bytes, bar);
   }
 }
 
@@ -262,21 +233,6 @@ __device__ __forceinline__ float2 two_sum(float a, float b) {
   const float bb = __fsub_rn(s, a);
   const float e = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
   return make_float2(s, e);
-}
-
-__device__ __forceinline__ void tile_convert_prec(int tid, const TileTab& tt, float4* buf) {
-  const int nb = tt.off[tt.nseg];
-  const int nseg = tt.nseg;
-#pragma unroll 1
-  for (int j = tid; j < nb; j += kThreads) {
-    int k = 0;  // entry of body j (<= 32 entries: linear scan of the offsets)
-    while (k + 1 < nseg && tt.off[k + 1] <= j) ++k;
-    const float4 h = buf[j], l = buf[kHalfTile + j];
-    const float2 x = two_sum(h.x, tt.sh[k][0]), y = two_sum(h.y, tt.sh[k][1]), z = two_sum(h.z, tt.sh[k][2]);
-    buf[j] = make_float4(-x.x, -y.x, -z.x, h.w);
-    buf[kHalfTile + j] = make_float4(-((x.y + l.x) + tt.sl[k][0]), -((y.y + l.y) + tt.sl[k][1]),
-                                     -((z.y + l.z) + tt.sl[k][2]), 0.f);
-  }
 }
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
@@ -404,136 +360,8 @@ __device__ __forceinline__ void tile_compute_prec(const float4* __restrict__ buf
 #ifndef FMM_P2P_MIN_BLOCKS
 #define FMM_P2P_MIN_BLOCKS 6
 #endif
-template <bool kAcc>
-__global__ void __launch_bounds__(kThreads, FMM_P2P_MIN_BLOCKS)
-k_p2p_fp32(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, const float4* __restrict__ bodyf,
-           const float4* __restrict__ bodyl, double* __restrict__ phi_out, double* __restrict__ acc_out,
-           double* __restrict__ partial) {
-  __shared__ __align__(16) float4 sS[2][kTileBodies];
-  __shared__ TileTab tabs[3];  // ring: tile k computes from tabs[k%3] while k+2 is resolved
-  __shared__ __align__(8) uint64_t bars[2];  // TMA completion, one per buffer
-  __shared__ __align__(16) P2PEnt st[32];    // list entries staged for the next tile_setup_ent
-
-  const P2PItem it = items[blockIdx.x];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int nt = it.te - it.tb;
-  const int slots = (nt + 1) >> 1;
-  const int G = kThreads / slots;
-  const int g = tid / slots, t = tid - g * slots;
-  const bool active = g < G;
-
-  Tgt T;
-  T.X = make_float2(0.f, 0.f);
-  T.Y = T.Z = T.XL = T.YL = T.ZL = T.X;
-  if (active) {
-    const int32_t i0 = it.tb + 2 * t, i1 = (2 * t + 1 < nt) ? i0 + 1 : i0;
-    const float4 b0 = bodyf[i0], b1 = bodyf[i1];
-    const float4 l0 = bodyl[i0], l1 = bodyl[i1];
-    T.X = make_float2(b0.x, b1.x);
-    T.Y = make_float2(b0.y, b1.y);
-    T.Z = make_float2(b0.z, b1.z);
-    T.XL = make_float2(l0.x, l1.x);
-    T.YL = make_float2(l0.y, l1.y);
-    T.ZL = make_float2(l0.z, l1.z);
-  }
-  Acc64 A;
-
-  // prologue: tile 0 staged and converted, tile 1 resolved
-  bool have = it.lb < it.le;
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  if (tid < 32 && have) {
-    tile_setup_ent(lane, it.le, it.lb, 0, ent + it.lb, tabs[0]);
-    __syncwarp();
-    tile_tma(lane, tabs[0], bodyf, bodyl, sS[0], &bars[0]);
-    const int32_t c1 = tabs[0].next;
-    if (c1 < it.le) tile_setup_ent(lane, it.le, c1, tabs[0].next_off, ent + c1, tabs[1]);
-  }
-  __syncthreads();
-  if (have) {
-    mbar_wait(&bars[0], 0);
-    if (tabs[0].prec) tile_convert_prec(tid, tabs[0], sS[0]);
-    else tile_convert(tid, tabs[0], sS[0]);
-  }
-  __syncthreads();
-  int k3 = 0, k2 = 0;  // tile index mod 3 (tables) and mod 2 (buffers)
-  unsigned kt = 0;     // tile index (TMA barrier parity of tile j is (j >> 1) & 1)
-  while (have) {
-    const TileTab& tc = tabs[k3];
-    const int n1 = k3 == 2 ? 0 : k3 + 1, n2 = n1 == 2 ? 0 : n1 + 1;
-    const TileTab& tn = tabs[n1];
-    const bool more = tc.next < it.le;
-    const int nb = tc.off[tc.nseg];
-    if (more && tid < 32) {
-      tile_tma(lane, tn, bodyf, bodyl, sS[k2 ^ 1], &bars[k2 ^ 1]);
-      ent_prefetch(lane, tn.next, it.le, ent, st);
-    }
-    if (active) {
-      if (!tc.prec)
-        tile_compute<kAcc>(sS[k2], nb, g, G, T, A);
-      else if (tc.guard)
-        tile_compute_prec<kAcc, true>(sS[k2], nb, g, G, T, A);
-      else
-        tile_compute_prec<kAcc, false>(sS[k2], nb, g, G, T, A);
-    }
-    if (more) {
-      mbar_wait(&bars[k2 ^ 1], ((kt + 1) >> 1) & 1u);
-      if (tn.prec) tile_convert_prec(tid, tn, sS[k2 ^ 1]);
-      else tile_convert(tid, tn, sS[k2 ^ 1]);
-      if (tid < 32 && tn.next < it.le) {
-        cp_async_wait_all();
-        __syncwarp();
-        tile_setup_ent(lane, it.le, tn.next, tn.next_off, st, tabs[n2]);
-      }
-    }
-    __syncthreads();  // tile k+1 published, tile k+2 resolved; everyone is done with tile k
-    have = more;
-    k3 = n1;
-    k2 ^= 1;
-    ++kt;
-  }
-  // reduce the G lane groups in fixed order (reusing the tile buffer) and write
-  double* red = reinterpret_cast<double*>(sS);  // [G][slots][2 targets][4]
-  if (active) {
-    double* r = red + 8 * (g * slots + t);
-    r[0] = A.ph0; r[1] = A.ax0; r[2] = A.ay0; r[3] = A.az0;
-    r[4] = A.ph1; r[5] = A.ax1; r[6] = A.ay1; r[7] = A.az1;
-  }
-  __syncthreads();
-  if (tid < nt) {
-    const int sl = tid >> 1, h = tid & 1;
-    double v[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int gg = 0; gg < G; ++gg) {
-      const double* r = red + 8 * (gg * slots + sl) + 4 * h;
-      v[0] += r[0];
-      v[1] += r[1];
-      v[2] += r[2];
-      v[3] += r[3];
-    }
-    if (it.pbase < 0) {
-      const int32_t i = it.tb + tid;
-      phi_out[i] = v[0];
-      if (kAcc) {
-        acc_out[3 * i] = v[1];
-        acc_out[3 * i + 1] = v[2];
-        acc_out[3 * i + 2] = v[3];
-      }
-    } else {
-      double* p = partial + 4 * ((int64_t)it.pbase + tid);
-      p[0] = v[0];
-      p[1] = v[1];
-      p[2] = v[2];
-      p[3] = v[3];
-    }
-  }
-}
-
 // ------------------------------------------------ FP32 kernel, warp-specialised pipeline ----
-// Same work decomposition and arithmetic as k_p2p_fp32, without per-tile CTA barriers: a fifth
+// One CTA per work item, five warps, no per-tile CTA barriers: a fifth
 // (producer) warp resolves each tile's list entries, issues its TMA bulk copies, converts the
 // landed bodies into the target frame and publishes the tile on full[b]; the four consumer
 // warps compute and release the buffer on empty[b] (one arrival per warp). Consumers never wait
@@ -1162,10 +990,7 @@ void run_p2p(fmm_ctx* c, cudaStream_t s) {
   if (c->n_p2p_items > 0) {
     if (c->cfg.precision == FMM_PREC_FP32_P2P) {
       const P2PEnt* ent = reinterpret_cast<const P2PEnt*>(c->p2p_ent.p);
-#ifndef FMM_P2P_WS
-#define FMM_P2P_WS 1
-#endif
-      if (FMM_P2P_WS) {
+      {
         // optional dynamic shared-memory pad: caps the P2P CTAs per SM (room for concurrent M2L)
         static const int pad = [] {
           const char* e = std::getenv("FMM_P2P_PAD_KB");
@@ -1183,12 +1008,6 @@ void run_p2p(fmm_ctx* c, cudaStream_t s) {
         else
           k_p2p_fp32_ws<false><<<(unsigned)c->n_p2p_items, kWsThreads, pad, s>>>(items, ent, c->bodyf.p, c->bodyl.p,
                                                                                  phi, acc, c->p2p_partial.p);
-      } else if (wa) {
-        k_p2p_fp32<true><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p, phi,
-                                                                       acc, c->p2p_partial.p);
-      } else {
-        k_p2p_fp32<false><<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p, phi,
-                                                                        acc, c->p2p_partial.p);
       }
     } else {
       k_p2p_fp64<<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p,
@@ -1211,7 +1030,7 @@ namespace fmmb {
 namespace {
 // Operator-level P2P (kernels.cpp:181-192 + acc) over (target range, source range) pairs of one
 // body array; thread per target body. FP32 mode: coordinates relative to the target range's
-// first body, FP32 pair math, FP64 accumulation (the same arithmetic as k_p2p_fp32).
+// first body, FP32 pair math, FP64 accumulation (the arithmetic of k_p2p_fp32_ws's far tiles).
 __global__ void k_op_p2p(int64_t count, const int4* __restrict__ rng, const double4* __restrict__ b,
                          int precision, double* __restrict__ phi, double* __restrict__ acc) {
   const int64_t r = blockIdx.x;
