@@ -98,9 +98,16 @@ int fmm_create(const fmm_config* cfg, fmm_ctx** out) {
       set_device(c);
       int lo = 0, hi = 0;  // the expansion chain outranks P2P, which fills the SMs it leaves idle
       CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-      CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));
+      // priorities: P2P list preparation (stream3) > FMM stream > overlap stream (stream2)
+      const int mid = hi < lo ? hi + 1 : hi;
+      CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, mid));
       CK(cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, lo));
+      // P2P list preparation alongside M2L: small latency-bound kernels, scheduled at the
+      // highest priority so that they are not starved by the M2L CTAs
+      CK(cudaStreamCreateWithPriority(&c->stream3, cudaStreamNonBlocking, hi));
       for (int i = 0; i < EV_COUNT; ++i) CK(cudaEventCreate(&c->ev[i]));
+      CK(cudaEventCreateWithFlags(&c->ev_lists, cudaEventDisableTiming));
+      c->pstream = c->stream;
       CK(cudaMallocHost(&c->hpin, 64 * sizeof(int64_t)));
       c->d_counters.ensure(32);
     } catch (...) {
@@ -117,9 +124,11 @@ void fmm_destroy(fmm_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  if (ctx->ev_lists) cudaEventDestroy(ctx->ev_lists);
   if (ctx->own_stream) ctx->stream = ctx->own_stream;
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
+  if (ctx->stream3) cudaStreamDestroy(ctx->stream3);
   if (ctx->hpin) cudaFreeHost(ctx->hpin);
   delete ctx;
 }
@@ -227,42 +236,64 @@ void evaluate_impl(fmm_ctx* c, bool reuse) {
       fmmb::build_tree(c);
     }
     CK(cudaEventRecord(c->ev[EV_BUILD1], c->stream));
+    // overlap: the P2P list and work list are prepared on the second stream (after the upward
+    // pass) while M2L runs on the first; P2P waits for both
+    c->p2p_overlap = c->overlap >= 1 && !reuse;
+    c->pstream = c->stream;
     auto lists = [&] {
       if (!reuse) fmmb::traverse(c);
       else if (c->cfg.precision == FMM_PREC_FP32_P2P) fmmb::build_p2p_entries(c);
     };
-    if (c->overlap) {
-      // The upward pass needs only the tree: it runs on the second stream while the traversal
-      // (and its host round trips) proceeds on the first; M2L joins both.
-      CK(cudaStreamWaitEvent(c->stream2, c->ev[EV_BUILD1], 0));
-      fmmb::run_upward(c, c->stream2);
-      CK(cudaEventRecord(c->ev[EV_UP1], c->stream2));
-      lists();
-      CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
-      CK(cudaStreamWaitEvent(c->stream, c->ev[EV_UP1], 0));
-      CK(cudaEventRecord(c->ev[EV_FORK], c->stream));
-    } else {
-      lists();
-      CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
-      fmmb::run_upward(c, c->stream);
-      CK(cudaEventRecord(c->ev[EV_UP1], c->stream));
-      CK(cudaEventRecord(c->ev[EV_FORK], c->stream));
+    try {
+      if (c->overlap) {
+        // The upward pass needs only the tree: it runs on the second stream while the traversal
+        // (and its host round trips) proceeds on the first; M2L joins both.
+        CK(cudaStreamWaitEvent(c->stream2, c->ev[EV_BUILD1], 0));
+        fmmb::run_upward(c, c->stream2);
+        CK(cudaEventRecord(c->ev[EV_UP1], c->stream2));
+        lists();
+        CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
+        CK(cudaStreamWaitEvent(c->stream, c->ev[EV_UP1], 0));
+        CK(cudaEventRecord(c->ev[EV_FORK], c->stream));
+      } else {
+        lists();
+        CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
+        fmmb::run_upward(c, c->stream);
+        CK(cudaEventRecord(c->ev[EV_UP1], c->stream));
+        CK(cudaEventRecord(c->ev[EV_FORK], c->stream));
+      }
+      const bool split = c->p2p_pending;  // the work list is being prepared on stream2
+      if (c->overlap >= 2) {
+        // M2L (FP64 pipe) on the high-priority stream and P2P (FP32 pipe) on the low-priority
+        // one, concurrently: P2P CTAs fill what the M2L CTAs leave of each SM
+        do_m2l(c, c->stream);
+        CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
+        fmmb::p2p_worklist_end(c);
+        CK(cudaEventRecord(c->ev_lists, c->stream3));
+        CK(cudaStreamWaitEvent(c->stream2, c->ev_lists, 0));
+        CK(cudaStreamWaitEvent(c->stream2, c->ev[EV_FORK], 0));
+        do_p2p(c, c->stream2);
+        CK(cudaEventRecord(c->ev[EV_P2P1], c->stream2));
+        CK(cudaStreamWaitEvent(c->stream, c->ev[EV_P2P1], 0));
+      } else {
+        do_m2l(c, c->stream);
+        CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
+        if (split) {  // finish the work list (host syncs on stream3 while M2L runs), then join
+          fmmb::p2p_worklist_end(c);
+          CK(cudaEventRecord(c->ev_lists, c->stream3));
+          CK(cudaStreamWaitEvent(c->stream, c->ev_lists, 0));
+        }
+        do_p2p(c, c->stream);
+        CK(cudaEventRecord(c->ev[EV_P2P1], c->stream));
+      }
+    } catch (...) {
+      c->p2p_overlap = false;
+      c->p2p_pending = false;
+      c->pstream = c->stream;
+      throw;
     }
-    if (c->overlap >= 2) {
-      // M2L (FP64 pipe) on the high-priority stream and P2P (FP32 pipe) on the low-priority
-      // one, concurrently: P2P CTAs fill what the M2L CTAs leave of each SM
-      CK(cudaStreamWaitEvent(c->stream2, c->ev[EV_FORK], 0));
-      do_p2p(c, c->stream2);
-      CK(cudaEventRecord(c->ev[EV_P2P1], c->stream2));
-      do_m2l(c, c->stream);
-      CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
-      CK(cudaStreamWaitEvent(c->stream, c->ev[EV_P2P1], 0));
-    } else {
-      do_m2l(c, c->stream);
-      CK(cudaEventRecord(c->ev[EV_M2L1], c->stream));
-      do_p2p(c, c->stream);
-      CK(cudaEventRecord(c->ev[EV_P2P1], c->stream));
-    }
+    c->p2p_overlap = false;
+    c->pstream = c->stream;
     fmmb::run_downward(c, c->stream);
     CK(cudaEventRecord(c->ev[EV_DOWN1], c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -733,6 +764,7 @@ int fmm_set_stream(fmm_ctx* c, void* stream) {
     set_device(c);
     if (!c->own_stream) c->own_stream = c->stream;
     c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    c->pstream = c->stream;
   });
 }
 

@@ -25,7 +25,8 @@ struct fmm_ctx {
   fmm_config cfg{};
   int ncoef = 0;
   cudaStream_t stream = nullptr;
-  cudaStream_t stream2 = nullptr;  // concurrent stream (P2P alongside the expansion chain)
+  cudaStream_t stream2 = nullptr;  // concurrent stream (upward pass alongside the traversal)
+  cudaStream_t stream3 = nullptr;  // P2P list preparation alongside M2L (high priority)
   cudaStream_t own_stream = nullptr;  // the context's stream while a caller stream is set
   std::string err;
 
@@ -69,6 +70,16 @@ struct fmm_ctx {
   fmmb::DBuf<int4> p2p_ent;
   fmmb::DBuf<double4> leaf_lo, leaf_hi;  // tight body boxes of the leaves (FP32 P2P near test)
   fmmb::DBuf<int64_t> ent_cls, ent_pre;  // entry class counters (near | far << 32) and their scan
+  // P2P list preparation: its own stream slot and scratch (it may run concurrently with M2L)
+  cudaStream_t pstream = nullptr;        // = stream, or stream3 while evaluate overlaps it
+  bool p2p_overlap = false;              // set by evaluate: prepare the P2P work list on stream3
+  cudaEvent_t ev_lists = nullptr;        // emitted keys complete / P2P work list ready
+  bool p2p_pending = false;              // work list begun, not finished (p2p_worklist_end)
+  fmmb::DBuf<unsigned char> tmp2;        // CUB temporary storage of the P2P path
+  fmmb::DBuf<uint64_t> p2p_keys_b2, p2p_keys_c;
+  fmmb::DBuf<int32_t> p2p_i32a, p2p_i32b, p2p_i32c;
+  fmmb::DBuf<int64_t> p2p_sum;
+  fmmb::DBuf<int4> p2p_items_raw;
   fmmb::DBuf<int32_t> self_pos;          // per cell: CSR position of its self entry, -1 = none         // per P2P list entry: {body_begin, count, shift.xy} + {shift.z,...}
   int64_t n_p2p_reduce = 0;
 
@@ -158,7 +169,9 @@ void shard_unpack(fmm_ctx* c, const double* d_recv, cudaStream_t s);
 void plan_partition_host(int64_t ncells, const int32_t* bb, const int32_t* be, const int32_t* cc,
                          const double* cell_cost, int world, int64_t* bounds, int32_t* owner);
 // p2p.cu
-void build_p2p_worklist(fmm_ctx* c);
+void build_p2p_worklist(fmm_ctx* c);  // begin + end on c->pstream
+void p2p_worklist_begin(fmm_ctx* c);  // entry prefix, per-leaf sums, async read of the total
+void p2p_worklist_end(fmm_ctx* c);    // items, entries, cost sort (host syncs on c->pstream)
 void build_p2p_entries(fmm_ctx* c);  // FP32 entries (near test on the current bodies)
 void run_p2p(fmm_ctx* c, cudaStream_t s);
 // expansions.cu
@@ -166,8 +179,9 @@ void run_upward(fmm_ctx* c, cudaStream_t s, int mode = 0);  // 0 all, 1 own cell
 void run_m2l(fmm_ctx* c, cudaStream_t s);
 void run_downward(fmm_ctx* c, cudaStream_t s);  // L2L + L2P + combine with P2P part
 
-// CUB temp helper
+// CUB temp helpers (the second one belongs to the P2P preparation path)
 void* temp_storage(fmm_ctx* c, size_t bytes);
+void* temp_storage2(fmm_ctx* c, size_t bytes);
 
 }  // namespace fmmb
 

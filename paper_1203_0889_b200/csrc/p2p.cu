@@ -875,10 +875,10 @@ __global__ void k_iota(int32_t* __restrict__ v, int64_t n) {
   if (i < n) v[i] = static_cast<int32_t>(i);
 }
 
-void exclusive_scan_i32(fmm_ctx* c, const int32_t* in, int32_t* out, int64_t n) {
+void exclusive_scan_i32(fmm_ctx* c, const int32_t* in, int32_t* out, int64_t n, cudaStream_t s) {
   size_t sb = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, in, out, (int)n, c->stream));
-  CK(cub::DeviceScan::ExclusiveSum(temp_storage(c, sb), sb, in, out, (int)n, c->stream));
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, in, out, (int)n, s));
+  CK(cub::DeviceScan::ExclusiveSum(temp_storage2(c, sb), sb, in, out, (int)n, s));
 }
 
 }  // namespace
@@ -886,7 +886,7 @@ void exclusive_scan_i32(fmm_ctx* c, const int32_t* in, int32_t* out, int64_t n) 
 // FP32 P2P list entries (self / near / far order, FP32 hi + lo shifts): depend on the lists and,
 // through the near test, on the bodies' tight leaf boxes (rebuilt by a tree-reuse step)
 void build_p2p_entries(fmm_ctx* c) {
-  cudaStream_t s = c->stream;
+  cudaStream_t s = c->pstream;
   const int64_t ne = c->n_p2p;
   P2PEnt* ent = reinterpret_cast<P2PEnt*>(c->p2p_ent.ensure(2 * (ne + 1)));
   double4* blo = c->leaf_lo.ensure(c->ncells);
@@ -901,7 +901,7 @@ void build_p2p_entries(fmm_ctx* c) {
   {
     size_t sb = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, cls, epre, (int)(ne + 1), s));
-    CK(cub::DeviceScan::ExclusiveSum(temp_storage(c, sb), sb, cls, epre, (int)(ne + 1), s));
+    CK(cub::DeviceScan::ExclusiveSum(temp_storage2(c, sb), sb, cls, epre, (int)(ne + 1), s));
   }
   if (ne > 0)
     k_ent_write<<<ceil_div(ne, 256), 256, 0, s>>>(c->p2p_tgt.p, c->p2p_src.p, ne, c->p2p_off.p, cls, epre, spos,
@@ -910,25 +910,38 @@ void build_p2p_entries(fmm_ctx* c) {
   c->kernel_launches += 5;
 }
 
-void build_p2p_worklist(fmm_ctx* c) {
-  cudaStream_t s = c->stream;
+// P2P work list, in two halves around the host read of the total pair count, on the P2P
+// preparation stream (c->pstream) and with buffers of its own, so that evaluate can run it
+// concurrently with M2L (see capi.cu).
+void p2p_worklist_begin(fmm_ctx* c) {
+  cudaStream_t s = c->pstream;
   const int64_t nl = c->nwl, ne = c->n_p2p;
-  // source-body prefix over all list entries, and each entry's target
+  // source-body prefix over all list entries
   int64_t* pre = c->p2p_pre.ensure(ne + 2);
-  int64_t* cnt = reinterpret_cast<int64_t*>(c->keys_a.ensure(ne + 2));
+  int64_t* cnt = reinterpret_cast<int64_t*>(c->p2p_keys_c.ensure(ne + 2));
   k_entry_counts<<<ceil_div(ne + 1, 256), 256, 0, s>>>(c->p2p_src.p, ne, c->c_body_begin.p, c->c_body_end.p, cnt);
   {
     size_t sb = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, cnt, pre, (int)(ne + 1), s));
-    CK(cub::DeviceScan::ExclusiveSum(temp_storage(c, sb), sb, cnt, pre, (int)(ne + 1), s));
+    CK(cub::DeviceScan::ExclusiveSum(temp_storage2(c, sb), sb, cnt, pre, (int)(ne + 1), s));
   }
-  int64_t* sum_ns = c->scan_a.ensure(nl + 1);
+  int64_t* sum_ns = c->p2p_sum.ensure(nl + 1);
   unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->d_counters.ensure(16)) + 12;
   CK(cudaMemsetAsync(tot, 0, sizeof(unsigned long long), s));
   k_leaf_sum<<<ceil_div(nl, 256), 256, 0, s>>>(c->wl, nl, c->p2p_off.p, pre, c->c_body_begin.p, c->c_body_end.p,
                                                sum_ns, tot);
   CK_LAUNCH("k_leaf_sum");
   CK(cudaMemcpyAsync(c->hpin + 16, tot, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  c->kernel_launches += 3;
+  c->p2p_pending = true;
+}
+
+void p2p_worklist_end(fmm_ctx* c) {
+  if (!c->p2p_pending) return;
+  cudaStream_t s = c->pstream;
+  const int64_t nl = c->nwl;
+  int64_t* pre = c->p2p_pre.p;
+  int64_t* sum_ns = c->p2p_sum.p;
   CK(cudaStreamSynchronize(s));
   c->p2p_body_pairs = c->hpin[16];
   const uint64_t total = static_cast<uint64_t>(c->p2p_body_pairs);
@@ -937,27 +950,27 @@ void build_p2p_worklist(fmm_ctx* c) {
   uint64_t cmax = total / (148ull * 8ull);
   if (cmax < 65536ull) cmax = 65536ull;
 
-  int32_t* counts = c->i32_a.ensure(3 * (nl + 1));
-  int32_t* offs = c->i32_b.ensure(3 * (nl + 1));
+  int32_t* counts = c->p2p_i32a.ensure(3 * (nl + 1));
+  int32_t* offs = c->p2p_i32b.ensure(3 * (nl + 1));
   int32_t *nitems = counts, *nred = counts + (nl + 1), *npart = counts + 2 * (nl + 1);
   int32_t *item_off = offs, *red_off = offs + (nl + 1), *part_off = offs + 2 * (nl + 1);
   CK(cudaMemsetAsync(counts, 0, sizeof(int32_t) * 3 * (nl + 1), s));
   k_leaf_cost<<<ceil_div(nl, 256), 256, 0, s>>>(c->wl, nl, c->p2p_off.p, c->c_body_begin.p, c->c_body_end.p,
                                                 cmax, sum_ns, nitems, nred, npart);
   CK_LAUNCH("k_leaf_cost");
-  exclusive_scan_i32(c, nitems, item_off, nl + 1);
-  exclusive_scan_i32(c, nred, red_off, nl + 1);
-  exclusive_scan_i32(c, npart, part_off, nl + 1);
-  int32_t* h = reinterpret_cast<int32_t*>(c->hpin);
+  exclusive_scan_i32(c, nitems, item_off, nl + 1, s);
+  exclusive_scan_i32(c, nred, red_off, nl + 1, s);
+  exclusive_scan_i32(c, npart, part_off, nl + 1, s);
+  int32_t* h = reinterpret_cast<int32_t*>(c->hpin + 24);
   CK(cudaMemcpyAsync(&h[0], item_off + nl, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&h[1], red_off + nl, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&h[2], part_off + nl, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   const int64_t nitem = h[0], nr = h[1], np = h[2];
-  P2PItem* items_raw = reinterpret_cast<P2PItem*>(c->pairs_a.ensure(4 * (nitem + 1)));  // 32 B each
+  P2PItem* items_raw = reinterpret_cast<P2PItem*>(c->p2p_items_raw.ensure(2 * (nitem + 1)));  // 32 B each
   P2PItem* items = reinterpret_cast<P2PItem*>(c->p2p_items.ensure(2 * (nitem + 1)));
-  uint64_t* costs = c->keys_a.ensure(nitem + 1);
-  uint64_t* costs_sorted = c->keys_b.ensure(nitem + 1);
+  uint64_t* costs = c->p2p_keys_c.ensure(nitem + 1);
+  uint64_t* costs_sorted = c->p2p_keys_b2.ensure(nitem + 1);
   int4* red = c->p2p_reduce.ensure(nr + 1);
   c->p2p_partial.ensure(4 * (np + 1));
   k_write_items<<<ceil_div(nl, 128), 128, 0, s>>>(c->wl, nl, c->p2p_off.p, pre, c->c_body_begin.p,
@@ -966,22 +979,29 @@ void build_p2p_worklist(fmm_ctx* c) {
   CK_LAUNCH("k_write_items");
   if (c->cfg.precision == FMM_PREC_FP32_P2P) build_p2p_entries(c);
   // cost-sorted (descending, stable) work list: the longest items launch first
-  int32_t* ord_in = c->i32_c.ensure(2 * (nitem + 1));
+  int32_t* ord_in = c->p2p_i32c.ensure(2 * (nitem + 1));
   int32_t* ord_out = ord_in + (nitem + 1);
   k_iota<<<ceil_div(nitem, 256), 256, 0, s>>>(ord_in, nitem);
   size_t sb = 0;
   CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, costs, costs_sorted, ord_in, ord_out, (int)nitem, 0, 48, s));
-  CK(cub::DeviceRadixSort::SortPairsDescending(temp_storage(c, sb), sb, costs, costs_sorted, ord_in, ord_out,
+  CK(cub::DeviceRadixSort::SortPairsDescending(temp_storage2(c, sb), sb, costs, costs_sorted, ord_in, ord_out,
                                                (int)nitem, 0, 48, s));
   k_gather_items<<<ceil_div(nitem, 256), 256, 0, s>>>(items_raw, ord_out, nitem, items);
   CK_LAUNCH("k_gather_items");
   c->n_p2p_items = nitem;
   c->n_p2p_reduce = nr;
   c->kernel_launches += 6;
+  c->p2p_pending = false;
+}
+
+void build_p2p_worklist(fmm_ctx* c) {
+  p2p_worklist_begin(c);
+  p2p_worklist_end(c);
 }
 
 void run_p2p(fmm_ctx* c, cudaStream_t s) {
   if (!c->have_lists) fail(FMM_ERR_STATE, "p2p: no interaction lists");
+  if (c->p2p_pending) fail(FMM_ERR_STATE, "p2p: work list not finished");
   const int64_t n = c->N;
   const int wa = c->cfg.with_acc ? 1 : 0;
   double* phi = c->phi_p2p.ensure(n);

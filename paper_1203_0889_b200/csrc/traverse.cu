@@ -327,8 +327,9 @@ inline bool keys32(const fmm_ctx* c) { return !c->cfg.mutual && small_keys(c->nc
 
 template <class KeyT>
 void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int32_t>& src, uint8_t* mir,
-                 int32_t* tgt = nullptr) {
-  cudaStream_t s = c->stream;
+                 int32_t* tgt = nullptr, bool p2p_path = false) {
+  // the P2P list uses the P2P preparation stream and scratch (it may overlap the M2L path)
+  cudaStream_t s = p2p_path ? c->pstream : c->stream;
   const int64_t nc = c->ncells;
   off.ensure(nc + 1);
   src.ensure(n > 0 ? n : 1);
@@ -337,13 +338,14 @@ void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int
     return;
   }
   const int sbits = bits_for(static_cast<uint64_t>(nc));
-  KeyT* kb = reinterpret_cast<KeyT*>(c->keys_b.ensure(n));
+  KeyT* kb = reinterpret_cast<KeyT*>(p2p_path ? c->p2p_keys_b2.ensure(n) : c->keys_b.ensure(n));
   size_t sb = 0;
   // 64-bit keys come in a deterministic order (ordered emission / given pairs): a stable sort on
   // the target bits keeps it within each target; 32-bit keys: the full (target, source) sort
   const int b0 = sizeof(KeyT) == 8 ? sbits : 0;
   CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys, kb, (int)n, b0, 2 * sbits, s));
-  CK(cub::DeviceRadixSort::SortKeys(temp_storage(c, sb), sb, keys, kb, (int)n, b0, 2 * sbits, s));
+  CK(cub::DeviceRadixSort::SortKeys(p2p_path ? temp_storage2(c, sb) : temp_storage(c, sb), sb, keys, kb, (int)n, b0,
+                                    2 * sbits, s));
   k_csr_from_keys<<<ceil_div(n + 1, 256), 256, 0, s>>>(kb, n, sbits, nc, off.p, src.p, mir, tgt);
   CK_LAUNCH("keys_to_csr");
   c->kernel_launches += 3;
@@ -370,6 +372,15 @@ void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
   cudaStream_t s = c->stream;
   c->n_m2l_emit = n_m2l;
   c->n_p2p_emit = n_p2p;
+  // The P2P list and work list may be prepared on the second stream, concurrently with the M2L
+  // list and kernel (evaluate with overlap, single rank, non-mutual: c->p2p_overlap). Sharded
+  // runs plan from both lists and mutual runs read both lengths back: one stream.
+  const bool split = c->p2p_overlap && c->world == 1 && !c->cfg.mutual;
+  c->pstream = split ? c->stream3 : c->stream;
+  if (split) {
+    CK(cudaEventRecord(c->ev_lists, s));  // the emitted keys are complete
+    CK(cudaStreamWaitEvent(c->pstream, c->ev_lists, 0));
+  }
   if (c->cfg.mutual) {
     // symmetrise (emitted + mirrored), then the same canonical CSR; off[ncells] of each list is
     // its executed length (self pairs have no mirror), read back with the M2L target count
@@ -381,19 +392,19 @@ void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
     CK_LAUNCH("k_mirror_keys");
     keys_to_csr(c, dm, 2 * n_m2l, c->m2l_off, c->m2l_src, c->m2l_mir.ensure(2 * n_m2l + 1));
     keys_to_csr(c, dp, 2 * n_p2p, c->p2p_off, c->p2p_src, c->p2p_mir.ensure(2 * n_p2p + 1),
-                c->p2p_tgt.ensure(2 * n_p2p + 1));
+                c->p2p_tgt.ensure(2 * n_p2p + 1), true);
     CK(cudaMemcpyAsync(c->hpin + 2, c->m2l_off.p + c->ncells, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->hpin + 3, c->p2p_off.p + c->ncells, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     n_m2l = c->hpin[2];
     n_p2p = c->hpin[3];
   } else if (keys32(c)) {
-    keys_to_csr(c, reinterpret_cast<uint32_t*>(c->m2l_keys.p), n_m2l, c->m2l_off, c->m2l_src, nullptr);
     keys_to_csr(c, reinterpret_cast<uint32_t*>(c->p2p_keys.p), n_p2p, c->p2p_off, c->p2p_src, nullptr,
-                c->p2p_tgt.ensure(n_p2p + 1));
+                c->p2p_tgt.ensure(n_p2p + 1), true);
+    keys_to_csr(c, reinterpret_cast<uint32_t*>(c->m2l_keys.p), n_m2l, c->m2l_off, c->m2l_src, nullptr);
   } else {
+    keys_to_csr(c, c->p2p_keys.p, n_p2p, c->p2p_off, c->p2p_src, nullptr, c->p2p_tgt.ensure(n_p2p + 1), true);
     keys_to_csr(c, c->m2l_keys.p, n_m2l, c->m2l_off, c->m2l_src, nullptr);
-    keys_to_csr(c, c->p2p_keys.p, n_p2p, c->p2p_off, c->p2p_src, nullptr, c->p2p_tgt.ensure(n_p2p + 1));
   }
   c->n_m2l = n_m2l;
   c->n_p2p = n_p2p;
@@ -405,6 +416,7 @@ void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
     c->shard_b0 = 0;
     c->shard_b1 = c->N;
   }
+  if (split) p2p_worklist_begin(c);  // queued on the second stream before the M2L host sync
   int32_t* flag = c->i32_c.ensure(c->ncells);
   k_flag_nonempty<<<ceil_div(c->ncells, 256), 256, 0, s>>>(c->m2l_off.p, c->ncells, c->c_body_begin.p,
                                                            c->c_body_end.p, c->shard_b0, c->shard_b1, flag);
@@ -421,7 +433,7 @@ void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
   c->n_m2l_targets = h[0];
   c->kernel_launches += 3;
   c->have_lists = true;
-  build_p2p_worklist(c);
+  if (!split) build_p2p_worklist(c);  // else finished by the caller (p2p_worklist_end)
 }
 
 void traverse(fmm_ctx* c) {

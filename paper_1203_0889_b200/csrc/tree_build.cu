@@ -315,6 +315,7 @@ int bits_for(uint64_t v) {
 }  // namespace
 
 void* temp_storage(fmm_ctx* c, size_t bytes) { return c->tmp.ensure(bytes > 0 ? bytes : 1); }
+void* temp_storage2(fmm_ctx* c, size_t bytes) { return c->tmp2.ensure(bytes > 0 ? bytes : 1); }
 
 void build_tree(fmm_ctx* c) {
   if (!c->have_bodies) fail(FMM_ERR_STATE, "build_tree: no bodies set");
