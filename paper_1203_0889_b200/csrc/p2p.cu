@@ -360,6 +360,11 @@ __device__ __forceinline__ void tile_compute_prec(const float4* __restrict__ buf
 #ifndef FMM_P2P_MIN_BLOCKS
 #define FMM_P2P_MIN_BLOCKS 6
 #endif
+// near test: tight body boxes closer than this fraction of (r_t + r_s) on every axis (the far
+// entries' pairs then have a relative FP32 distance error below ~1.4e-5)
+#ifndef FMM_P2P_NEAR_GAP
+#define FMM_P2P_NEAR_GAP 0.02
+#endif
 // ------------------------------------------------ FP32 kernel, warp-specialised pipeline ----
 // One CTA per work item, five warps, no per-tile CTA barriers: a fifth
 // (producer) warp resolves each tile's list entries, issues its TMA bulk copies, converts the
@@ -760,12 +765,12 @@ __global__ void k_write_items(const int32_t* __restrict__ leaves, int64_t nleave
 
 // P2P list entries: {source body range, kind, FP64 centre shift into the target leaf frame as
 // FP32 hi + lo}. Within each target's (source-sorted) list the order is
-// self entry, near entries, far entries (each group ascending by source), so that a work item's
+// far entries, near entries, self entry (each group ascending by source), so that a work item's
 // tiles each hold one class: only the self tile runs the r^2 == 0 guard and only self / near
 // tiles pay for compensated coordinates. Near = the tight body boxes of the two leaves are less
-// than 0.05 (r_t + r_s) apart along every axis; a far entry's body pairs are then at least that
-// far apart, and FP32 offsets (magnitude <= ~4.5 (r_t + r_s) in the target frame) give them a
-// relative distance error below ~5e-6.
+// than FMM_P2P_NEAR_GAP (r_t + r_s) apart along every axis; a far entry's body pairs are then at
+// least that far apart, and FP32 offsets (magnitude <= ~4.5 (r_t + r_s) in the target frame)
+// give them a relative distance error below ~1.4e-5.
 // Items still partition the list positions, so every entry is computed exactly once.
 __device__ __forceinline__ bool near_leaf(const double4 tlo, const double4 thi, const double4 slo, const double4 shi,
                                           double lim) {
@@ -824,7 +829,7 @@ __global__ void k_ent_class(const int32_t* __restrict__ tgt, const int32_t* __re
     self_pos[t] = static_cast<int32_t>(k);
     v = 0;
   } else {
-    const bool nr = near_leaf(blo[t], bhi[t], blo[s], bhi[s], 0.05 * (cr[t].w + cr[s].w));
+    const bool nr = near_leaf(blo[t], bhi[t], blo[s], bhi[s], FMM_P2P_NEAR_GAP * (cr[t].w + cr[s].w));
     v = nr ? 1ll : (1ll << 32);
   }
   cls[k] = v;
@@ -844,15 +849,18 @@ __global__ void k_ent_write(const int32_t* __restrict__ tgt, const int32_t* __re
   const int64_t lo0 = P0 & 0xffffffffll, hi0 = P0 >> 32;
   int64_t pos;
   int kind;
+  // far entries first, then near, the self entry last: an item's short compensated tiles come
+  // after its full far tiles, so the producer stages them while the consumers are busy
+  (void)hs;
   if (s == t) {
-    pos = l0;
+    pos = l1 - 1;
     kind = kKindSelf;
   } else if (v == 1) {
-    pos = l0 + hs + ((Pk & 0xffffffffll) - lo0);
+    const int64_t nfar = (pre[l1] >> 32) - hi0;
+    pos = l0 + nfar + ((Pk & 0xffffffffll) - lo0);
     kind = kKindNear;
   } else {
-    const int64_t nnear = (pre[l1] & 0xffffffffll) - lo0;
-    pos = l0 + hs + nnear + ((Pk >> 32) - hi0);
+    pos = l0 + ((Pk >> 32) - hi0);
     kind = kKindFar;
   }
   const double4 ct = cr[t], cs = cr[s];
