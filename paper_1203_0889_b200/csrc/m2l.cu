@@ -358,57 +358,6 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
   });
 }
 
-// --------------------------------------------------------------- shared-memory M2L (p >= 7) ----
-// The same harmonic reduction as the register kernel (p = 10: 2 035 terms instead of 5 005,
-// 136 derivatives instead of 220, 100 accumulators instead of 220). Lane = source, warp =
-// target (grid-stride over targets; a fixed pool of warps). The lane's Dt row (g_c <= 2) lives
-// in shared memory (odd stride: conflict-free); its detraced source row is read through L1;
-// Lambda (b_c <= 1) is accumulated in register blocks of kBlk coefficients that round-trip
-// through an L2-resident scratch row per (warp slot, lane). The 32 partial rows are reduced
-// once per target, then the c >= 2 entries follow from the trace identity.
-template <int P>
-struct BigCfg {
-  static constexpr int N = MI<P>::N;
-  static constexpr int NA = HM<P>::NA, NG = HM<P>::NG;
-  static constexpr int S = odd_stride(NG);
-#ifndef FMM_BIG_WARPS
-#define FMM_BIG_WARPS 6
-#endif
-#ifndef FMM_BIG_BLK
-#define FMM_BIG_BLK 32
-#endif
-  static constexpr int kWarps = FMM_BIG_WARPS;
-  static constexpr int kBlk = FMM_BIG_BLK;
-  static constexpr int kBlocks = (NA + kBlk - 1) / kBlk;
-};
-
-// Dt_g for g_c <= 2 into a shared-memory row (compact HM::g_of order), scaled recurrence
-template <int P>
-__device__ __forceinline__ void derivs_row_h(double rx, double ry, double rz, double* row) {
-  using T = MI<P>;
-  using H = HM<P>;
-  const double r2 = (rx * rx + ry * ry) + rz * rz;
-  const double d0 = rsqrt(r2);
-  const double inv_r2 = d0 * d0;
-  row[0] = d0;
-  static_for<T::N>([&](auto I) {
-    constexpr int i = decltype(I)::value;
-    constexpr int a = T::ea(i), b = T::eb(i), c = T::ec(i), n = T::deg(i);
-    if constexpr (i > 0 && c <= 2) {
-      constexpr double cn = double(n - 1) / double(2 * n - 1);
-      constexpr double an = -double(2 * n - 1) / double(n);
-      double acc = 0.0;
-      if constexpr (a >= 1) acc = fma(double(a) * rx, row[H::g_of(index_of(a - 1, b, c))], acc);
-      if constexpr (b >= 1) acc = fma(double(b) * ry, row[H::g_of(index_of(a, b - 1, c))], acc);
-      if constexpr (c >= 1) acc = fma(double(c) * rz, row[H::g_of(index_of(a, b, c - 1))], acc);
-      if constexpr (a >= 2) acc = fma(double(a * (a - 1)) * cn, row[H::g_of(index_of(a - 2, b, c))], acc);
-      if constexpr (b >= 2) acc = fma(double(b * (b - 1)) * cn, row[H::g_of(index_of(a, b - 2, c))], acc);
-      if constexpr (c >= 2) acc = fma(double(c * (c - 1)) * cn, row[H::g_of(index_of(a, b, c - 2))], acc);
-      row[H::g_of(i)] = (an * inv_r2) * acc;
-    }
-  });
-}
-
 // Lambda (compact, lanes reduced) -> full reference-order Lambda by the trace identity, then
 // L_b += (-1)^{|b|}/b! Lambda_b. cmp: NA reduced values, full: N doubles of scratch (smem).
 template <int P>
@@ -439,82 +388,6 @@ __device__ __forceinline__ void trace_fill_store(int lane, const double* cmp, do
     constexpr double w = ((T::deg(i) & 1) ? -1.0 : 1.0) / T::fact(i);
     if (lane == i % 32) Lt[i] += w * full[i];
   });
-}
-
-template <int P>
-__global__ void __launch_bounds__(32 * BigCfg<P>::kWarps)
-k_m2l_big(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* __restrict__ off,
-          const int32_t* __restrict__ src, const double4* __restrict__ cr, const double* __restrict__ Mt,
-          const double* __restrict__ zero_row, double* __restrict__ L, double* __restrict__ scratch) {
-  using T = MI<P>;
-  using H = HM<P>;
-  using C = BigCfg<P>;
-  constexpr int N = C::N, NA = C::NA, S = C::S;
-  extern __shared__ double smem[];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* wsm = smem + (size_t)w * 32 * S;  // the warp's 32 Dt rows (epilogue: cmp + full)
-  double* myD = wsm + lane * S;
-  const int64_t slot = blockIdx.x * (int64_t)C::kWarps + w;
-  const int64_t nslots = (int64_t)gridDim.x * C::kWarps;
-  double* part = scratch + (slot * 32 + lane) * (int64_t)NA;  // this lane's partial Lambda row
-  double* rows = scratch + slot * 32 * (int64_t)NA;           // the warp's 32 rows
-  for (int64_t wid = slot; wid < ntargets; wid += nslots) {
-    const int32_t t = targets[wid];
-    const double4 ct = cr[t];
-    const int64_t l0 = off[t], l1 = off[t + 1];
-    for (int i = 0; i < NA; ++i) part[i] = 0.0;
-    for (int64_t base = l0; base < l1; base += 32) {
-      const int64_t k = base + lane;
-      const bool valid = k < l1;
-      const int32_t s = valid ? src[k] : t;
-      double rx = 1.0, ry = 0.0, rz = 0.0;
-      if (valid) {
-        const double4 cs = cr[s];
-        rx = cs.x - ct.x;  // R = source centre - target centre (traversal.hpp:146)
-        ry = cs.y - ct.y;
-        rz = cs.z - ct.z;
-      }
-      derivs_row_h<P>(rx, ry, rz, myD);
-      const double* Ms = valid ? Mt + (int64_t)s * NA : zero_row;
-      static_for<C::kBlocks>([&](auto BI) {
-        constexpr int b0 = decltype(BI)::value * C::kBlk;
-        constexpr int b1 = (b0 + C::kBlk < NA) ? b0 + C::kBlk : NA;
-        double lam[b1 - b0];
-#pragma unroll
-        for (int j = 0; j < b1 - b0; ++j) lam[j] = part[b0 + j];
-        static_for<NA>([&](auto KA) {
-          constexpr int ka = decltype(KA)::value;
-          constexpr int ia = H::a_full(ka);
-          constexpr int aa = T::ea(ia), ab = T::eb(ia), ac = T::ec(ia), da = T::deg(ia);
-          if constexpr (da + T::deg(H::a_full(b0)) <= P - 1) {
-            // keep the multipole loads from being hoisted en masse (register pressure)
-            if constexpr (ka % 8 == 0) __syncwarp();
-            const double m = __ldg(Ms + ka);
-            static_for<b1 - b0>([&](auto J) {
-              constexpr int ib = H::a_full(b0 + decltype(J)::value);
-              if constexpr (da + T::deg(ib) <= P - 1) {
-                constexpr int ig = H::g_of(index_of(aa + T::ea(ib), ab + T::eb(ib), ac + T::ec(ib)));
-                lam[decltype(J)::value] = fma(m, myD[ig], lam[decltype(J)::value]);
-              }
-            });
-          }
-        });
-#pragma unroll
-        for (int j = 0; j < b1 - b0; ++j) part[b0 + j] = lam[j];
-      });
-    }
-    __syncwarp();
-    double* cmp = wsm;           // NA reduced values
-    double* full = wsm + NA + 1;  // N values (32 * S >= NA + N + 1)
-    for (int kk = lane; kk < NA; kk += 32) {
-      double acc = 0.0;
-      for (int j = 0; j < 32; ++j) acc += rows[(int64_t)j * NA + kk];
-      cmp[kk] = acc;
-    }
-    __syncwarp();
-    trace_fill_store<P>(lane, cmp, full, L + (int64_t)t * N);
-    __syncwarp();
-  }
 }
 
 // ------------------------------------------------- staged-row M2L (p >= 7), v2 ----
@@ -770,69 +643,39 @@ struct M2L {
                                                                     c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
       CK_LAUNCH("k_m2l_reg");
       c->kernel_launches += 2;
-      return;
+    } else {  // p >= 7 (only these orders instantiate the staged-row kernel)
+    using C2 = BigCfg2<P>;
+    const size_t smem2 = C2::kSmemPerWarp * C2::kWarps;
+    static bool attr2 = false;
+    if (!attr2) {
+      CK(cudaFuncSetAttribute(k_m2l_big2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      attr2 = true;
     }
-#ifndef FMM_M2L_BIG_V2
-#define FMM_M2L_BIG_V2 1
-#endif
-    if (FMM_M2L_BIG_V2) {
-      using C2 = BigCfg2<P>;
-      const size_t smem2 = C2::kSmemPerWarp * C2::kWarps;
-      static bool attr2 = false;
-      if (!attr2) {
-        CK(cudaFuncSetAttribute(k_m2l_big2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-        attr2 = true;
-      }
-      if (c->n_m2l_targets == 0) return;
-      double* Mt = c->m2l_mt.ensure(c->ncells * C2::NA + 1);
-      launch_detrace<P>(c, Mt, s);
-      const int32_t* tg = c->m2l_targets.p;
+    if (c->n_m2l_targets == 0) return;
+    double* Mt = c->m2l_mt.ensure(c->ncells * C2::NA + 1);
+    launch_detrace<P>(c, Mt, s);
+    const int32_t* tg = c->m2l_targets.p;
 #ifndef FMM_BIG2_SORT
 #define FMM_BIG2_SORT 1
 #endif
-      if (C2::kWarps > 1 && FMM_BIG2_SORT) {
-        const int64_t nt = c->n_m2l_targets;
-        uint32_t* kin = reinterpret_cast<uint32_t*>(c->keys_a.ensure(nt + 1));
-        uint32_t* kout = reinterpret_cast<uint32_t*>(c->keys_b.ensure(nt + 1));
-        int32_t* tout = c->i32_b.ensure(nt + 1);
-        k_target_chunks<<<ceil_div(nt, 256), 256, 0, s>>>(c->m2l_targets.p, nt, c->m2l_off.p, kin);
-        size_t sb = 0;
-        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, kin, kout, c->m2l_targets.p, tout, (int)nt, 0, 16, s));
-        CK(cub::DeviceRadixSort::SortPairsDescending(temp_storage(c, sb), sb, kin, kout, c->m2l_targets.p, tout,
-                                                     (int)nt, 0, 16, s));
-        tg = tout;
-        c->kernel_launches += 4;
-      }
-      k_m2l_big2<P><<<(unsigned)ceil_div(c->n_m2l_targets, C2::kWarps), 32 * C2::kWarps, smem2, s>>>(
-          tg, c->n_m2l_targets, c->m2l_off.p, c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
-      CK_LAUNCH("k_m2l_big2");
-      c->kernel_launches += 2;
-      return;
+    if (C2::kWarps > 1 && FMM_BIG2_SORT) {
+      const int64_t nt = c->n_m2l_targets;
+      uint32_t* kin = reinterpret_cast<uint32_t*>(c->keys_a.ensure(nt + 1));
+      uint32_t* kout = reinterpret_cast<uint32_t*>(c->keys_b.ensure(nt + 1));
+      int32_t* tout = c->i32_b.ensure(nt + 1);
+      k_target_chunks<<<ceil_div(nt, 256), 256, 0, s>>>(c->m2l_targets.p, nt, c->m2l_off.p, kin);
+      size_t sb = 0;
+      CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, kin, kout, c->m2l_targets.p, tout, (int)nt, 0, 16, s));
+      CK(cub::DeviceRadixSort::SortPairsDescending(temp_storage(c, sb), sb, kin, kout, c->m2l_targets.p, tout,
+                                                   (int)nt, 0, 16, s));
+      tg = tout;
+      c->kernel_launches += 4;
     }
-    using C = BigCfg<P>;
-    const size_t smem = sizeof(double) * C::kWarps * 32 * C::S;
-    static bool attr_set = false;
-    if (!attr_set) {
-      CK(cudaFuncSetAttribute(k_m2l_big<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_set = true;
+    k_m2l_big2<P><<<(unsigned)ceil_div(c->n_m2l_targets, C2::kWarps), 32 * C2::kWarps, smem2, s>>>(
+        tg, c->n_m2l_targets, c->m2l_off.p, c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
+    CK_LAUNCH("k_m2l_big2");
+    c->kernel_launches += 2;
     }
-    if (c->n_m2l_targets == 0) return;
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_m2l_big<P>, 32 * C::kWarps, smem));
-    int sms = 148;
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->cfg.device));
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * std::max(per_sm, 1),
-                                                               (c->n_m2l_targets + C::kWarps - 1) / C::kWarps));
-    double* scratch = c->m2l_scratch.ensure((size_t)grid * C::kWarps * 32 * C::NA + C::NA);
-    double* zero_row = scratch + (size_t)grid * C::kWarps * 32 * C::NA;
-    CK(cudaMemsetAsync(zero_row, 0, sizeof(double) * C::NA, s));
-    double* Mt = c->m2l_mt.ensure(c->ncells * C::NA + 1);
-    launch_detrace<P>(c, Mt, s);
-    k_m2l_big<P><<<(unsigned)grid, 32 * C::kWarps, smem, s>>>(c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p,
-                                                              c->m2l_src.p, c->c_cr.p, Mt, zero_row, c->L.p,
-                                                              scratch);
-    CK_LAUNCH("k_m2l_big");
-    c->kernel_launches += 3;
   }
 };
 

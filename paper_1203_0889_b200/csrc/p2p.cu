@@ -18,7 +18,6 @@
 // Each tile's FP32 partial sums are folded into FP64 per-target accumulators ("FP64-checked
 // accumulation").
 #include <cub/cub.cuh>
-#include <cstdlib>
 
 #include "context.cuh"
 #include "tma.cuh"
@@ -1018,25 +1017,12 @@ void run_p2p(fmm_ctx* c, cudaStream_t s) {
   if (c->n_p2p_items > 0) {
     if (c->cfg.precision == FMM_PREC_FP32_P2P) {
       const P2PEnt* ent = reinterpret_cast<const P2PEnt*>(c->p2p_ent.p);
-      {
-        // optional dynamic shared-memory pad: caps the P2P CTAs per SM (room for concurrent M2L)
-        static const int pad = [] {
-          const char* e = std::getenv("FMM_P2P_PAD_KB");
-          return e ? std::atoi(e) * 1024 : 0;
-        }();
-        static bool attr = false;
-        if (!attr && pad > 0) {
-          CK(cudaFuncSetAttribute(k_p2p_fp32_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad));
-          CK(cudaFuncSetAttribute(k_p2p_fp32_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad));
-          attr = true;
-        }
-        if (wa)
-          k_p2p_fp32_ws<true><<<(unsigned)c->n_p2p_items, kWsThreads, pad, s>>>(items, ent, c->bodyf.p, c->bodyl.p,
-                                                                                phi, acc, c->p2p_partial.p);
-        else
-          k_p2p_fp32_ws<false><<<(unsigned)c->n_p2p_items, kWsThreads, pad, s>>>(items, ent, c->bodyf.p, c->bodyl.p,
-                                                                                 phi, acc, c->p2p_partial.p);
-      }
+      if (wa)
+        k_p2p_fp32_ws<true><<<(unsigned)c->n_p2p_items, kWsThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p, phi,
+                                                                            acc, c->p2p_partial.p);
+      else
+        k_p2p_fp32_ws<false><<<(unsigned)c->n_p2p_items, kWsThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p, phi,
+                                                                             acc, c->p2p_partial.p);
     } else {
       k_p2p_fp64<<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p,
                                                               c->bodies.p, phi, acc, c->p2p_partial.p, wa);

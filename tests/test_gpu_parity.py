@@ -361,6 +361,19 @@ def test_time_step_tree_reuse(fmmlib, orc, precision):
         x.close()
 
 
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 7, 9])
+def test_pipeline_other_orders(fmmlib, orc, p):
+    """The orders the BASELINE configs do not use (each M2L / expansion kernel is instantiated
+    per order): FP64 pipeline against the oracle."""
+    bodies = fmmlib.generate_bodies(3, 6000, 20 + p)
+    t = oracle_run(orc, bodies, 32, p, 0.5)
+    ctx = run_gpu(fmmlib, bodies, 32, p, 0.5, "fp64")
+    phi, acc = ctx.results("tree")
+    assert rel_l2(phi, t.phi()) <= 1e-6, (p, rel_l2(phi, t.phi()))
+    assert rel_l2(acc, t.acc()) <= 1e-6, (p, rel_l2(acc, t.acc()))
+    ctx.close()
+
+
 def test_tree_reuse_across_distributions(fmmlib, orc):
     """One context, successive body sets of growing depth: the partial-digit sort keyed on the
     previous depth must fall back to the full sort (and the level batches must continue) so that
