@@ -109,6 +109,7 @@ int fmm_create(const fmm_config* cfg, fmm_ctx** out) {
       CK(cudaStreamCreateWithPriority(&c->stream3, cudaStreamNonBlocking, hi));
       for (int i = 0; i < EV_COUNT; ++i) CK(cudaEventCreate(&c->ev[i]));
       CK(cudaEventCreateWithFlags(&c->ev_lists, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_l2l, cudaEventDisableTiming));
       c->pstream = c->stream;
       CK(cudaMallocHost(&c->hpin, 64 * sizeof(int64_t)));
       c->d_counters.ensure(32);
@@ -127,6 +128,7 @@ void fmm_destroy(fmm_ctx* ctx) {
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->ev_lists) cudaEventDestroy(ctx->ev_lists);
+  if (ctx->ev_l2l) cudaEventDestroy(ctx->ev_l2l);
   if (ctx->own_stream) ctx->stream = ctx->own_stream;
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
@@ -285,8 +287,15 @@ void evaluate_impl(fmm_ctx* c, bool reuse) {
           CK(cudaEventRecord(c->ev_lists, c->stream3));
           CK(cudaStreamWaitEvent(c->stream, c->ev_lists, 0));
         }
+        if (c->overlap) {  // L2L needs only the locals: it runs beside P2P on the highest-priority
+                           // stream (its small level launches get the SM slots P2P CTAs free)
+          CK(cudaStreamWaitEvent(c->stream3, c->ev[EV_M2L1], 0));
+          fmmb::run_downward(c, c->stream3, 1);
+          CK(cudaEventRecord(c->ev_l2l, c->stream3));
+        }
         do_p2p(c, c->stream);
         CK(cudaEventRecord(c->ev[EV_P2P1], c->stream));
+        if (c->overlap) CK(cudaStreamWaitEvent(c->stream, c->ev_l2l, 0));
       }
     } catch (...) {
       c->p2p_overlap = false;
@@ -296,7 +305,7 @@ void evaluate_impl(fmm_ctx* c, bool reuse) {
     }
     c->p2p_overlap = false;
     c->pstream = c->stream;
-    fmmb::run_downward(c, c->stream);
+    fmmb::run_downward(c, c->stream, (c->overlap == 1) ? 2 : 3);
     CK(cudaEventRecord(c->ev[EV_DOWN1], c->stream));
     CK(cudaStreamSynchronize(c->stream));
     fmm_stage_times& t = c->times;

@@ -74,6 +74,7 @@ struct fmm_ctx {
   cudaStream_t pstream = nullptr;        // = stream, or stream3 while evaluate overlaps it
   bool p2p_overlap = false;              // set by evaluate: prepare the P2P work list on stream3
   cudaEvent_t ev_lists = nullptr;        // emitted keys complete / P2P work list ready
+  cudaEvent_t ev_l2l = nullptr;          // L2L done (it runs beside P2P)
   bool p2p_pending = false;              // work list begun, not finished (p2p_worklist_end)
   fmmb::DBuf<unsigned char> tmp2;        // CUB temporary storage of the P2P path
   fmmb::DBuf<uint64_t> p2p_keys_b2, p2p_keys_c;
@@ -177,7 +178,7 @@ void run_p2p(fmm_ctx* c, cudaStream_t s);
 // expansions.cu
 void run_upward(fmm_ctx* c, cudaStream_t s, int mode = 0);  // 0 all, 1 own cells, 2 shared cells
 void run_m2l(fmm_ctx* c, cudaStream_t s);
-void run_downward(fmm_ctx* c, cudaStream_t s);  // L2L + L2P + combine with P2P part
+void run_downward(fmm_ctx* c, cudaStream_t s, int part = 3);  // 1: L2L, 2: L2P + combine, 3: both
 
 // CUB temp helpers (the second one belongs to the P2P preparation path)
 void* temp_storage(fmm_ctx* c, size_t bytes);

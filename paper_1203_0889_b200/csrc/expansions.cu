@@ -368,25 +368,28 @@ struct Upward {
 
 template <int P>
 struct Downward {
-  static void run(fmm_ctx* c, cudaStream_t s) {
-    const int N = MI<P>::N;
+  // part 1: L2L, level by level (needs only the locals: may run beside P2P); part 2: L2P and the
+  // near-field combine (needs the P2P result)
+  static void run(fmm_ctx* c, cudaStream_t s, int part) {
     int launches = 0;
-    for (int l = 1; l <= c->depth; ++l) {
-      const int32_t b = c->level_start[l], e = c->level_start[l + 1];
-      if (e <= b) continue;
-      const int grid = std::min(ceil_div(e - b, 4), 148 * kSweepBlocksPerSM);
-      k_l2l<P><<<grid, 128, 0, s>>>(b, e, c->c_parent.p, c->c_cr.p, c->L.p);
-      CK_LAUNCH("k_l2l");
+    if (part & 1)
+      for (int l = 1; l <= c->depth; ++l) {
+        const int32_t b = c->level_start[l], e = c->level_start[l + 1];
+        if (e <= b) continue;
+        const int grid = std::min(ceil_div(e - b, 4), 148 * kSweepBlocksPerSM);
+        k_l2l<P><<<grid, 128, 0, s>>>(b, e, c->c_parent.p, c->c_cr.p, c->L.p);
+        CK_LAUNCH("k_l2l");
+        ++launches;
+      }
+    if ((part & 2) && c->nwl > 0) {
+      k_l2p<P><<<ceil_div(c->nwl, 4), 128, 0, s>>>(c->wl, c->nwl, c->c_body_begin.p, c->c_body_end.p, c->c_cr.p,
+                                                   c->bodies.p, c->L.p, c->phi_p2p.p, c->acc_p2p.p,
+                                                   c->phi.ensure(c->N), c->acc.ensure(3 * c->N),
+                                                   c->cfg.with_acc ? 1 : 0);
+      CK_LAUNCH("k_l2p");
       ++launches;
     }
-    (void)N;
-    if (c->nwl > 0)
-    k_l2p<P><<<ceil_div(c->nwl, 4), 128, 0, s>>>(c->wl, c->nwl, c->c_body_begin.p, c->c_body_end.p,
-                                                     c->c_cr.p, c->bodies.p, c->L.p, c->phi_p2p.p, c->acc_p2p.p,
-                                                     c->phi.ensure(c->N), c->acc.ensure(3 * c->N),
-                                                     c->cfg.with_acc ? 1 : 0);
-    CK_LAUNCH("k_l2p");
-    c->kernel_launches += launches + 1;
+    c->kernel_launches += launches;
   }
 };
 
@@ -399,10 +402,10 @@ void run_upward(fmm_ctx* c, cudaStream_t s, int mode) {
   c->have_M = true;
 }
 
-void run_downward(fmm_ctx* c, cudaStream_t s) {
+void run_downward(fmm_ctx* c, cudaStream_t s, int part) {
   if (!c->have_tree) fail(FMM_ERR_STATE, "downward: no tree");
-  dispatch_order<Downward>(c->cfg.order, c, s);
-  c->have_out = true;
+  dispatch_order<Downward>(c->cfg.order, c, s, part);
+  if (part & 2) c->have_out = true;
 }
 
 }  // namespace fmmb
