@@ -1,6 +1,7 @@
 // m2l.cu — the FP64 M2L kernel (reference: m2l, kernels.cpp:98-111, applied over the M2L list
 // by KernelVisitor::m2l_pair, traversal.hpp:143-152). See expansions.cu for the conventions.
 #include <algorithm>
+#include <atomic>
 
 #include <cub/cub.cuh>
 
@@ -21,6 +22,16 @@
 
 namespace fmmb {
 namespace {
+
+// kernel attributes are per device: set them once for each device a context runs on (marked
+// only after the attribute is set: a concurrent first use just sets it twice)
+template <class F>
+inline void once_per_device(std::atomic<uint64_t>& mask, int device, F&& set) {
+  const uint64_t bit = 1ull << (device & 63);
+  if (mask.load() & bit) return;
+  set();
+  mask.fetch_or(bit);
+}
 
 // ---------------------------------------------------------------- register M2L (p <= 6) ----
 // Harmonic (traceless) reduction. Dt_g = g! D_g = d^g(1/|R|) is harmonic, so
@@ -104,11 +115,10 @@ __global__ void __launch_bounds__(kDetraceThreads) k_detrace(const double* __res
 template <int P>
 void launch_detrace(fmm_ctx* c, double* Mt, cudaStream_t s) {
   const size_t smem = sizeof(double) * kDetraceThreads * odd_stride(MI<P>::N);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};  // per device: the attribute is a per-device setting
+  once_per_device(attr, c->cfg.device, [&] {
     CK(cudaFuncSetAttribute(k_detrace<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  });
   k_detrace<P><<<ceil_div(c->ncells, kDetraceThreads), kDetraceThreads, smem, s>>>(c->M.p, c->ncells, Mt);
   CK_LAUNCH("k_detrace");
 }
@@ -631,11 +641,10 @@ struct M2L {
       constexpr int S = m2l_row_stride(HM<P>::NA);
       constexpr int kBufs = (HM<P>::NA * 8) % 16 == 0 && FMM_M2L_DB ? 2 : 1;
       const size_t smem = sizeof(double) * kM2LWarps * kBufs * 32 * S;
-      static bool attr = false;
-      if (!attr) {
+      static std::atomic<uint64_t> attr{0};
+      once_per_device(attr, c->cfg.device, [&] {
         CK(cudaFuncSetAttribute(k_m2l_reg<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-      }
+      });
       if (c->n_m2l_targets == 0) return;
       double* Mt = c->m2l_mt.ensure(c->ncells * HM<P>::NA + 1);
       launch_detrace<P>(c, Mt, s);
@@ -646,11 +655,10 @@ struct M2L {
     } else {  // p >= 7 (only these orders instantiate the staged-row kernel)
     using C2 = BigCfg2<P>;
     const size_t smem2 = C2::kSmemPerWarp * C2::kWarps;
-    static bool attr2 = false;
-    if (!attr2) {
+    static std::atomic<uint64_t> attr2{0};
+    once_per_device(attr2, c->cfg.device, [&] {
       CK(cudaFuncSetAttribute(k_m2l_big2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-      attr2 = true;
-    }
+    });
     if (c->n_m2l_targets == 0) return;
     double* Mt = c->m2l_mt.ensure(c->ncells * C2::NA + 1);
     launch_detrace<P>(c, Mt, s);
