@@ -88,6 +88,46 @@ int main() {
   const double rel = std::sqrt(static_cast<double>(num / den));
   std::printf("serial pipeline rel_l2 vs direct sum: %.3e\n", rel);
   CHECK(rel <= 1e-2);
+  // mutual mode (test_traversal.cpp:182-210, :320-345): the mutual emission symmetrised equals
+  // the non-mutual one, and the mutual KernelVisitor pipeline matches the non-mutual potentials
+  {
+    TraversalConfig mcfg = cfg;
+    mcfg.mutual = true;
+    Collector mcol;
+    dual_tree_traverse(t, t, mcfg, mcol, [](auto) {});
+    std::set<std::tuple<char, int, int>> sym;
+    for (const auto& [k, a, b] : mcol.tuples) {
+      sym.emplace(k, a, b);
+      sym.emplace(k, b, a);
+    }
+    CHECK(sym == col.tuples);
+    CHECK(mcol.tuples.size() < col.tuples.size());
+    Tree tm = build_tree(bodies, 64, 6);
+    upward_pass(tm, kt);
+    KernelVisitor mvis(tm, tm, kt, true);
+    dual_tree_traverse(tm, tm, mcfg, mvis, [](auto) {});
+    downward_pass(tm, kt);
+    const auto phim = potentials(tm);
+    long double dn = 0, dd = 0;
+    for (std::size_t i = 0; i < phi.size(); ++i) {
+      dn += (phim[i] - phi[i]) * (phim[i] - phi[i]);
+      dd += phi[i] * phi[i];
+    }
+    CHECK(std::sqrt(static_cast<double>(dn / dd)) < 1e-12);
+    // m2l_mutual = the two one-directional translations (test_kernels.cpp:187-200)
+    std::vector<Real> Ms(56), Mt(56), tl(56, 0.0), sl(56, 0.0), t1(56, 0.0), s1(56, 0.0);
+    for (int i = 0; i < 56; ++i) {
+      Ms[i] = qd(rng);
+      Mt[i] = qd(rng);
+    }
+    const Vec3 R{2.2, -1.7, 0.9}, nR{-2.2, 1.7, -0.9};
+    m2l_mutual(kt, Ms, Mt, R, tl, sl);
+    m2l(kt, Ms, R, t1);
+    m2l(kt, Mt, nR, s1);
+    double diff = 0;
+    for (int i = 0; i < 56; ++i) diff = std::max(diff, std::abs(tl[i] - t1[i]) + std::abs(sl[i] - s1[i]));
+    CHECK(diff == 0.0);
+  }
   // error behaviour mirrors the reference
   bool threw = false;
   try {
