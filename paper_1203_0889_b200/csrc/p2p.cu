@@ -166,7 +166,8 @@ __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cur
     incl[h] += running;
     running = __shfl_sync(0xffffffffu, incl[h], 31);
     m[h] = __ballot_sync(0xffffffffu, valid[h] && incl[h] <= cap);
-    other[h] = __ballot_sync(0xffffffffu, valid[h] && kind[h] != kind0);
+    // classes: far | compensated (near and self share tiles; the self entry comes last)
+    other[h] = __ballot_sync(0xffffffffu, valid[h] && (kind[h] == kKindFar) != (kind0 == kKindFar));
   }
   int nseg = 0;  // the fitting entries are a prefix of the 64
 #pragma unroll
@@ -182,8 +183,12 @@ __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cur
 #pragma unroll
   for (int h = H - 1; h >= 0; --h)
     if (other[h]) first_other = 32 * h + __ffs(other[h]) - 1;
-  if (kind0 == kKindSelf) nseg = 1;
-  else nseg = min(nseg, first_other);
+  nseg = min(nseg, first_other);
+  // the r^2 == 0 guard is needed iff the tile holds the self entry
+  unsigned selfm = 0;
+#pragma unroll
+  for (int h = 0; h < H; ++h)
+    selfm |= __ballot_sync(0xffffffffu, valid[h] && kind[h] == kKindSelf && h * 32 + lane < nseg);
 #pragma unroll
   for (int h = 0; h < H; ++h) {
     const int idx = h * 32 + lane;
@@ -202,7 +207,7 @@ __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cur
     tt.nseg = nseg;
     tt.next = huge ? cursor : cursor + nseg;
     tt.next_off = huge ? cur_off + cap : 0;
-    tt.guard = kind0 == kKindSelf ? 1 : 0;
+    tt.guard = selfm ? 1 : 0;
     tt.prec = kind0 == kKindFar ? 0 : 1;
   }
 }
