@@ -74,10 +74,22 @@ __device__ __forceinline__ void classify(const int2 pr, const double4* __restric
 // Counters (ctr): [0] M2L total, [1] P2P total, [2] overflow flag, [4 + L] frontier size of
 // level L (level 0 = the root pair), [64 + L] chunk tickets of level L.
 constexpr int kStepThreads = 256;
-// pairs per thread: 4 with atomic slot reservation (32-bit keys), 8 with the ordered look-back
-// (fewer, larger chunks amortise the look-back)
+// pairs per thread: 2 with atomic slot reservation (32-bit keys), 4 with the ordered look-back
+// (larger chunks amortise the look-back); 8 CTAs of 256 threads per SM. The kernel is latency
+// bound (ncu at C3: issue 25 %, L2 50 % hit, ~30 cycles per issued instruction), so occupancy
+// beats the register spill this costs (tools/trav_ab.sh: traversal C2 -5 %, C5 -4 % against
+// 4/8 pairs at 4-5 CTAs/SM)
+#ifndef FMM_STEP_PER64
+#define FMM_STEP_PER64 4
+#endif
+#ifndef FMM_STEP_PER32
+#define FMM_STEP_PER32 2
+#endif
+#ifndef FMM_STEP_MINB
+#define FMM_STEP_MINB 8
+#endif
 template <class KeyT>
-constexpr int step_per() { return sizeof(KeyT) == 8 ? 8 : 4; }
+constexpr int step_per() { return sizeof(KeyT) == 8 ? FMM_STEP_PER64 : FMM_STEP_PER32; }
 template <class KeyT>
 constexpr int step_chunk() { return kStepThreads * step_per<KeyT>(); }
 constexpr int kTicketBase = 64;
@@ -92,7 +104,7 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
 }
 
 template <class KeyT>
-__global__ void __launch_bounds__(kStepThreads)
+__global__ void __launch_bounds__(kStepThreads, FMM_STEP_MINB)
 k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, const int32_t* __restrict__ cc,
        const int32_t* __restrict__ cb, double theta, double theta2, int mutual, int sbits, KeyT* __restrict__ m2l_keys,
        KeyT* __restrict__ p2p_keys, int2* __restrict__ next, unsigned long long* __restrict__ ctr, int64_t cap_m,
@@ -474,7 +486,7 @@ void traverse(fmm_ctx* c) {
     CK(cudaMemsetAsync(ctr, 0, 128 * sizeof(unsigned long long), s));
     // look-back state: one flag + 4 values per chunk of the largest frontier (flags zeroed on
     // (re)allocation only: every launch uses a fresh epoch)
-    const int64_t nchunk = cap_f / step_chunk<uint32_t>() + 2;
+    const int64_t nchunk = cap_f / std::min(step_chunk<uint32_t>(), step_chunk<uint64_t>()) + 2;
     if (c->lb_flag.cap < static_cast<size_t>(nchunk)) {
       c->lb_flag.ensure(nchunk);
       CK(cudaMemsetAsync(c->lb_flag.p, 0, sizeof(uint32_t) * c->lb_flag.cap, s));
