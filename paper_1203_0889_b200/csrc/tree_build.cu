@@ -240,13 +240,13 @@ __global__ void k_leaf_map(const int32_t* __restrict__ leaves, int64_t nleaves, 
 // leaf_of_body. Larger leaves (level-21 overflow only) raise *big for the global fallback.
 constexpr int kRankMax = 1024;
 __global__ void __launch_bounds__(128)
-k_leaf_sort(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __restrict__ bb,
+k_leaf_sort(const int32_t* __restrict__ leaves, const int64_t* __restrict__ d_nleaves, const int32_t* __restrict__ bb,
             const int32_t* __restrict__ be, const int32_t* __restrict__ sidx, int32_t* __restrict__ perm,
             int32_t* __restrict__ leaf_of_body, int32_t* __restrict__ big) {
   __shared__ int32_t sv[4][kRankMax];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t wid = blockIdx.x * 4ll + w;
-  if (wid >= nleaves) return;
+  if (wid >= *d_nleaves) return;  // launched for every cell: the leaf count stays on the device
   const int32_t leaf = leaves[wid];
   const int32_t b = bb[leaf], e = be[leaf], n = e - b;
   for (int32_t i = lane; i < n; i += 32) leaf_of_body[b + i] = leaf;
@@ -477,22 +477,21 @@ void build_tree(fmm_ctx* c) {
   }
   int32_t* big = reinterpret_cast<int32_t*>(nsel + 1);
   CK(cudaMemsetAsync(big, 0, sizeof(int32_t), s));
-  CK(cudaMemcpyAsync(hp, nsel, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  c->nleaves = hp[0];
   c->wl = leaves;
-  c->nwl = c->nleaves;
   c->shard_planned = false;
 
-  // 6. within-leaf input order: rank sort per leaf; global (leaf, index) sort only when a
-  //    level-21 leaf exceeds kRankMax bodies
+  // 6. within-leaf input order: rank sort per leaf (grid over the cells, the leaf count read on
+  //    the device, so the leaf count and the big-leaf flag come back in one host read); global
+  //    (leaf, index) sort only when a level-21 leaf exceeds kRankMax bodies
   int32_t* leaf_of_body = c->leaf_of_body.ensure(n);
   int32_t* perm = c->perm.ensure(n);
-  k_leaf_sort<<<ceil_div(c->nleaves, 4), 128, 0, s>>>(leaves, c->nleaves, c->c_body_begin.p, c->c_body_end.p, sidx,
-                                                      perm, leaf_of_body, big);
+  k_leaf_sort<<<ceil_div(ncells, 4), 128, 0, s>>>(leaves, nsel, c->c_body_begin.p, c->c_body_end.p, sidx, perm,
+                                                  leaf_of_body, big);
   CK_LAUNCH("k_leaf_sort");
-  CK(cudaMemcpyAsync(hp + 1, big, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hp, nsel, sizeof(int64_t) + sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  c->nleaves = hp[0];
+  c->nwl = c->nleaves;
   launches += 3;
   if (*reinterpret_cast<int32_t*>(hp + 1)) {
     uint64_t* ckey = c->keys_a.ensure(n);
