@@ -257,16 +257,23 @@ def run_sharded(args, fb, torch, world, rank, local):
     dist.all_reduce(own_p2p)
     inter = int(own_p2p.item()) + n_m2l_problem  # M2L pairs of shared targets counted once
 
-    # e2e through the public API: every rank copies the step's bodies H2D from pinned memory and
-    # reads its results back (tree order) each step; max over ranks
+    # e2e through the public API, per rank and step: H2D of this rank's 1/world share of the
+    # bodies from pinned memory, NCCL all-gather of the shares over NVLink (every rank builds the
+    # full tree), the sharded step, and D2H of the results this rank owns (its contiguous
+    # tree-order body range, read from the context's result buffers); max over ranks
     e2e = None
     if not args.no_e2e:
-        import ctypes as C
-        h_in = torch.from_numpy(bodies).pin_memory()
-        h_phi = torch.empty(n, dtype=torch.float64).pin_memory()
-        h_acc = torch.empty(3 * n, dtype=torch.float64).pin_memory()
-        dp = C.POINTER(C.c_double)
-        ptr = lambda tns: C.cast(tns.data_ptr(), dp)  # noqa: E731
+        chunk = n // world  # n = 2^20 * world
+        h_in = torch.from_numpy(np.ascontiguousarray(bodies[rank * chunk:(rank + 1) * chunk])).pin_memory()
+        d_part = torch.empty_like(h_in, device="cuda")
+        h_phi = torch.empty(n, dtype=torch.float64).pin_memory()  # own range <= n
+        h_acc = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+
+        class _Dev:  # zero-copy torch view of a context result buffer
+            def __init__(self, ptr, shape):
+                self.__cuda_array_interface__ = {"shape": shape, "typestr": "<f8", "data": (ptr, False),
+                                                 "version": 3, "strides": None}
+
         ts = []
         dist.barrier()
         torch.cuda.synchronize()
@@ -274,15 +281,24 @@ def run_sharded(args, fb, torch, world, rank, local):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            d_bodies.copy_(h_in, non_blocking=True)
-            step()
-            rc = ctx.lib.fmm_get_results(ctx.h, ptr(h_phi), ptr(h_acc), 0)
-            assert rc == 0, ctx.lib.fmm_last_error(ctx.h)
+            d_part.copy_(h_in, non_blocking=True)
+            dist.all_gather_into_tensor(d_bodies, d_part)
+            sinfo = step()
+            b0, b1 = int(sinfo.body_begin), int(sinfo.body_end)
+            pphi, pacc = ctx.results_device()
+            d_phi = torch.as_tensor(_Dev(pphi, (n,)), device="cuda")
+            d_acc = torch.as_tensor(_Dev(pacc, (n, 3)), device="cuda")
+            h_phi[:b1 - b0].copy_(d_phi[b0:b1], non_blocking=True)
+            h_acc[:b1 - b0].copy_(d_acc[b0:b1], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
             ts.append(time.perf_counter() - t0)
+        assert np.isfinite(h_phi[:b1 - b0].numpy()).all()
         e2e_ms = torch.tensor([float(np.mean(ts)) * 1e3], device="cuda")
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": inter / (e2e_ms.item() * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms.item(),
-               "h2d_bytes_per_step": int(n * 32), "d2h_bytes_per_step": int(n * 32)}
+               "h2d_bytes_per_step": int(chunk * 32), "d2h_bytes_per_step": int((b1 - b0) * 32),
+               "per": "rank 0 (each rank copies its own share; bodies all-gathered over NVLink: "
+                      f"{int(n * 32)} bytes per rank)"}
     if rank == 0:
         line = {"metric": METRIC, "value": inter / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -306,6 +322,8 @@ def run_sharded(args, fb, torch, world, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sharded (torchrun) path even at world size 1 (tests the NCCL flow on one GPU)")
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -327,7 +345,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.sharded:
         return run_sharded(args, fb, torch, world, rank, local)
     dist = None
 
