@@ -693,21 +693,31 @@ __global__ void k_entry_counts(const int32_t* __restrict__ src, int64_t n, const
   }
 }
 
-// per work leaf: S = sum of source sizes (from the entry prefix), total cost reduced per warp
+// per work leaf: S = sum of source sizes (from the entry prefix), total cost reduced per warp;
+// total[1] = a bound on any one item's cost (min(leaf size, kThreads) * S), which sizes the
+// cost sort's key range
 __global__ void k_leaf_sum(const int32_t* __restrict__ leaves, int64_t nleaves, const int64_t* __restrict__ off,
                             const int64_t* __restrict__ pre, const int32_t* __restrict__ bb,
                             const int32_t* __restrict__ be, int64_t* __restrict__ sum_ns,
                             unsigned long long* __restrict__ total) {
   const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  unsigned long long v = 0;
+  unsigned long long v = 0, m = 0;
   if (w < nleaves) {
     const int32_t leaf = leaves[w];
     const int64_t S = pre[off[leaf + 1]] - pre[off[leaf]];
+    const int32_t nt = be[leaf] - bb[leaf];
     sum_ns[w] = S;
-    v = static_cast<unsigned long long>(S) * static_cast<unsigned long long>(be[leaf] - bb[leaf]);
+    v = static_cast<unsigned long long>(S) * static_cast<unsigned long long>(nt);
+    m = static_cast<unsigned long long>(S) * static_cast<unsigned long long>(min(nt, kThreads));
   }
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0 && v) atomicAdd(total, v);
+  for (int o = 16; o > 0; o >>= 1) {
+    v += __shfl_xor_sync(0xffffffffu, v, o);
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
+  if ((threadIdx.x & 31) == 0 && v) {
+    atomicAdd(total, v);
+    atomicMax(total + 1, m);
+  }
 }
 
 // items of one work leaf (thread each): chunk j covers list entries [bnd_j, bnd_{j+1}) where
@@ -939,11 +949,11 @@ void p2p_worklist_begin(fmm_ctx* c) {
   }
   int64_t* sum_ns = c->p2p_sum.ensure(nl + 1);
   unsigned long long* tot = reinterpret_cast<unsigned long long*>(c->d_counters.ensure(16)) + 12;
-  CK(cudaMemsetAsync(tot, 0, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(tot, 0, 2 * sizeof(unsigned long long), s));
   k_leaf_sum<<<ceil_div(nl, 256), 256, 0, s>>>(c->wl, nl, c->p2p_off.p, pre, c->c_body_begin.p, c->c_body_end.p,
                                                sum_ns, tot);
   CK_LAUNCH("k_leaf_sum");
-  CK(cudaMemcpyAsync(c->hpin + 16, tot, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(c->hpin + 16, tot, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   c->kernel_launches += 3;
   c->p2p_pending = true;
 }
@@ -995,9 +1005,13 @@ void p2p_worklist_end(fmm_ctx* c) {
   int32_t* ord_out = ord_in + (nitem + 1);
   k_iota<<<ceil_div(nitem, 256), 256, 0, s>>>(ord_in, nitem);
   size_t sb = 0;
-  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, costs, costs_sorted, ord_in, ord_out, (int)nitem, 0, 48, s));
+  // every item cost is below 2^cost_bits (C2: ~20 bits, 3 radix passes instead of 6)
+  const uint64_t cbound = static_cast<uint64_t>(c->hpin[17]);
+  const int cost_bits = std::min(48, std::max(1, 64 - __builtin_clzll(cbound | 1ull)));
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, costs, costs_sorted, ord_in, ord_out, (int)nitem, 0,
+                                               cost_bits, s));
   CK(cub::DeviceRadixSort::SortPairsDescending(temp_storage2(c, sb), sb, costs, costs_sorted, ord_in, ord_out,
-                                               (int)nitem, 0, 48, s));
+                                               (int)nitem, 0, cost_bits, s));
   k_gather_items<<<ceil_div(nitem, 256), 256, 0, s>>>(items_raw, ord_out, nitem, items);
   CK_LAUNCH("k_gather_items");
   c->n_p2p_items = nitem;
