@@ -81,7 +81,6 @@ struct fmm_ctx {
   fmmb::DBuf<int32_t> p2p_i32a, p2p_i32b, p2p_i32c;
   fmmb::DBuf<int64_t> p2p_sum;
   fmmb::DBuf<int4> p2p_items_raw;
-  fmmb::DBuf<int32_t> self_pos;          // per cell: CSR position of its self entry, -1 = none         // per P2P list entry: {body_begin, count, shift.xy} + {shift.z,...}
   int64_t n_p2p_reduce = 0;
 
   // expansions and outputs

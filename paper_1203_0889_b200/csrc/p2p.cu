@@ -823,14 +823,13 @@ __global__ void k_leaf_boxes(const int32_t* __restrict__ leaves, int64_t nleaves
 }
 
 // Entry-parallel (C3's halo leaf alone has 57 K entries): pass 1 classifies every entry
-// (self / near / far) and records each target's self position; an exclusive scan of the packed
-// per-class indicators (near in the low, far in the high 32 bits) gives every entry its rank
-// within its target's class; pass 2 writes the entry at
-//   self: l0 | near: l0 + has_self + near rank | far: l0 + has_self + n_near + far rank.
+// (self / near / far); an exclusive scan of the packed per-class indicators (near in the low,
+// far in the high 32 bits) gives every entry its rank within its target's class; pass 2 writes
+// the entry at
+//   far: l0 + far rank | near: l0 + n_far + near rank | self: l1 - 1 (the list's last entry).
 __global__ void k_ent_class(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src, int64_t ne,
                             const double4* __restrict__ cr, const double4* __restrict__ blo,
-                            const double4* __restrict__ bhi, int64_t* __restrict__ cls,
-                            int32_t* __restrict__ self_pos) {
+                            const double4* __restrict__ bhi, int64_t* __restrict__ cls) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k > ne) return;
   if (k == ne) {
@@ -840,7 +839,6 @@ __global__ void k_ent_class(const int32_t* __restrict__ tgt, const int32_t* __re
   const int32_t t = tgt[k], s = src[k];
   int64_t v;
   if (s == t) {
-    self_pos[t] = static_cast<int32_t>(k);
     v = 0;
   } else {
     const bool nr = near_leaf(blo[t], bhi[t], blo[s], bhi[s], FMM_P2P_NEAR_GAP * (cr[t].w + cr[s].w));
@@ -851,21 +849,19 @@ __global__ void k_ent_class(const int32_t* __restrict__ tgt, const int32_t* __re
 
 __global__ void k_ent_write(const int32_t* __restrict__ tgt, const int32_t* __restrict__ src, int64_t ne,
                             const int64_t* __restrict__ off, const int64_t* __restrict__ cls,
-                            const int64_t* __restrict__ pre, const int32_t* __restrict__ self_pos,
+                            const int64_t* __restrict__ pre,
                             const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
                             const double4* __restrict__ cr, P2PEnt* __restrict__ ent) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= ne) return;
   const int32_t t = tgt[k], s = src[k];
   const int64_t l0 = off[t], l1 = off[t + 1];
-  const int64_t hs = self_pos[t] >= 0 ? 1 : 0;
   const int64_t v = cls[k], P0 = pre[l0], Pk = pre[k];
   const int64_t lo0 = P0 & 0xffffffffll, hi0 = P0 >> 32;
   int64_t pos;
   int kind;
   // far entries first, then near, the self entry last: an item's short compensated tiles come
   // after its full far tiles, so the producer stages them while the consumers are busy
-  (void)hs;
   if (s == t) {
     pos = l1 - 1;
     kind = kKindSelf;
@@ -917,16 +913,14 @@ void build_p2p_entries(fmm_ctx* c) {
                                                              c->c_body_end.p, c->bodies.p, blo, bhi);
   int64_t* cls = c->ent_cls.ensure(ne + 1);
   int64_t* epre = c->ent_pre.ensure(ne + 1);
-  int32_t* spos = c->self_pos.ensure(c->ncells);
-  CK(cudaMemsetAsync(spos, 0xff, sizeof(int32_t) * c->ncells, s));
-  k_ent_class<<<ceil_div(ne + 1, 256), 256, 0, s>>>(c->p2p_tgt.p, c->p2p_src.p, ne, c->c_cr.p, blo, bhi, cls, spos);
+  k_ent_class<<<ceil_div(ne + 1, 256), 256, 0, s>>>(c->p2p_tgt.p, c->p2p_src.p, ne, c->c_cr.p, blo, bhi, cls);
   {
     size_t sb = 0;
     CK(cub::DeviceScan::ExclusiveSum(nullptr, sb, cls, epre, (int)(ne + 1), s));
     CK(cub::DeviceScan::ExclusiveSum(temp_storage2(c, sb), sb, cls, epre, (int)(ne + 1), s));
   }
   if (ne > 0)
-    k_ent_write<<<ceil_div(ne, 256), 256, 0, s>>>(c->p2p_tgt.p, c->p2p_src.p, ne, c->p2p_off.p, cls, epre, spos,
+    k_ent_write<<<ceil_div(ne, 256), 256, 0, s>>>(c->p2p_tgt.p, c->p2p_src.p, ne, c->p2p_off.p, cls, epre,
                                                   c->c_body_begin.p, c->c_body_end.p, c->c_cr.p, ent);
   CK_LAUNCH("k_ent_write");
   c->kernel_launches += 5;
