@@ -79,6 +79,9 @@ constexpr int kStepThreads = 256;
 // bound (ncu at C3: issue 25 %, L2 50 % hit, ~30 cycles per issued instruction), so occupancy
 // beats the register spill this costs (tools/trav_ab.sh: traversal C2 -5 %, C5 -4 % against
 // 4/8 pairs at 4-5 CTAs/SM)
+#ifndef FMM_TRAV_ORDERED64  // 64-bit keys: ordered look-back emission (1) or atomic slots + full sort (0)
+#define FMM_TRAV_ORDERED64 1
+#endif
 #ifndef FMM_STEP_PER64
 #define FMM_STEP_PER64 4
 #endif
@@ -115,7 +118,7 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
   // 64-bit keys (more than 2^16 cells, or mutual mode): ordered emission by look-back, and the
   // lists only need a stable sort on the target bits; 32-bit keys: atomic slot reservation (the
   // full (target, source) sort canonicalises them; measured cheaper at C2)
-  constexpr bool kOrdered = sizeof(KeyT) == 8;
+  constexpr bool kOrdered = sizeof(KeyT) == 8 && FMM_TRAV_ORDERED64;
   constexpr int kStepPer = step_per<KeyT>();
   constexpr int kStepChunk = step_chunk<KeyT>();
   __shared__ typename Scan::TempStorage scan_tmp;
@@ -354,7 +357,7 @@ void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int
   size_t sb = 0;
   // 64-bit keys come in a deterministic order (ordered emission / given pairs): a stable sort on
   // the target bits keeps it within each target; 32-bit keys: the full (target, source) sort
-  const int b0 = sizeof(KeyT) == 8 ? sbits : 0;
+  const int b0 = (sizeof(KeyT) == 8 && FMM_TRAV_ORDERED64) ? sbits : 0;
   CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys, kb, (int)n, b0, 2 * sbits, s));
   CK(cub::DeviceRadixSort::SortKeys(p2p_path ? temp_storage2(c, sb) : temp_storage(c, sb), sb, keys, kb, (int)n, b0,
                                     2 * sbits, s));
