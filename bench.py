@@ -11,7 +11,8 @@ reference's xorshift64* generator.
           the bodies resident in HBM before the timed region (CUDA events on the FMM stream);
   e2e     the same metric through the C-ABI with host buffers: H2D of the bodies, the step,
           and D2H of phi + acceleration (input order) inside the timed region;
-  roofline  the P2P kernel's FP32 throughput (20 flops per body pair) against the FP32 peak;
+  roofline  the P2P kernel's throughput (20 flops per body pair) against the peak of the pipe
+            it runs on (FP32 for --precision fp32, FP64 for the fp64 parity mode);
   cpu_baseline  the reference's own CPU FMM (oracle/_ref, its scheduler) on the host cores.
 
 `--impl reference` times the reference's CPU FMM (oracle/_ref) with all host threads.
@@ -405,14 +406,22 @@ def main():
     peaks = load_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     sms = torch.cuda.get_device_properties(local).multi_processor_count
-    fp32_peak = sms * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s
+    fp32 = args.precision == "fp32"
+    lanes = 128 if fp32 else 64  # FP32 / FP64 lanes per SM (FFMA2 126, DFMA 60 ops/clk/SM measured)
+    pipe_peak = sms * lanes * 2 * sm_max * 1e6 / 1e12  # TFLOP/s
+    p2p_name = "k_p2p_fp32_ws" if fp32 else "k_p2p_fp64"
     p2p_kernel = float(np.mean(p2p_alone))
     achieved = FLOPS_PER_PAIR * info.p2p_body_pairs / (p2p_kernel * 1e-3) / 1e12
     # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f)["k_p2p_fp32_ws"]["dram_bytes_per_launch"]
+            tj = json.load(f)
+        key = f"{args.config}/{args.precision}"
+        if key in tj.get("by_config", {}):
+            traffic = tj["by_config"][key]["dram_bytes_per_launch"]
+        elif key == "C2/fp32":
+            traffic = tj[p2p_name]["dram_bytes_per_launch"]
     except Exception:
         traffic = None
 
@@ -482,14 +491,16 @@ def main():
             "m2l_pairs_per_s": info.n_m2l / (ms_per_step * 1e-3),
             "stage_ms": {k: v / args.steps for k, v in stage_acc.items()},
             "p2p_kernel_ms": p2p_kernel, "m2l_kernel_ms": float(np.mean(m2l_ms)),
-            "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                         "frac": achieved / fp32_peak, "traffic": traffic,
-                         "traffic_unit": "bytes per launch (dram read + write, ncu --set full, C2)",
-                         "kernel": "k_p2p_fp32_ws", "flops_per_unit": FLOPS_PER_PAIR,
+            "roofline": {"bound": "fp32" if fp32 else "fp64", "achieved": achieved, "peak": pipe_peak,
+                         "unit": "TFLOP/s", "frac": achieved / pipe_peak, "traffic": traffic,
+                         "traffic_unit": f"bytes per launch (dram read + write, ncu, {args.config} "
+                                         f"{args.precision}; profiles/ncu_traffic.json)",
+                         "kernel": p2p_name, "flops_per_unit": FLOPS_PER_PAIR,
                          "timing": "CUDA events around the P2P launch in a serialised pass after the timed steps (the kernel runs alone), L2 flushed",
-                         "peak_source": f"derived: {sms} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz "
-                                        "(sm_max_mhz of MEASURED_PEAKS.json; FFMA microbenchmark "
-                                        "measured 126-128 lane-ops/clk/SM)"},
+                         "peak_source": f"derived: {sms} SMs x {lanes} {'FP32' if fp32 else 'FP64'} lanes x 2 x "
+                                        f"{sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json; "
+                                        + ("FFMA2 microbenchmark measured 126-128 lane-ops/clk/SM)" if fp32 else
+                                           "DFMA microbenchmark measured 60 lane-ops/clk/SM)")},
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
             "gpu_launches": launches, "tree": {"ncells": info.ncells, "nleaves": info.nleaves,
                                                "depth": info.depth},
