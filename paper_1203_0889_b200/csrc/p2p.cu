@@ -545,7 +545,8 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
 
 // ------------------------------------------------------------------------ FP64 kernel ----
 // Parity mode: absolute FP64 coordinates and the reference's arithmetic
-// (dx = x_i - y_j, r2 = (dx*dx + dy*dy) + dz*dz, skip r2 == 0, phi += q / sqrt(r2)).
+// (dx = x_i - y_j, r2 = (dx*dx + dy*dy) + dz*dz, skip r2 == 0, phi += q / sqrt(r2)), with
+// 1/sqrt(r2) as rsqrt (<= 1 ulp) rather than an IEEE sqrt followed by an IEEE divide.
 __global__ void __launch_bounds__(kThreads, 4)
 k_p2p_fp64(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_list,
            const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
@@ -589,7 +590,7 @@ k_p2p_fp64(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_li
         const double dx = bt.x - s.x, dy = bt.y - s.y, dz = bt.z - s.z;
         const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
         if (r2 == 0.0) continue;
-        const double ri = 1.0 / sqrt(r2);
+        const double ri = rsqrt(r2);  // <= 1 ulp; one Newton sequence instead of IEEE sqrt + divide
         const double qr = s.w * ri;
         phi_d += qr;
         if (with_acc) {
