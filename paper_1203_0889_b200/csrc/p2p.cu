@@ -547,6 +547,22 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
 // Parity mode: absolute FP64 coordinates and the reference's arithmetic
 // (dx = x_i - y_j, r2 = (dx*dx + dy*dy) + dz*dz, skip r2 == 0, phi += q / sqrt(r2)), with
 // 1/sqrt(r2) as rsqrt (<= 1 ulp) rather than an IEEE sqrt followed by an IEEE divide.
+__device__ __forceinline__ void p2p_pair_fp64(const double4& bt, const double4& s, int with_acc, double& phi,
+                                              double& ax, double& ay, double& az) {
+  const double dx = bt.x - s.x, dy = bt.y - s.y, dz = bt.z - s.z;
+  const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  if (r2 == 0.0) return;
+  const double ri = rsqrt(r2);  // <= 1 ulp; one Newton sequence instead of IEEE sqrt + divide
+  const double qr = s.w * ri;
+  phi += qr;
+  if (with_acc) {
+    const double qr3 = qr * ri * ri;
+    ax += dx * qr3;
+    ay += dy * qr3;
+    az += dz * qr3;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, 4)
 k_p2p_fp64(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_list,
            const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
@@ -558,17 +574,21 @@ k_p2p_fp64(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_li
   __shared__ int32_t seg_src[kTileSegs];
   __shared__ int32_t seg_boff[kTileSegs];
   __shared__ int32_t nxt[3];
-  __shared__ double red[4][kThreads];
+  __shared__ double red[8][kThreads];
 
+  // Two targets per thread (t and t + nh): one shared-memory source read serves two pairs.
   const P2PItem it = items[blockIdx.x];
   const int tid = threadIdx.x;
   const int nt = it.te - it.tb;
-  const int G = kThreads / nt;
-  const int g = tid / nt, t = tid - g * nt;
+  const int nh = (nt + 1) >> 1;
+  const int G = kThreads / nh;
+  const int g = tid / nh, t = tid - g * nh;
   const bool active = g < G;
-  double4 bt = make_double4(0, 0, 0, 0);
+  double4 bt = make_double4(0, 0, 0, 0), bu = make_double4(0, 0, 0, 0);
   if (active) bt = bodies[it.tb + t];
+  if (active && t + nh < nt) bu = bodies[it.tb + t + nh];  // else a dummy whose sums are dropped
   double phi_d = 0.0, ax_d = 0.0, ay_d = 0.0, az_d = 0.0;
+  double phi_e = 0.0, ax_e = 0.0, ay_e = 0.0, az_e = 0.0;
   int32_t cursor = it.lb, cur_off = 0;
   while (cursor < it.le) {
     tile_setup<kTile>(tid, it.le, cursor, cur_off, src_list, bb, be, seg_off, seg_src, seg_boff, nxt);
@@ -587,18 +607,8 @@ k_p2p_fp64(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_li
     if (active) {
       for (int j = g; j < nb; j += G) {
         const double4 s = sS[j];
-        const double dx = bt.x - s.x, dy = bt.y - s.y, dz = bt.z - s.z;
-        const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-        if (r2 == 0.0) continue;
-        const double ri = rsqrt(r2);  // <= 1 ulp; one Newton sequence instead of IEEE sqrt + divide
-        const double qr = s.w * ri;
-        phi_d += qr;
-        if (with_acc) {
-          const double qr3 = qr * ri * ri;
-          ax_d += dx * qr3;
-          ay_d += dy * qr3;
-          az_d += dz * qr3;
-        }
+        p2p_pair_fp64(bt, s, with_acc, phi_d, ax_d, ay_d, az_d);
+        p2p_pair_fp64(bu, s, with_acc, phi_e, ax_e, ay_e, az_e);
       }
     }
     cursor = nxt[0];
@@ -609,11 +619,16 @@ k_p2p_fp64(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_li
   red[1][tid] = ax_d;
   red[2][tid] = ay_d;
   red[3][tid] = az_d;
+  red[4][tid] = phi_e;
+  red[5][tid] = ax_e;
+  red[6][tid] = ay_e;
+  red[7][tid] = az_e;
   __syncthreads();
   if (tid < nt) {
+    const int h = tid >= nh ? 1 : 0, tt = tid - h * nh;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     for (int gg = 0; gg < G; ++gg)
-      for (int c = 0; c < 4; ++c) v[c] += red[c][gg * nt + tid];
+      for (int c = 0; c < 4; ++c) v[c] += red[4 * h + c][gg * nh + tt];
     if (it.pbase < 0) {
       const int32_t i = it.tb + tid;
       phi_out[i] = v[0];
