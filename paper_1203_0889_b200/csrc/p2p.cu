@@ -545,14 +545,15 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
 
 // ------------------------------------------------------------------------ FP64 kernel ----
 // Parity mode: absolute FP64 coordinates and the reference's arithmetic
-// (dx = x_i - y_j, r2 = (dx*dx + dy*dy) + dz*dz, skip r2 == 0, phi += q / sqrt(r2)), with
-// 1/sqrt(r2) as rsqrt (<= 1 ulp) rather than an IEEE sqrt followed by an IEEE divide.
+// (dx = x_i - y_j, r2 = dx^2 + dy^2 + dz^2, skip r2 == 0, phi += q / sqrt(r2)), with r2 fused
+// (FMA) and 1/sqrt(r2) as rsqrt (<= 1 ulp) rather than an IEEE sqrt followed by an IEEE divide.
 __device__ __forceinline__ void p2p_pair_fp64(const double4& bt, const double4& s, int with_acc, double& phi,
                                               double& ax, double& ay, double& az) {
   const double dx = bt.x - s.x, dy = bt.y - s.y, dz = bt.z - s.z;
-  const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-  if (r2 == 0.0) return;
-  const double ri = rsqrt(r2);  // <= 1 ulp; one Newton sequence instead of IEEE sqrt + divide
+  const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));  // zero exactly when dx = dy = dz = 0
+  // rsqrt: <= 1 ulp, one Newton sequence instead of IEEE sqrt + divide; r2 == 0 (the self pair)
+  // contributes nothing, as a select rather than a branch
+  const double ri = r2 > 0.0 ? rsqrt(r2) : 0.0;
   const double qr = s.w * ri;
   phi += qr;
   if (with_acc) {
