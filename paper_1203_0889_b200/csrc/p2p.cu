@@ -564,7 +564,10 @@ __device__ __forceinline__ void p2p_pair_fp64(const double4& bt, const double4& 
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 4)
+#ifndef FMM_P2P64_MIN_BLOCKS
+#define FMM_P2P64_MIN_BLOCKS 8  // 64 registers, 8 CTAs/SM (A/B at C2: 4 -> 9.14 ms, 6 -> 8.44, 7 -> 8.35, 8 -> 8.25)
+#endif
+__global__ void __launch_bounds__(kThreads, FMM_P2P64_MIN_BLOCKS)
 k_p2p_fp64(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_list,
            const int32_t* __restrict__ bb, const int32_t* __restrict__ be,
            const double4* __restrict__ bodies, double* __restrict__ phi_out, double* __restrict__ acc_out,
