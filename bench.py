@@ -141,9 +141,109 @@ def flush_l2(buf):
         buf.zero_()
 
 
+DIST = {1: "uniform [-1,1]^3, q in (0,1/N]", 2: "uniform [-1,1]^3, q in (0,1/N]",
+        3: "Plummer sphere (scale radius 1, r <= 100), q = 1/N", 4: "uniform [-1,1]^3, q in (0,1/N]",
+        5: "unit sphere surface (normalised Gaussian), q in [-1,1]/N"}
+L2_NOTE = ("flushed between steps by a 256 MB write (device buffer on the GPU arm, host buffer on "
+           "the CPU reference arm); > 126 MB L2")
+
+
+def workload_config(cfg_name, n, world=1, strong=False):
+    """The `config` object, identical for the GPU arm and the CPU reference arm."""
+    gen, n_cfg, p, n_crit, theta = CONFIGS[cfg_name]
+    cfg = {"workload": f"{cfg_name}: N={n} {DIST[gen]}, p={p}, n_crit={n_crit}, theta={theta}, "
+                       "potential+acceleration (reference: potential)",
+           "n_bodies": n, "order": p, "n_crit": n_crit, "theta": theta, "l2": L2_NOTE,
+           "seed": 1}
+    if world > 1:
+        cfg["parallelism"] = (f"dp{world}: target leaves sharded by cost-balanced Morton range, NCCL "
+                              "all-gather of owned multipoles" + (" (strong scaling: N fixed)" if strong else ""))
+    else:
+        cfg["parallelism"] = "single GPU"
+    return cfg
+
+
+def _ref_bodies(gen, n):
+    """BASELINE bodies from the oracle's restated generator (bit-identical to
+    fmm_generate_bodies, tests/test_oracle.py): the reference arm never loads libfmm_b200.so."""
+    import oracle
+    return oracle.Oracle().generate_baseline_bodies(gen, n, 1)
+
+
+def _ref_interactions(ref, bodies, n_crit, p, theta):
+    t = ref.build_tree(bodies, n_crit, p)
+    c = t.cells()
+    m, pp = t.traverse(theta)
+    nb = (c.body_end - c.body_begin).astype(np.int64)
+    return int((nb[pp[:, 0]] * nb[pp[:, 1]]).sum()), len(m)
+
+
+def _host_flush(buf):
+    buf += 1  # 256 MB write: the CPU arm's counterpart of the GPU arm's L2 flush
+
+
+STAGES = ("build", "upward", "traversal+m2l+p2p", "downward")
+
+
+def cpu_reference(gen, n, p, n_crit, theta, steps=1, warmup=0, single_core=False):
+    """The reference CPU FMM (oracle/_ref: the unmodified sources) at the config's N.
+    All cores: its scheduler with nproc-1 workers + the helping master (scheduler.cpp:62-72),
+    Q = RunConfig's default (engine.hpp:32-35). Optional 1 core: inline traversal with Q = inf
+    on a thread pinned to one core. Per-stage medians (engine.cpp:69-106)."""
+    import oracle
+    ref = oracle.Reference()
+    bodies = _ref_bodies(gen, n)
+    n_pairs, n_m2l = _ref_interactions(ref, bodies, n_crit, p, theta)
+    inter = n_pairs + n_m2l
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    threads = max(1, cores - 1)
+    q = max(n // 100, 64)
+    flush = np.zeros(256 << 20, np.uint8)
+    for _ in range(warmup):
+        ref.step(bodies, n_crit, p, theta, q, threads)
+    totals, stages = [], []
+    for _ in range(max(1, steps)):
+        _host_flush(flush)
+        t0 = time.perf_counter()
+        st, _ = ref.step(bodies, n_crit, p, theta, q, threads)
+        totals.append(time.perf_counter() - t0)
+        stages.append(st)
+    sec = float(np.median(totals))
+    out = {"value": inter / sec, "ms_per_step": sec * 1e3, "cores": cores, "threads": threads + 1,
+           "interactions_per_step": inter, "p2p_body_pairs": n_pairs, "m2l_pairs": n_m2l,
+           "stage_ms": dict(zip(STAGES, (1e3 * np.median(np.array(stages), 0)).tolist())),
+           "sample": f"full config N={n}: reference scheduler, {threads} workers + master on {cores} host "
+                     f"cores, Q={q}, median of {len(totals)} step(s)"}
+    try:
+        import platform
+        out["cpu_model"] = next((ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo")
+                                 if ln.startswith("model name")), platform.processor())
+    except Exception:
+        pass
+    if single_core:
+        import threading
+        res = {}
+
+        def pinned():
+            cpu = sorted(os.sched_getaffinity(0))[0]
+            os.sched_setaffinity(0, {cpu})  # this thread only (Linux: pid 0 = calling thread)
+            t0 = time.perf_counter()
+            st, _ = ref.step(bodies, n_crit, p, theta, 1 << 30, 0)
+            res["s"] = time.perf_counter() - t0
+            res["st"] = st
+
+        th = threading.Thread(target=pinned)
+        th.start()
+        th.join()
+        out["single_core"] = {"ms_per_step": res["s"] * 1e3, "value": inter / res["s"], "cores": 1,
+                              "stage_ms": dict(zip(STAGES, (1e3 * np.asarray(res["st"])).tolist())),
+                              "setting": "inline traversal, Q=inf, thread pinned to one core, 1 step"}
+    return out
+
+
 def run_reference(args, cfg_name):
-    """--impl reference: the reference's own CPU FMM (oracle/_ref, scheduler with all host
-    threads) on a bounded sample of the workload; rank 0 only."""
+    """--impl reference: the reference's own CPU FMM (oracle/_ref) on the host cores, at the
+    config's full N (C4/C5: a bounded sample, see --ref-n); rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -152,53 +252,26 @@ def run_reference(args, cfg_name):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfmmref.so not built"}))
         return 0
     gen, n_full, p, n_crit, theta = CONFIGS[cfg_name]
-    res = cpu_reference_sample(gen, n_full, p, n_crit, theta, args.ref_sample, steps=args.steps,
-                               warmup=args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    n = args.ref_n or (n_full if n_full <= (1 << 20) else (1 << 20))
+    res = cpu_reference(gen, n, p, n_crit, theta, steps=args.steps, warmup=min(args.warmup, 1),
+                        single_core=not args.no_single_core)
+    cfg = workload_config(cfg_name, n_full, world, strong=cfg_name == "C4")
     line = {"metric": METRIC, "impl": "reference", "value": res["value"], "unit": UNIT,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE generator, seeded)",
-            "config": res["config"],
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1),
+            "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE generator: reference xorshift64*, seed 1)", "config": cfg,
+            "interactions_per_step": res["interactions_per_step"], "stage_ms": res["stage_ms"],
             "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": res["cores"],
                              "kind": "reference", "sample": res["sample"]},
-            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "cpu_model": res.get("cpu_model"), "single_core": res.get("single_core"),
+            "warmup_note": "CPU arm: at most 1 warm-up step (no device state to warm)"}
+    if n != n_full:
+        line["sampled_n"] = n
     print(json.dumps(line))
     return 0
-
-
-def cpu_reference_sample(gen, n_full, p, n_crit, theta, n_sample, steps=1, warmup=0):
-    """The reference CPU FMM (build + upward + scheduled traversal/kernels + downward) on a
-    same-distribution sample of n_sample bodies; interactions/s = (P2P pairs + M2L pairs)/s."""
-    import oracle
-    import paper_1203_0889_b200.fmm as fb
-    ref = oracle.Reference()
-    n = min(n_sample, n_full)
-    bodies = fb.generate_bodies(gen, n, 1)
-    cores = os.cpu_count() or 1
-    threads = max(1, cores - 1)  # the master also executes tasks (scheduler.cpp:62-72)
-    # interaction counts of this sample (reference traversal)
-    t = ref.build_tree(bodies, n_crit, p)
-    c = t.cells()
-    m, pp = t.traverse(theta)
-    nb = (c.body_end - c.body_begin).astype(np.int64)
-    inter = int((nb[pp[:, 0]] * nb[pp[:, 1]]).sum()) + len(m)
-    del t
-    q = max(n // 100, 64)  # RunConfig default queue threshold (engine.hpp:32-35)
-    for _ in range(warmup):
-        ref.step(bodies, n_crit, p, theta, q, threads)
-    times = []
-    for _ in range(max(1, steps)):
-        t0 = time.perf_counter()
-        ref.step(bodies, n_crit, p, theta, q, threads)
-        times.append(time.perf_counter() - t0)
-    sec = float(np.mean(times))
-    return {"value": inter / sec, "ms_per_step": sec * 1e3, "cores": cores,
-            "sample": f"N={n} bodies of the same distribution (p={p}, n_crit={n_crit}, theta={theta}), "
-                      f"reference scheduler with {threads} workers + master, {len(times)} step(s), "
-                      f"{inter} interactions/step",
-            "config": {"workload": f"C{gen}: same distribution/p/n_crit/theta as the GPU arm; reference CPU "
-                                   f"FMM timed on a bounded N={n} sample (interactions/s)",
-                       "n_bodies": n, "order": p, "n_crit": n_crit, "theta": theta}}
 
 
 def run_sharded(args, fb, torch, world, rank, local):
@@ -330,9 +403,14 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C2", choices=list(CONFIGS))
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
-    ap.add_argument("--ref-sample", type=int, default=262144)
+    ap.add_argument("--ref-n", type=int, default=0,
+                    help="CPU reference N (default: the config's N up to 2^20; C4/C5 sample 2^20)")
+    ap.add_argument("--no-single-core", action="store_true",
+                    help="reference arm: skip the 1-core (Q=inf, pinned) step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fp64-mode", action="store_true",
+                    help="skip the FP64 parity-mode leg (reported as fp64_mode in the line)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
@@ -348,8 +426,56 @@ def main():
     torch.cuda.set_device(local)
     if world > 1 or args.sharded:
         return run_sharded(args, fb, torch, world, rank, local)
-    dist = None
+    return run_single(args, fb, torch, local)
 
+
+def time_steps(ctx, torch, flush, steps, clk=None):
+    """K evaluate() steps, L2 flushed before each; per-step CUDA-event times from the library."""
+    step_ms, p2p_ms, m2l_ms, launches, stage_acc = [], [], [], 0, {}
+    torch.cuda.synchronize()
+    for _ in range(steps):
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        ctx.evaluate()
+        t = ctx.stage_times()
+        step_ms.append(t.total_ms)
+        p2p_ms.append(t.p2p_kernel_ms)
+        m2l_ms.append(t.m2l_kernel_ms)
+        launches += t.kernel_launches
+        for k in ("build_ms", "traverse_ms", "upward_ms", "m2l_ms", "p2p_ms", "downward_ms"):
+            stage_acc[k] = stage_acc.get(k, 0.0) + getattr(t, k)
+    torch.cuda.synchronize()
+    return step_ms, p2p_ms, m2l_ms, launches, {k: v / steps for k, v in stage_acc.items()}
+
+
+def serialised_kernel_times(ctx, torch, flush, reps):
+    """Roofline pass (outside the timed steps): stages serialised so that the P2P and M2L
+    kernels each run alone (in the default overlap the L2L levels share the SMs with P2P and the
+    P2P work list with M2L)."""
+    p2p, m2l = [], []
+    ctx.set_overlap(0)
+    for _ in range(reps):
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        ctx.evaluate()
+        t = ctx.stage_times()
+        p2p.append(t.p2p_kernel_ms)
+        m2l.append(t.m2l_kernel_ms)
+    ctx.set_overlap(1)
+    return float(np.mean(p2p)), float(np.mean(m2l))
+
+
+M2L_FLOPS = {4: 335, 6: 1469, 8: 4699, 10: 12455}  # SURVEY.md section 8(d), per M2L pair
+
+
+def m2l_flops_per_pair(p):
+    """2 C(p+5, 6) (one FMA per folded term) + the D-table recurrence
+    over the n_coef(p) derivatives of degree <= p-1 (multi_index.cpp:59-85, ~10 flops each)."""
+    from math import comb
+    return M2L_FLOPS.get(p, 2 * comb(p + 5, 6) + 10 * (p * (p + 1) * (p + 2) // 6))
+
+
+def run_single(args, fb, torch, local):
     gen, n, p, n_crit, theta = CONFIGS[args.config]
     bodies = fb.generate_bodies(gen, n, 1)
     ctx = fb.Context(order=p, n_crit=n_crit, theta=theta, precision=args.precision, device=local,
@@ -358,61 +484,28 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     ctx.set_bodies_device(d_bodies.data_ptr(), n)
     # default stage order: the upward pass runs on a second stream concurrently with the
-    # traversal; M2L, P2P and the downward pass follow on one stream (P2P timed alone)
-
+    # traversal; the P2P work list beside M2L; L2L beside P2P
     for _ in range(args.warmup):
         ctx.evaluate()
     info = ctx.tree_info()
     inter = int(info.p2p_body_pairs) + int(info.n_m2l)
-
-    step_ms, p2p_ms, m2l_ms, launches = [], [], [], 0
-    stage_acc = {}
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush_l2(flush)
-            torch.cuda.synchronize()
-            ctx.evaluate()
-            t = ctx.stage_times()
-            step_ms.append(t.total_ms)
-            p2p_ms.append(t.p2p_kernel_ms)
-            m2l_ms.append(t.m2l_kernel_ms)
-            launches += t.kernel_launches
-            for k in ("build_ms", "traverse_ms", "upward_ms", "m2l_ms", "p2p_ms", "downward_ms"):
-                stage_acc[k] = stage_acc.get(k, 0.0) + getattr(t, k)
-    torch.cuda.synchronize()
-    # roofline pass (outside the timed steps): stages serialised so that the P2P kernel runs
-    # alone (in the default overlap the L2L levels share the SMs with it)
-    p2p_alone = []
-    ctx.set_overlap(0)
-    for _ in range(max(3, min(args.steps, 10))):
-        flush_l2(flush)
-        torch.cuda.synchronize()
-        ctx.evaluate()
-        p2p_alone.append(ctx.stage_times().p2p_kernel_ms)
-    ctx.set_overlap(1)
-    total_ms = float(np.sum(step_ms))
-    if dist:
-        tt = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
-    ms_per_step = total_ms / args.steps
-    value = inter * world / (ms_per_step * 1e-3)
+        step_ms, p2p_ms, m2l_ms, launches, stage_ms = time_steps(ctx, torch, flush, args.steps)
+    ms_per_step = float(np.sum(step_ms)) / args.steps
+    value = inter / (ms_per_step * 1e-3)
+    p2p_kernel, m2l_kernel = serialised_kernel_times(ctx, torch, flush, max(3, min(args.steps, 10)))
 
-    # roofline: the P2P kernel, FP32 pipe (20 flops per body pair), CUDA events around its
-    # launch in the serialised pass (the kernel runs alone)
+    # roofline: the P2P kernel (dominant at C2), 20 flops per body pair, against the peak of the
+    # pipe it runs on
     peaks = load_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     fp32 = args.precision == "fp32"
-    lanes = 128 if fp32 else 64  # FP32 / FP64 lanes per SM (FFMA2 126, DFMA 60 ops/clk/SM measured)
-    pipe_peak = sms * lanes * 2 * sm_max * 1e6 / 1e12  # TFLOP/s
+    fp32_peak = sms * 128 * 2 * sm_max * 1e6 / 1e12
+    fp64_peak = sms * 64 * 2 * sm_max * 1e6 / 1e12
+    pipe_peak = fp32_peak if fp32 else fp64_peak
     p2p_name = "k_p2p_fp32_ws" if fp32 else "k_p2p_fp64"
-    p2p_kernel = float(np.mean(p2p_alone))
     achieved = FLOPS_PER_PAIR * info.p2p_body_pairs / (p2p_kernel * 1e-3) / 1e12
-    # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -420,10 +513,38 @@ def main():
         key = f"{args.config}/{args.precision}"
         if key in tj.get("by_config", {}):
             traffic = tj["by_config"][key]["dram_bytes_per_launch"]
-        elif key == "C2/fp32":
-            traffic = tj[p2p_name]["dram_bytes_per_launch"]
     except Exception:
         traffic = None
+    # M2L: FP64 pipe (flops per pair: SURVEY.md section 8d) and its algorithmic HBM bytes
+    # (one source multipole row per pair + one local row per target), CUDA events, alone
+    ncoef = p * (p + 1) * (p + 2) // 6
+    m2l_fpp = m2l_flops_per_pair(p)
+    m2l_tf = m2l_fpp * info.n_m2l / (m2l_kernel * 1e-3) / 1e12
+    m2l_bytes = 8 * ncoef * (info.n_m2l + info.ncells)
+    m2l_kname = "k_m2l_reg<%d>" % p if p <= 6 else "k_m2l_big2<%d>" % p
+    roofline_m2l = {"bound": "fp64", "achieved": m2l_tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": m2l_tf / fp64_peak, "kernel": m2l_kname, "flops_per_unit": m2l_fpp,
+                    "unit_of_work": "M2L cell pair", "kernel_ms": m2l_kernel,
+                    "hbm_gbs_algorithmic": m2l_bytes / (m2l_kernel * 1e-3) / 1e9,
+                    "hbm_peak_gbs": float(peaks.get("hbm_gbs", 6446.6)),
+                    "peak_source": f"derived: {sms} SMs x 64 FP64 lanes x 2 x {sm_max:.0f} MHz (DFMA "
+                                   "microbenchmark 60 lane-ops/clk/SM, profiles/r1_microbench_pipes.txt)"}
+
+    # FP64 parity mode (the reference's precision): same workload, its own context and steps
+    fp64_mode = None
+    if fp32 and not args.no_fp64_mode:
+        c64 = fb.Context(order=p, n_crit=n_crit, theta=theta, precision="fp64", device=local, with_acc=True)
+        c64.set_bodies_device(d_bodies.data_ptr(), n)
+        for _ in range(3):
+            c64.evaluate()
+        k64 = max(3, min(args.steps, 10))
+        s64, p64, _, _, st64 = time_steps(c64, torch, flush, k64)
+        ms64 = float(np.mean(s64))
+        a64 = FLOPS_PER_PAIR * info.p2p_body_pairs / (float(np.mean(p64)) * 1e-3) / 1e12
+        fp64_mode = {"ms_per_step": ms64, "value": inter / (ms64 * 1e-3), "unit": UNIT, "steps": k64,
+                     "stage_ms": st64, "p2p_kernel": "k_p2p_fp64", "p2p_kernel_ms": float(np.mean(p64)),
+                     "p2p_frac_of_fp64_peak": a64 / fp64_peak}
+        c64.close()
 
     # e2e through the C-ABI with host buffers (pinned), H2D + step + D2H in the timed region
     e2e = None
@@ -439,8 +560,6 @@ def main():
             lib.fmm_set_bodies(ctx.h, ptr(h_in), n)
             lib.fmm_evaluate(ctx.h)
             lib.fmm_get_results(ctx.h, ptr(h_phi), ptr(h_acc), 1)
-        if dist:
-            dist.barrier()
         torch.cuda.synchronize()
         ts = []
         for _ in range(args.steps):
@@ -453,62 +572,63 @@ def main():
             ts.append(time.perf_counter() - t0)
             assert rc == 0, lib.fmm_last_error(ctx.h)
         e2e_ms = float(np.mean(ts)) * 1e3
-        if dist:
-            tt = torch.tensor([e2e_ms], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_ms = float(tt.item())
-        e2e = {"value": inter * world / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": int(n * 32), "d2h_bytes_per_step": int(n * 8 * 4)}
+        e2e = {"value": inter / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(n * 32), "d2h_bytes_per_step": int(n * 8 * 4),
+               "path": "fmm_set_bodies(host) + fmm_evaluate + fmm_get_results(host, input order)"}
 
+    # CPU baseline: the unmodified reference (oracle/_ref) at the same N, all host cores, 1 step
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline:
         try:
             import oracle
-            if oracle.reference_available():
-                r = cpu_reference_sample(gen, n, p, n_crit, theta, args.ref_sample)
+            if oracle.reference_available() and n <= (1 << 20):
+                r = cpu_reference(gen, n, p, n_crit, theta, steps=1)
                 cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
-                       "sample": r["sample"]}
+                       "sample": r["sample"], "ms_per_step": r["ms_per_step"], "stage_ms": r["stage_ms"]}
+            elif oracle.reference_available():
+                nr = 1 << 20
+                r = cpu_reference(gen, nr, p, n_crit, theta, steps=1)
+                cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
+                       "sample": f"N={nr} sample of the {args.config} distribution (full N would take "
+                                 f"minutes per step): " + r["sample"],
+                       "ms_per_step": r["ms_per_step"], "stage_ms": r["stage_ms"]}
             else:
                 cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                        "sample": "oracle/_ref not built"}
         except Exception as e:  # the baseline never blocks the GPU number
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 P2P / f64 expansions"
-            if args.precision == "fp32" else "f64",
-            "data": "synthetic (BASELINE C2 generator: reference xorshift64*, seed 1+rank)",
-            "config": {"workload": f"{args.config}: N={n} uniform [-1,1]^3, p={p}, n_crit={n_crit}, "
-                                   f"theta={theta}, potential+acceleration",
-                       "n_bodies": n, "order": p, "n_crit": n_crit, "theta": theta,
-                       "precision": args.precision, "l2": "flushed (256 MB write) between steps",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
-            "interactions_per_step": inter, "p2p_body_pairs": int(info.p2p_body_pairs),
-            "m2l_pairs": int(info.n_m2l), "p2p_pairs_per_s": info.p2p_body_pairs / (ms_per_step * 1e-3),
-            "m2l_pairs_per_s": info.n_m2l / (ms_per_step * 1e-3),
-            "stage_ms": {k: v / args.steps for k, v in stage_acc.items()},
-            "p2p_kernel_ms": p2p_kernel, "m2l_kernel_ms": float(np.mean(m2l_ms)),
-            "roofline": {"bound": "fp32" if fp32 else "fp64", "achieved": achieved, "peak": pipe_peak,
-                         "unit": "TFLOP/s", "frac": achieved / pipe_peak, "traffic": traffic,
-                         "traffic_unit": f"bytes per launch (dram read + write, ncu, {args.config} "
-                                         f"{args.precision}; profiles/ncu_traffic.json)",
-                         "kernel": p2p_name, "flops_per_unit": FLOPS_PER_PAIR,
-                         "timing": "CUDA events around the P2P launch in a serialised pass after the timed steps (the kernel runs alone), L2 flushed",
-                         "peak_source": f"derived: {sms} SMs x {lanes} {'FP32' if fp32 else 'FP64'} lanes x 2 x "
-                                        f"{sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json; "
-                                        + ("FFMA2 microbenchmark measured 126-128 lane-ops/clk/SM)" if fp32 else
-                                           "DFMA microbenchmark measured 60 lane-ops/clk/SM)")},
-            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
-            "gpu_launches": launches, "tree": {"ncells": info.ncells, "nleaves": info.nleaves,
-                                               "depth": info.depth},
-        }
-        print(json.dumps(line))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 P2P / f64 expansions" if fp32 else "f64",
+        "data": "synthetic (BASELINE generator: reference xorshift64*, seed 1)",
+        "config": workload_config(args.config, n), "precision": args.precision,
+        "interactions_per_step": inter, "p2p_body_pairs": int(info.p2p_body_pairs),
+        "m2l_pairs": int(info.n_m2l), "p2p_pairs_per_s": info.p2p_body_pairs / (ms_per_step * 1e-3),
+        "m2l_pairs_per_s": info.n_m2l / (ms_per_step * 1e-3),
+        "stage_ms": stage_ms, "p2p_kernel_ms": p2p_kernel, "m2l_kernel_ms": m2l_kernel,
+        "roofline": {"bound": "fp32" if fp32 else "fp64", "achieved": achieved, "peak": pipe_peak,
+                     "unit": "TFLOP/s", "frac": achieved / pipe_peak, "traffic": traffic,
+                     "traffic_unit": f"bytes per launch (dram read + write, ncu, {args.config} "
+                                     f"{args.precision}; profiles/ncu_traffic.json)",
+                     "kernel": p2p_name, "flops_per_unit": FLOPS_PER_PAIR,
+                     "unit_of_work": "target-source body pair (n_t * n_s per P2P leaf pair)",
+                     "timing": "CUDA events around the P2P launch in a serialised pass after the timed "
+                               "steps (the kernel runs alone), L2 flushed",
+                     "peak_source": f"derived: {sms} SMs x {128 if fp32 else 64} {'FP32' if fp32 else 'FP64'} "
+                                    f"lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json, which "
+                                    "has no FP32/FP64 figure; microbenchmarks: FFMA2 126-128, DFMA 60 "
+                                    "lane-ops/clk/SM). Flop convention: 20 per pair (SURVEY 8d), rsqrt = 2 "
+                                    "flops in both precisions"},
+        "roofline_m2l": roofline_m2l, "fp64_mode": fp64_mode,
+        "e2e": e2e, "cpu_baseline": cpu, "clocks": clk.summary(),
+        "gpu_launches": launches, "tree": {"ncells": info.ncells, "nleaves": info.nleaves,
+                                           "depth": info.depth},
+    }
+    print(json.dumps(line))
     ctx.close()
-    if dist:
-        dist.destroy_process_group()
     return 0
 
 

@@ -123,6 +123,14 @@ int fmm_set_overlap(fmm_ctx* ctx, int on);
  * The GPU executes the symmetrised lists with target-owned writes (no atomics): results equal
  * the non-mutual mode's. Invalidates the current lists. Not supported with fmm_set_partition. */
 int fmm_set_mutual(fmm_ctx* ctx, int on);
+/* Test hook for the traversal's rarely taken paths (the production choice is automatic):
+ * force_keys64 = 1 emits 64-bit (target, source) keys with the ordered look-back emission even
+ * when the tree has <= 2^16 cells (the path C3-C5 take); initial_capacity > 0 starts the
+ * frontier and list buffers at that many entries so the overflow regrow-and-rerun runs (the
+ * path C4 needs); 0 restores the default sizing. *regrows (optional) = rerun attempts of the
+ * last traversal. */
+int fmm_set_traversal_debug(fmm_ctx* ctx, int force_keys64, int64_t initial_capacity);
+int fmm_get_traversal_regrows(fmm_ctx* ctx, int* regrows);
 
 /* ---- outputs ------------------------------------------------------------------------ */
 /* order: 0 = tree (sorted) body order (potentials(), tree.cpp:121-126), 1 = input order.

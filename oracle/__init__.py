@@ -202,6 +202,11 @@ class Oracle:
         L.orc_n_coef.restype = C.c_int64
         L.orc_n_coef.argtypes = [C.c_int64]
         L.orc_index_of.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.orc_evaluate_par.argtypes = [C.POINTER(_Tree), C.c_double, C.c_int, C.c_void_p, _u64p,
+                                       _i64p, _i64p]
+        L.orc_group_by_target.argtypes = [C.c_int64, C.c_int64, _i32p, _i64p, _i32p, C.c_int]
+        L.orc_direct_sum_targets.argtypes = [C.c_int64, _dp, _dp, C.c_int64, _i64p, _dp, _dp]
+        L.orc_generate_baseline_bodies.argtypes = [C.c_int, C.c_int64, C.c_uint64, _dp]
 
     # ---- tree / traversal / pipeline ------------------------------------------------
     def build_tree(self, xyzq: np.ndarray, n_crit: int, p: int) -> OracleTree:
@@ -236,6 +241,62 @@ class Oracle:
         if rc:
             raise OracleError(ERRORS.get(rc, str(rc)))
         return ev.value, nm.value, npp.value
+
+    def evaluate_par(self, tree: OracleTree, theta: float, with_acc: bool = True,
+                     leaf_mask: np.ndarray | None = None):
+        """Non-mutual pipeline on all host cores (OpenMP), bit-identical to ``evaluate``.
+        leaf_mask (bool per cell) limits phi/acc to the marked leaves. Returns
+        (p2p_evals, n_m2l, n_p2p)."""
+        ev, nm, npp = C.c_uint64(), C.c_int64(), C.c_int64()
+        mask = None
+        if leaf_mask is not None:
+            mask = np.ascontiguousarray(leaf_mask, dtype=np.uint8)
+            assert len(mask) == tree.ncells
+        rc = self.lib.orc_evaluate_par(C.byref(tree._t), theta, int(with_acc),
+                                       mask.ctypes.data if mask is not None else None,
+                                       C.byref(ev), C.byref(nm), C.byref(npp))
+        if rc:
+            raise OracleError(ERRORS.get(rc, str(rc)))
+        return ev.value, nm.value, npp.value
+
+    def group_by_target(self, ncells: int, pairs: np.ndarray, sort_sources: bool = True):
+        """(offsets[ncells+1], sources): CSR by target; sources ascending per target when
+        sort_sources (the canonical multiset form, comparable with fmm_get_lists)."""
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        off = np.zeros(ncells + 1, np.int64)
+        src = np.zeros(max(len(pairs), 1), np.int32)
+        rc = self.lib.orc_group_by_target(ncells, len(pairs), _ptr(pairs, _i32p), _ptr(off, _i64p),
+                                          _ptr(src, _i32p), int(sort_sources))
+        if rc:
+            raise OracleError("bad target index")
+        return off, src[:len(pairs)]
+
+    def lists_csr(self, tree: OracleTree, theta: float, mutual: bool = False):
+        """Traversal lists as canonical CSR: (m2l_off, m2l_src, p2p_off, p2p_src)."""
+        m, p = self.traverse(tree, theta, mutual)
+        mo, ms = self.group_by_target(tree.ncells, m)
+        del m
+        po, ps = self.group_by_target(tree.ncells, p)
+        return mo, ms, po, ps
+
+    def direct_sum_targets(self, pos: np.ndarray, q: np.ndarray, idx: np.ndarray):
+        """Long-double direct sum (oracle.cpp:8-23 + acc) for the listed targets only."""
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        phi = np.zeros(len(idx))
+        acc = np.zeros((len(idx), 3))
+        self.lib.orc_direct_sum_targets(len(q), _ptr(pos, _dp), _ptr(q, _dp), len(idx),
+                                        _ptr(idx, _i64p), _ptr(phi, _dp), _ptr(acc, _dp))
+        return phi, acc
+
+    def generate_baseline_bodies(self, config: int, n: int, seed: int = 1) -> np.ndarray:
+        """BASELINE.json config 1..5 bodies (AoS x, y, z, q), SURVEY.md section 8d."""
+        out = np.zeros((n, 4))
+        rc = self.lib.orc_generate_baseline_bodies(config, n, seed, _ptr(out, _dp))
+        if rc:
+            raise OracleError(ERRORS.get(rc, str(rc)))
+        return out
 
     def direct_sum(self, pos: np.ndarray, q: np.ndarray, with_acc: bool = True):
         pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)

@@ -856,3 +856,253 @@ int orc_generate_reference_bodies(int dist, int64_t n, uint64_t seed, double* xy
   for (int64_t i = 0; i < n; ++i) xyzq[4 * i + 3] -= mean;
   return ORC_OK;
 }
+
+/* ------------------------------------------------- parallel checker (tests only) -- */
+/* The non-mutual pipeline of orc_evaluate, split so that it runs on all host cores and stays
+ * BIT-IDENTICAL to the serial version: every accumulation target sees its contributions in the
+ * serial order.
+ *   upward   level by level, deepest first (tree.cpp builds cells in BFS order, so a level is a
+ *            contiguous range; a parent reads only its children, in child order);
+ *   lists    the FIFO-emitted lists of orc_traverse, grouped by target with a STABLE counting
+ *            sort (each target keeps its emission order, KernelVisitor traversal.hpp:138-164);
+ *   kernels  one target cell per task: its M2L sources then its P2P sources in that order (M2L
+ *            writes locals, P2P writes body potentials: the serial interleaving of the two is
+ *            irrelevant);
+ *   downward level by level, root first (traversal.cpp:52-63).
+ * cell_mask (optional, ncells bytes): evaluate only the marked leaves; their ancestors are
+ * added here. Unmarked leaves keep phi = acc = 0 and unmarked cells' locals are not formed. */
+static int orc_level_ranges(const orc_tree* t, int64_t* lb /* [ORC_MAX_TREE_LEVEL + 2] */, int* nlev) {
+  int L = -1;
+  for (int64_t ci = 0; ci < t->ncells; ++ci) {
+    const int lv = t->cells[ci].level;
+    if (lv < L || lv > ORC_MAX_TREE_LEVEL) return 1; /* not BFS ordered */
+    while (L < lv) lb[++L] = ci;
+  }
+  lb[L + 1] = t->ncells;
+  *nlev = L + 1;
+  return 0;
+}
+
+int orc_group_by_target(int64_t ncells, int64_t n, const int32_t* pairs, int64_t* offsets,
+                        int32_t* sources, int sort_sources) {
+  memset(offsets, 0, sizeof(int64_t) * (size_t)(ncells + 1));
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t tt = pairs[2 * i];
+    if (tt < 0 || tt >= ncells) return ORC_ERR_ALLOC;
+    ++offsets[tt + 1];
+  }
+  for (int64_t c = 0; c < ncells; ++c) offsets[c + 1] += offsets[c];
+  int64_t* fill = malloc(sizeof(int64_t) * (size_t)(ncells > 0 ? ncells : 1));
+  if (!fill) return ORC_ERR_ALLOC;
+  memcpy(fill, offsets, sizeof(int64_t) * (size_t)ncells);
+  for (int64_t i = 0; i < n; ++i) sources[fill[pairs[2 * i]]++] = pairs[2 * i + 1];
+  free(fill);
+  if (sort_sources) {
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t c = 0; c < ncells; ++c) { /* insertion sort: lists are short or nearly sorted */
+      int32_t* s = sources + offsets[c];
+      const int64_t k = offsets[c + 1] - offsets[c];
+      for (int64_t i = 1; i < k; ++i) {
+        const int32_t v = s[i];
+        int64_t j = i - 1;
+        while (j >= 0 && s[j] > v) { s[j + 1] = s[j]; --j; }
+        s[j + 1] = v;
+      }
+    }
+  }
+  return ORC_OK;
+}
+
+int orc_evaluate_par(orc_tree* t, double theta, int with_acc, const uint8_t* cell_mask,
+                     uint64_t* p2p_evals, int64_t* n_m2l_out, int64_t* n_p2p_out) {
+  orc_tables kt;
+  int rc = orc_tables_init(&kt, t->order);
+  if (rc) return rc;
+  const int nc = kt.n;
+  int64_t lb[ORC_MAX_TREE_LEVEL + 2];
+  int nlev = 0;
+  if (orc_level_ranges(t, lb, &nlev)) {
+    orc_tables_free(&kt);
+    return ORC_ERR_ALLOC;
+  }
+  uint8_t* active = malloc((size_t)t->ncells);
+  if (!active) { orc_tables_free(&kt); return ORC_ERR_ALLOC; }
+  if (cell_mask) {
+    memset(active, 0, (size_t)t->ncells);
+    for (int64_t ci = t->ncells - 1; ci >= 0; --ci) /* children follow parents */
+      if (cell_mask[ci] || active[ci]) {
+        active[ci] = 1;
+        if (t->cells[ci].parent >= 0) active[t->cells[ci].parent] = 1;
+      }
+  } else {
+    memset(active, 1, (size_t)t->ncells);
+  }
+  /* upward (traversal.cpp:36-50), every cell: sources may be anywhere */
+  for (int L = nlev - 1; L >= 0; --L) {
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t ci = lb[L]; ci < lb[L + 1]; ++ci) {
+      const orc_cell* c = &t->cells[ci];
+      double* M = t->multipole + ci * nc;
+      if (c->child_count == 0) {
+        orc_p2m(&kt, c->body_end - c->body_begin, t->pos + 3 * (int64_t)c->body_begin,
+                t->q + c->body_begin, c->center, M);
+      } else {
+        for (int32_t k = 0; k < c->child_count; ++k) {
+          const orc_cell* ch = &t->cells[c->child_begin + k];
+          const double shift[3] = {ch->center[0] - c->center[0], ch->center[1] - c->center[1],
+                                   ch->center[2] - c->center[2]};
+          orc_m2m(&kt, t->multipole + (int64_t)(c->child_begin + k) * nc, shift, M);
+        }
+      }
+    }
+  }
+  int64_t nm = 0, np = 0;
+  int32_t *m2l = NULL, *p2p = NULL;
+  rc = orc_traverse(t, theta, 0, &nm, &m2l, &np, &p2p);
+  int64_t *mo = NULL, *po = NULL;
+  int32_t *ms = NULL, *ps = NULL;
+  if (!rc) {
+    mo = malloc(sizeof(int64_t) * (size_t)(t->ncells + 1));
+    po = malloc(sizeof(int64_t) * (size_t)(t->ncells + 1));
+    ms = malloc(sizeof(int32_t) * (size_t)(nm > 0 ? nm : 1));
+    ps = malloc(sizeof(int32_t) * (size_t)(np > 0 ? np : 1));
+    if (!mo || !po || !ms || !ps) rc = ORC_ERR_ALLOC;
+  }
+  if (!rc) rc = orc_group_by_target(t->ncells, nm, m2l, mo, ms, 0);
+  if (!rc) rc = orc_group_by_target(t->ncells, np, p2p, po, ps, 0);
+  free(m2l);
+  free(p2p);
+  uint64_t ev = 0;
+  int err = 0;
+  if (!rc) {
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : ev)
+    for (int64_t ci = 0; ci < t->ncells; ++ci) {
+      if (!active[ci]) continue;
+      for (int64_t k = mo[ci]; k < mo[ci + 1]; ++k)
+        if (apply_m2l(t, &kt, (int32_t)ci, ms[k], 0)) {
+#pragma omp atomic write
+          err = ORC_ERR_SINGULAR_M2L;
+        }
+      for (int64_t k = po[ci]; k < po[ci + 1]; ++k) ev += apply_p2p(t, (int32_t)ci, ps[k], 0, with_acc);
+    }
+    rc = err;
+  }
+  free(mo); free(po); free(ms); free(ps);
+  if (!rc) {
+    double* acc_save = t->acc;
+    if (!with_acc) t->acc = NULL;
+    for (int L = 0; L < nlev; ++L) { /* downward (traversal.cpp:52-63) */
+#pragma omp parallel for schedule(dynamic, 16)
+      for (int64_t ci = lb[L]; ci < lb[L + 1]; ++ci) {
+        if (!active[ci]) continue;
+        const orc_cell* c = &t->cells[ci];
+        if (c->parent >= 0) {
+          const orc_cell* pc = &t->cells[c->parent];
+          const double shift[3] = {c->center[0] - pc->center[0], c->center[1] - pc->center[1],
+                                   c->center[2] - pc->center[2]};
+          orc_l2l(&kt, t->local + (int64_t)c->parent * nc, shift, t->local + ci * nc);
+        }
+        if (c->child_count == 0)
+          orc_l2p(&kt, t->local + ci * nc, c->center, c->body_end - c->body_begin,
+                  t->pos + 3 * (int64_t)c->body_begin, t->phi + c->body_begin,
+                  t->acc ? t->acc + 3 * (int64_t)c->body_begin : NULL);
+      }
+    }
+    t->acc = acc_save;
+  }
+  free(active);
+  orc_tables_free(&kt);
+  if (p2p_evals) *p2p_evals = ev;
+  if (n_m2l_out) *n_m2l_out = nm;
+  if (n_p2p_out) *n_p2p_out = np;
+  return rc;
+}
+
+/* Direct sum over a subset of targets (oracle.cpp:8-23 + acc), all N sources, parallel over
+ * targets; idx are input-order indices, outputs are per listed target. */
+void orc_direct_sum_targets(int64_t n, const double* pos, const double* q, int64_t nt,
+                            const int64_t* idx, double* phi, double* acc) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t k = 0; k < nt; ++k) {
+    const int64_t i = idx[k];
+    long double s = 0.0L, ax = 0.0L, ay = 0.0L, az = 0.0L;
+    for (int64_t j = 0; j < n; ++j) {
+      if (j == i) continue;
+      const double dx = pos[3 * i] - pos[3 * j], dy = pos[3 * i + 1] - pos[3 * j + 1],
+                   dz = pos[3 * i + 2] - pos[3 * j + 2];
+      const double r2 = (dx * dx + dy * dy) + dz * dz;
+      if (r2 == 0.0) continue;
+      const long double inv_r = 1.0L / sqrtl((long double)r2);
+      s += (long double)q[j] * inv_r;
+      const long double w = (long double)q[j] * inv_r * inv_r * inv_r;
+      ax += w * (long double)dx;
+      ay += w * (long double)dy;
+      az += w * (long double)dz;
+    }
+    phi[k] = (double)s;
+    if (acc) {
+      acc[3 * k] = (double)ax;
+      acc[3 * k + 1] = (double)ay;
+      acc[3 * k + 2] = (double)az;
+    }
+  }
+}
+
+/* BASELINE.json configs 1..5, an independent restatement for the checker and
+ * the reference arm: the reference's xorshift64* (dataset.cpp:10-34), seed per config, per body
+ * the position (Vec3(u(),u(),u()) evaluated right to left by g++: z first) then the charge.
+ *   1, 2, 4  uniform [-1,1]^3, q = (1 - u01)/N in (0, 1/N]
+ *   3        Plummer: r = 1/sqrt(U^(-2/3) - 1), resampled while r > 100 or not finite;
+ *            direction by cube rejection (s > 1 or s < 1e-8 rejected); q = 1/N
+ *   5        unit sphere surface: Box-Muller sqrt(-2 ln(1-u1)) cos(2 pi u2) per axis (z first),
+ *            normalised; q = uniform(-1,1)/N */
+int orc_generate_baseline_bodies(int config, int64_t n, uint64_t seed, double* xyzq) {
+  if (n < 1) return ORC_ERR_EMPTY_INPUT;
+  if (config < 1 || config > 5) return ORC_ERR_ALLOC;
+  orc_rng r;
+  orc_rng_init(&r, seed);
+  const double dn = (double)n;
+  const double two_pi = 6.283185307179586;
+  for (int64_t i = 0; i < n; ++i) {
+    double* b = xyzq + 4 * i;
+    if (config == 3) {
+      double rad;
+      do {
+        const double U = orc_rng_uniform01(&r);
+        rad = 1.0 / sqrt(pow(U, -2.0 / 3.0) - 1.0);
+      } while (!(rad <= 100.0) || !isfinite(rad));
+      double v[3], s;
+      do {
+        v[2] = orc_rng_uniform(&r, -1.0, 1.0);
+        v[1] = orc_rng_uniform(&r, -1.0, 1.0);
+        v[0] = orc_rng_uniform(&r, -1.0, 1.0);
+        s = (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2];
+      } while (s > 1.0 || s < 1e-8);
+      const double inv = rad / sqrt(s);
+      b[0] = v[0] * inv;
+      b[1] = v[1] * inv;
+      b[2] = v[2] * inv;
+      b[3] = 1.0 / dn;
+    } else if (config == 5) {
+      double v[3], s;
+      do {
+        for (int d = 2; d >= 0; --d) {
+          const double u1 = orc_rng_uniform01(&r), u2 = orc_rng_uniform01(&r);
+          v[d] = sqrt(-2.0 * log(1.0 - u1)) * cos(two_pi * u2);
+        }
+        s = (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2];
+      } while (s == 0.0);
+      const double inv = 1.0 / sqrt(s);
+      b[0] = v[0] * inv;
+      b[1] = v[1] * inv;
+      b[2] = v[2] * inv;
+      b[3] = orc_rng_uniform(&r, -1.0, 1.0) / dn;
+    } else {
+      b[2] = orc_rng_uniform(&r, -1.0, 1.0);
+      b[1] = orc_rng_uniform(&r, -1.0, 1.0);
+      b[0] = orc_rng_uniform(&r, -1.0, 1.0);
+      b[3] = (1.0 - orc_rng_uniform01(&r)) / dn;
+    }
+  }
+  return ORC_OK;
+}

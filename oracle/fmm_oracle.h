@@ -151,6 +151,22 @@ int orc_apply_lists(orc_tree* t, const orc_tables* kt, int64_t n_m2l, const int3
 int orc_evaluate(orc_tree* t, double theta, int mutual, int with_acc, uint64_t* p2p_evals,
                  int64_t* n_m2l, int64_t* n_p2p);
 
+/* Parallel checker (OpenMP), bit-identical to orc_evaluate for the non-mutual mode: upward and
+ * downward level by level, kernels per target cell with each target's contributions applied in
+ * the FIFO emission order. cell_mask (ncells bytes, optional) restricts phi/acc to the marked
+ * leaves (ancestors added internally). */
+int orc_evaluate_par(orc_tree* t, double theta, int with_acc, const uint8_t* cell_mask,
+                     uint64_t* p2p_evals, int64_t* n_m2l, int64_t* n_p2p);
+/* Stable counting sort of (target, source) pairs into CSR by target; sort_sources = 1 sorts
+ * each target's sources ascending (the canonical multiset form). */
+int orc_group_by_target(int64_t ncells, int64_t n, const int32_t* pairs, int64_t* offsets,
+                        int32_t* sources, int sort_sources);
+/* direct_sum restricted to the listed targets (input order indices), all sources. */
+void orc_direct_sum_targets(int64_t n, const double* pos, const double* q, int64_t nt,
+                            const int64_t* idx, double* phi, double* acc);
+/* BASELINE.json configs 1..5; output AoS xyzq. */
+int orc_generate_baseline_bodies(int config, int64_t n, uint64_t seed, double* xyzq);
+
 /* direct_sum (oracle.cpp:8-23) in long double; acc extension; input order arrays. */
 void orc_direct_sum(int64_t n, const double* pos, const double* q, double* phi, double* acc);
 /* compare (oracle.cpp:25-47). Returns 0 or ORC_ERR_EMPTY_INPUT-free status. */

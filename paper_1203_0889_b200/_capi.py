@@ -98,6 +98,8 @@ SIGNATURES = {
     "fmm_synchronize": (C.c_int, [_vp]),
     "fmm_set_overlap": (C.c_int, [_vp, C.c_int]),
     "fmm_set_mutual": (C.c_int, [_vp, C.c_int]),
+    "fmm_set_traversal_debug": (C.c_int, [_vp, C.c_int, C.c_int64]),
+    "fmm_get_traversal_regrows": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "fmm_update_bodies": (C.c_int, [_vp, _dp, C.c_int64]),
     "fmm_evaluate_reuse": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "fmm_get_stage_trace": (C.c_int, [_vp, _vp, C.c_int, C.POINTER(C.c_int)]),

@@ -717,6 +717,22 @@ int fmm_set_mutual(fmm_ctx* c, int on) {
   });
 }
 
+int fmm_set_traversal_debug(fmm_ctx* c, int force_keys64, int64_t initial_capacity) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (initial_capacity < 0) fail(FMM_ERR_ARG, "initial_capacity must be >= 0");
+    c->dbg_keys64 = force_keys64 != 0;
+    c->dbg_cap = initial_capacity;
+    c->have_lists = c->have_L = c->have_out = false;
+  });
+}
+
+int fmm_get_traversal_regrows(fmm_ctx* c, int* regrows) {
+  if (!c || !regrows) return FMM_ERR_ARG;
+  *regrows = c->trav_regrows;
+  return FMM_OK;
+}
+
 // ---------------------------------------------------------------------- sharding -------
 int fmm_set_partition(fmm_ctx* c, int rank, int world) {
   if (!c) return FMM_ERR_ARG;

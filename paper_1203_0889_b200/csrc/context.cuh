@@ -106,6 +106,9 @@ struct fmm_ctx {
   fmmb::DBuf<uint32_t> lb_flag;             // traversal look-back: per-chunk status (epoch tagged)
   fmmb::DBuf<uint64_t> lb_val;              // traversal look-back: per-chunk aggregate / prefix
   uint32_t trav_epoch = 0;                  // one epoch per k_step launch
+  bool dbg_keys64 = false;                  // test hook: 64-bit keys on any tree
+  int64_t dbg_cap = 0;                      // test hook: initial traversal buffer capacity
+  int trav_regrows = 0;                     // rerun attempts of the last traversal
   fmmb::DBuf<int32_t> bnd;           // child boundaries of one level (9 per cell)
   fmmb::DBuf<int32_t> bnd_lev;       // device level table (tree build)
   int last_depth = 6;                // depth of the previous build (level batch, sorted digits)

@@ -338,7 +338,7 @@ int bits_for(uint64_t v) {
 // Keys are 32-bit when 2 * ceil(log2 ncells) <= 32 (half the sort traffic), else 64-bit.
 inline bool small_keys(int64_t ncells) { return 2 * bits_for(static_cast<uint64_t>(ncells)) <= 32; }
 // mutual mode carries the mirror flag in bit 63: always 64-bit keys
-inline bool keys32(const fmm_ctx* c) { return !c->cfg.mutual && small_keys(c->ncells); }
+inline bool keys32(const fmm_ctx* c) { return !c->cfg.mutual && !c->dbg_keys64 && small_keys(c->ncells); }
 
 template <class KeyT>
 void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int32_t>& src, uint8_t* mir,
@@ -467,9 +467,9 @@ void traverse(fmm_ctx* c) {
   unsigned long long* ctr = reinterpret_cast<unsigned long long*>(c->trav_ctr.ensure(128));
   unsigned long long* h = reinterpret_cast<unsigned long long*>(c->hpin);
   // first call: capacities from the cell count; afterwards the buffers keep their size
-  const int64_t want_f = std::max<int64_t>(c->ncells * 256, 1 << 16);
-  const int64_t want_m = std::max<int64_t>(c->ncells * 512, 1 << 16);
-  const int64_t want_p = std::max<int64_t>(c->nleaves * 256, 1 << 16);
+  const int64_t want_f = c->dbg_cap > 0 ? c->dbg_cap : std::max<int64_t>(c->ncells * 256, 1 << 16);
+  const int64_t want_m = c->dbg_cap > 0 ? c->dbg_cap : std::max<int64_t>(c->ncells * 512, 1 << 16);
+  const int64_t want_p = c->dbg_cap > 0 ? c->dbg_cap : std::max<int64_t>(c->nleaves * 256, 1 << 16);
   if (c->pairs_a.cap < static_cast<size_t>(want_f)) c->pairs_a.ensure(want_f);
   if (c->pairs_d.cap < static_cast<size_t>(want_f)) c->pairs_d.ensure(want_f);
   if (c->m2l_keys.cap < static_cast<size_t>(want_m)) c->m2l_keys.ensure(want_m);
@@ -482,6 +482,7 @@ void traverse(fmm_ctx* c) {
   const int32_t tb0 = static_cast<int32_t>(filter ? c->shard_b0 : 0);
   const int32_t tb1 = static_cast<int32_t>(filter ? c->shard_b1 : c->N);
   for (int attempt = 0;; ++attempt) {
+    c->trav_regrows = attempt;
     const int64_t cap_f = static_cast<int64_t>(std::min(c->pairs_a.cap, c->pairs_d.cap));
     // KeyT buffers are uint64_t arrays; 32-bit keys use twice the count
     const int64_t cap_m = static_cast<int64_t>(c->m2l_keys.cap) * (small ? 2 : 1);
@@ -528,7 +529,7 @@ void traverse(fmm_ctx* c) {
     // whose frontier was truncated; the levels after it saw a partial frontier and their counts
     // are lower bounds. Grow each buffer to its count (+ slack), and at least double the ones
     // that may be underestimated; every attempt completes at least one more level.
-    if (attempt >= 8) fail(FMM_ERR_CUDA, "traverse: output overflow after regrow");
+    if (attempt >= 24) fail(FMM_ERR_CUDA, "traverse: output overflow after regrow");
     bool trunc = false;
     int64_t fgrow = 0;
     for (int L = 0; L <= nlev; ++L) {

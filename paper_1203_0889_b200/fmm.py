@@ -172,6 +172,16 @@ class Context:
         self._c(self.lib.fmm_set_mutual(self.h, int(on)))
         self.cfg.mutual = int(on)
 
+    def set_traversal_debug(self, force_keys64: bool = False, initial_capacity: int = 0):
+        """Test hook (fmm_set_traversal_debug): force the 64-bit-key ordered emission and/or a
+        small initial buffer capacity so the overflow regrow path runs."""
+        self._c(self.lib.fmm_set_traversal_debug(self.h, int(force_keys64), int(initial_capacity)))
+
+    def traversal_regrows(self) -> int:
+        r = C.c_int(0)
+        self._c(self.lib.fmm_get_traversal_regrows(self.h, C.byref(r)))
+        return r.value
+
     # outputs
     def results(self, order: str = "tree", with_acc: bool = True):
         phi = np.zeros(self.n)

@@ -259,3 +259,58 @@ def test_acc_extension_fmm_vs_direct(orc):
         _, acc_d = orc.direct_sum(t.positions(), t.charges())
         errs.append(orc.compare(t.acc().ravel(), acc_d.ravel())[0])
     assert errs[1] < errs[0] and errs[0] < 5e-2 and errs[1] < 5e-4
+
+
+@pytest.mark.parametrize("case", [(1, 16384, 4, 64, 0.5), (3, 30000, 6, 64, 0.5),
+                                  (5, 20000, 10, 64, 0.5), (4, 40000, 8, 128, 0.4)],
+                         ids=["C1", "C3", "C5", "C4"])
+def test_parallel_checker_is_bit_identical(orc, case):
+    """orc_evaluate_par (OpenMP, used by the full-size GPU parity tests) reproduces the serial
+    pipeline bit for bit: potentials, accelerations, multipoles, locals, counts; a leaf mask
+    gives the same bits on the marked leaves."""
+    cfg, n, p, n_crit, theta = case
+    bodies = orc.generate_baseline_bodies(cfg, n, 1)
+    ts = orc.build_tree(bodies, n_crit, p)
+    rs = orc.evaluate(ts, theta, with_acc=True)
+    tp = orc.build_tree(bodies, n_crit, p)
+    rp = orc.evaluate_par(tp, theta, with_acc=True)
+    assert rs == rp
+    for a, b in ((ts.phi(), tp.phi()), (ts.acc(), tp.acc()), (ts.multipoles(), tp.multipoles()),
+                 (ts.locals(), tp.locals())):
+        assert np.array_equal(a, b)
+    c = tp.cells()
+    leaves = np.flatnonzero(c.child_count == 0)[::5]
+    mask = np.zeros(tp.ncells, bool)
+    mask[leaves] = True
+    tm = orc.build_tree(bodies, n_crit, p)
+    orc.evaluate_par(tm, theta, with_acc=True, leaf_mask=mask)
+    sel = np.concatenate([np.arange(c.body_begin[k], c.body_end[k]) for k in leaves])
+    assert np.array_equal(tm.phi()[sel], ts.phi()[sel])
+    assert np.array_equal(tm.acc()[sel], ts.acc()[sel])
+
+
+def test_lists_csr_canonical(orc):
+    """CSR grouping of the FIFO lists: offsets = per-target counts, sources ascending, same
+    multiset as the emitted pairs."""
+    bodies = orc.generate_baseline_bodies(3, 20000, 2)
+    t = orc.build_tree(bodies, 64, 6)
+    m, p = orc.traverse(t, 0.5)
+    mo, ms, po, ps = orc.lists_csr(t, 0.5)
+    for pairs, off, src in ((m, mo, ms), (p, po, ps)):
+        assert off[-1] == len(pairs)
+        assert np.array_equal(np.diff(off), np.bincount(pairs[:, 0], minlength=t.ncells))
+        tgt = np.repeat(np.arange(t.ncells, dtype=np.int64), np.diff(off))
+        keys = (tgt << 32) | src.astype(np.int64)
+        assert np.all(np.diff(keys) > 0)  # strictly ascending: no duplicate pairs
+        ref = np.sort((pairs[:, 0].astype(np.int64) << 32) | pairs[:, 1].astype(np.int64))
+        assert np.array_equal(keys, ref)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_baseline_generator_matches_library(orc, cfg):
+    """The oracle's BASELINE generator (used by the reference arm, which must not load the
+    product library) is bit-identical to fmm_generate_bodies (host code, no GPU needed)."""
+    import paper_1203_0889_b200 as fb
+    a = orc.generate_baseline_bodies(cfg, 5000, 7)
+    b = fb.generate_bodies(cfg, 5000, 7)
+    assert np.array_equal(a, b)
