@@ -82,6 +82,7 @@ typedef struct {
   float p2p_kernel_ms;   /* the P2P kernel alone (roofline numerator's denominator) */
   float m2l_kernel_ms;   /* the M2L kernel alone */
   int32_t p2p_launches, m2l_launches, kernel_launches;
+  float exchange_ms;     /* sharded step: the NCCL all-gather of the multipoles (0 otherwise) */
 } fmm_stage_times;
 
 /* ---- lifecycle --------------------------------------------------------------------- */
@@ -232,6 +233,30 @@ int fmm_upward_finish(fmm_ctx* ctx, const double* d_recv);
 /* Run subsequent stages on `stream` (a cudaStream_t; NULL restores the context's own stream),
  * e.g. the stream an NCCL collective is issued on. */
 int fmm_set_stream(fmm_ctx* ctx, void* stream);
+/* ---- the sharded step with its NCCL exchange inside the library ----------------------
+ * Bootstrap like NCCL itself: rank 0 calls fmm_comm_unique_id and ships the 128 bytes to the
+ * other ranks (MPI_Bcast, torch.distributed, a file, ...); every rank then calls
+ * fmm_comm_init(ctx, id, rank, world) (= ncclCommInitRank + fmm_set_partition). A step is
+ *   fmm_set_bodies / fmm_set_bodies_shard;  fmm_evaluate_sharded(ctx, &info);
+ * which runs build, traversal (cost plan on the first step, Morton-filtered targets later), the
+ * own cells' P2M/M2M, one ncclAllGather of the owned multipoles (on a second stream, under the
+ * P2P kernel), the shared ancestors, M2L, P2P and L2L/L2P of the own leaves. Afterwards the
+ * tree-order body range [info.body_begin, info.body_end) is final on this rank:
+ * fmm_get_owned_results copies it (and its input-order indices) to the host. NCCL is loaded at
+ * run time (libnccl.so.2); FMM_ERR_UNSUPPORTED without it. world = 1 runs fmm_evaluate. */
+#define FMM_COMM_ID_BYTES 128
+int fmm_comm_unique_id(void* id);
+int fmm_comm_init(fmm_ctx* ctx, const void* id, int rank, int world);
+int fmm_comm_destroy(fmm_ctx* ctx);
+/* Bodies of all ranks from each rank's share: rank r passes bodies [r*chunk, min(n_total,
+ * (r+1)*chunk)) of the input order, chunk = ceil(n_total / world); the shares are all-gathered
+ * over NVLink into the full input array (one H2D of the share per rank). */
+int fmm_set_bodies_shard(fmm_ctx* ctx, const double* xyzq_share, int64_t n_share, int64_t n_total);
+int fmm_evaluate_sharded(fmm_ctx* ctx, fmm_shard_info* info);
+/* Results of the own tree-order range (info.body_begin..body_end) to host buffers of
+ * body_end - body_begin entries; input_index (optional) = their input-order indices. */
+int fmm_get_owned_results(fmm_ctx* ctx, double* phi, double* acc, int64_t* input_index);
+
 /* Host-only (no GPU): the partition plan the traversal uses. cell_cost holds each leaf's cost
  * (ignored for non-leaves). bounds[world+1] (body indices), owner[ncells] (rank or -1). */
 int fmm_plan_partition(int64_t ncells, const int32_t* body_begin, const int32_t* body_end,

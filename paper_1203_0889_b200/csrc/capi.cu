@@ -44,7 +44,8 @@ void require_device() {
 }
 
 enum { EV_BUILD0 = 0, EV_BUILD1, EV_TRAV1, EV_UP1, EV_M2L1, EV_P2P1, EV_DOWN1, EV_P2PK0, EV_P2PK1, EV_M2LK0,
-       EV_M2LK1, EV_FORK, EV_COUNT };
+       EV_M2LK1, EV_FORK, EV_XCH0, EV_XCH1, EV_COUNT };
+static_assert(EV_COUNT <= 16, "fmm_ctx::ev holds 16 events");
 
 float ms_between(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
@@ -134,6 +135,10 @@ void fmm_destroy(fmm_ctx* ctx) {
   if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
   if (ctx->stream3) cudaStreamDestroy(ctx->stream3);
   if (ctx->hpin) cudaFreeHost(ctx->hpin);
+  try {
+    fmmb::comm_destroy(ctx);
+  } catch (...) {
+  }
   delete ctx;
 }
 
@@ -325,6 +330,7 @@ void evaluate_impl(fmm_ctx* c, bool reuse) {
     t.p2p_launches = 1;
     t.m2l_launches = 1;
     t.kernel_launches = c->kernel_launches;
+    t.exchange_ms = 0.f;
   }
 }
 
@@ -792,6 +798,142 @@ int fmm_set_stream(fmm_ctx* c, void* stream) {
     if (!c->own_stream) c->own_stream = c->stream;
     c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
     c->pstream = c->stream;
+  });
+}
+
+// ------------------------------------------------------- sharded step with NCCL (comm.cu) ----
+int fmm_comm_unique_id(void* id) {
+  if (!id) return FMM_ERR_ARG;
+  return guard(nullptr, [&] { fmmb::comm_unique_id(id); });
+}
+
+int fmm_comm_init(fmm_ctx* c, const void* id, int rank, int world) {
+  if (!c || !id) return FMM_ERR_ARG;
+  const int rc = fmm_set_partition(c, rank, world);
+  if (rc) return rc;
+  return guard(c, [&] {
+    set_device(c);
+    fmmb::comm_init(c, id, rank, world);
+  });
+}
+
+int fmm_comm_destroy(fmm_ctx* c) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] { fmmb::comm_destroy(c); });
+}
+
+int fmm_set_bodies_shard(fmm_ctx* c, const double* share, int64_t n_share, int64_t n_total) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (n_total <= 0) fail(FMM_ERR_EMPTY_INPUT, "empty input");
+    if (!c->nccl_comm) fail(FMM_ERR_STATE, "set_bodies_shard: no communicator (fmm_comm_init)");
+    const int world = c->comm_world, rank = c->comm_rank;
+    const int64_t chunk = (n_total + world - 1) / world;
+    const int64_t b0 = std::min<int64_t>(n_total, rank * chunk), b1 = std::min<int64_t>(n_total, b0 + chunk);
+    if (n_share != b1 - b0) fail(FMM_ERR_ARG, "set_bodies_shard: share size != this rank's chunk");
+    if (n_share > 0 && !share) fail(FMM_ERR_ARG, "null bodies");
+    set_device(c);
+    double4* stage = c->body_share.ensure(chunk);
+    if (n_share < chunk) CK(cudaMemsetAsync(stage + n_share, 0, (chunk - n_share) * sizeof(double4), c->stream));
+    if (n_share > 0)
+      CK(cudaMemcpyAsync(stage, share, n_share * sizeof(double4), cudaMemcpyHostToDevice, c->stream));
+    double4* all = c->xyzq_in.ensure(chunk * world);
+    fmmb::comm_all_gather(c, reinterpret_cast<const double*>(stage), reinterpret_cast<double*>(all), 4 * chunk,
+                          c->stream);
+    c->N = n_total;
+    c->kernel_launches = 0;
+    c->have_bodies = true;
+    c->have_tree = c->have_lists = c->have_M = c->have_L = c->have_out = false;
+  });
+}
+
+int fmm_evaluate_sharded(fmm_ctx* c, fmm_shard_info* info) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_bodies) fail(FMM_ERR_STATE, "evaluate_sharded: no bodies");
+    set_device(c);
+    c->kernel_launches = 0;
+    if (c->world == 1) {
+      evaluate_impl(c, false);
+      c->times.exchange_ms = 0.f;
+    } else {
+      if (!c->nccl_comm || c->comm_world != c->world)
+        fail(FMM_ERR_STATE, "evaluate_sharded: no communicator for this partition (fmm_comm_init)");
+      cudaStream_t s = c->stream, x = c->stream2;
+      CK(cudaEventRecord(c->ev[EV_BUILD0], s));
+      fmmb::build_tree(c);
+      CK(cudaEventRecord(c->ev[EV_BUILD1], s));
+      fmmb::traverse(c);  // lists, partition, own leaves, P2P work list
+      CK(cudaEventRecord(c->ev[EV_TRAV1], s));
+      // exchange stream: own cells' multipoles -> all-gather -> shared ancestors
+      const int64_t chunk = std::max<int64_t>(c->chunk_cells * c->ncoef, 1);
+      double* send = c->shard_send.ensure(chunk);
+      double* recv = c->shard_recv.ensure(chunk * c->world);
+      CK(cudaStreamWaitEvent(x, c->ev[EV_TRAV1], 0));
+      CK(cudaMemsetAsync(c->M.ensure((size_t)c->ncells * c->ncoef), 0, sizeof(double) * c->ncells * c->ncoef, x));
+      fmmb::run_upward(c, x, 1);
+      fmmb::shard_pack(c, send, x);
+      CK(cudaEventRecord(c->ev[EV_XCH0], x));
+      fmmb::comm_all_gather(c, send, recv, chunk, x);
+      CK(cudaEventRecord(c->ev[EV_XCH1], x));
+      fmmb::shard_unpack(c, recv, x);
+      fmmb::run_upward(c, x, 2);
+      CK(cudaEventRecord(c->ev[EV_UP1], x));
+      // FMM stream: P2P of the own leaves (needs no multipole) under the exchange
+      CK(cudaEventRecord(c->ev[EV_FORK], s));
+      do_p2p(c, s);
+      CK(cudaEventRecord(c->ev[EV_P2P1], s));
+      CK(cudaStreamWaitEvent(s, c->ev[EV_UP1], 0));
+      do_m2l(c, s);
+      CK(cudaEventRecord(c->ev[EV_M2L1], s));
+      c->have_L = true;
+      fmmb::run_downward(c, s, 3);
+      CK(cudaEventRecord(c->ev[EV_DOWN1], s));
+      CK(cudaStreamSynchronize(s));
+      fmm_stage_times& t = c->times;
+      t.build_ms = ms_between(c->ev[EV_BUILD0], c->ev[EV_BUILD1]);
+      t.traverse_ms = ms_between(c->ev[EV_BUILD1], c->ev[EV_TRAV1]);
+      t.upward_ms = ms_between(c->ev[EV_TRAV1], c->ev[EV_UP1]);  // includes the exchange
+      t.p2p_ms = ms_between(c->ev[EV_FORK], c->ev[EV_P2P1]);
+      t.m2l_ms = ms_between(c->ev[EV_P2P1], c->ev[EV_M2L1]);     // includes any wait for the exchange
+      t.downward_ms = ms_between(c->ev[EV_M2L1], c->ev[EV_DOWN1]);
+      t.total_ms = ms_between(c->ev[EV_BUILD0], c->ev[EV_DOWN1]);
+      t.p2p_kernel_ms = ms_between(c->ev[EV_P2PK0], c->ev[EV_P2PK1]);
+      t.m2l_kernel_ms = ms_between(c->ev[EV_M2LK0], c->ev[EV_M2LK1]);
+      t.exchange_ms = ms_between(c->ev[EV_XCH0], c->ev[EV_XCH1]);
+      t.p2p_launches = 1;
+      t.m2l_launches = 1;
+      t.kernel_launches = c->kernel_launches;
+    }
+    if (info) {
+      info->rank = c->rank;
+      info->world = c->world;
+      info->body_begin = c->shard_b0;
+      info->body_end = c->shard_b1;
+      info->own_leaves = c->nwl;
+      info->own_cells = c->world > 1 ? c->rank_cells_off[c->rank + 1] - c->rank_cells_off[c->rank] : c->ncells;
+      info->chunk_doubles = c->world > 1 ? c->chunk_cells * c->ncoef : 0;
+    }
+  });
+}
+
+int fmm_get_owned_results(fmm_ctx* c, double* phi, double* acc, int64_t* input_index) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (!c->have_out) fail(FMM_ERR_STATE, "get_owned_results: no results");
+    if (acc && !c->cfg.with_acc) fail(FMM_ERR_STATE, "acceleration was not requested (with_acc = 0)");
+    set_device(c);
+    const int64_t b0 = c->shard_b0, n = c->shard_b1 - c->shard_b0;
+    if (n <= 0) return;
+    if (phi) CK(cudaMemcpyAsync(phi, c->phi.p + b0, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (acc) CK(cudaMemcpyAsync(acc, c->acc.p + 3 * b0, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    std::vector<int32_t> idx;
+    if (input_index) {
+      idx.resize(n);
+      CK(cudaMemcpyAsync(idx.data(), c->perm.p + b0, n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < static_cast<int64_t>(idx.size()); ++i) input_index[i] = idx[i];
   });
 }
 

@@ -135,6 +135,11 @@ struct fmm_ctx {
   fmmb::DBuf<uint64_t> body_keys;          // sorted 63-bit body keys (tree order), sharded runs
   bool body_keys_valid = false;
   fmmb::DBuf<int64_t> shard_bounds;        // device copy of the world + 1 body bounds
+  // NCCL (comm.cu): the communicator of fmm_comm_init and the exchange buffers of the step
+  void* nccl_comm = nullptr;               // ncclComm_t
+  int comm_rank = 0, comm_world = 0;
+  fmmb::DBuf<double> shard_send, shard_recv;
+  fmmb::DBuf<double4> body_share;          // fmm_set_bodies_shard staging (one chunk)
   int64_t trav_b0 = 0, trav_b1 = 0;        // traversal target filter [b0, b1)
 
   // fmm_evaluate: 1 = upward pass on stream2 concurrently with the traversal; 2 = also M2L and
@@ -163,6 +168,12 @@ void traverse(fmm_ctx* c);
 void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p);  // lists from c->m2l_keys/p2p_keys
 void lists_from_pairs(fmm_ctx* c, const int2* d_m2l, int64_t n_m2l, const int2* d_p2p,
                       int64_t n_p2p);
+// comm.cu (NCCL bound at run time)
+void comm_unique_id(void* out128);
+int comm_version();
+void comm_init(fmm_ctx* c, const void* id128, int rank, int world);
+void comm_destroy(fmm_ctx* c);
+void comm_all_gather(fmm_ctx* c, const double* send, double* recv, size_t count, cudaStream_t s);
 // shard.cu
 void plan_shards(fmm_ctx* c);      // after the lists: partition, own leaves, owners
 bool shard_bounds_from_plan(fmm_ctx* c);  // before the traversal: bounds from the kept plan
