@@ -525,8 +525,10 @@ def run_single(args, fb, torch, local):
     roofline_m2l = {"bound": "fp64", "achieved": m2l_tf, "peak": fp64_peak, "unit": "TFLOP/s",
                     "frac": m2l_tf / fp64_peak, "kernel": m2l_kname, "flops_per_unit": m2l_fpp,
                     "unit_of_work": "M2L cell pair", "kernel_ms": m2l_kernel,
-                    "hbm_gbs_algorithmic": m2l_bytes / (m2l_kernel * 1e-3) / 1e9,
-                    "hbm_peak_gbs": float(peaks.get("hbm_gbs", 6446.6)),
+                    "source_bytes_per_s_algorithmic": m2l_bytes / (m2l_kernel * 1e-3),
+                    "bytes_note": "8 n_coef bytes per pair (source row) + per cell (local row); the "
+                                  "multipoles of C1-C3 (<= 29 MB) are L2-resident, so this rate is "
+                                  "served by L2, not HBM; HBM peak %.0f GB/s" % float(peaks.get("hbm_gbs", 6446.6)),
                     "peak_source": f"derived: {sms} SMs x 64 FP64 lanes x 2 x {sm_max:.0f} MHz (DFMA "
                                    "microbenchmark 60 lane-ops/clk/SM, profiles/r1_microbench_pipes.txt)"}
 
