@@ -275,52 +275,47 @@ def run_reference(args, cfg_name):
 
 
 def run_sharded(args, fb, torch, world, rank, local):
-    """torchrun, one rank per GPU: weak scaling, N = 2^20 * world bodies of the config's
-    distribution held by every rank; target leaves sharded by cost-balanced Morton range; the
-    owned multipoles all-gathered with NCCL over NVLink (the step's only data-path exchange)."""
+    """torchrun, one rank per GPU. The step is the library's fmm_evaluate_sharded: every rank
+    builds the (bit-identical) tree, traverses its targets, computes its own cells' multipoles and
+    all-gathers them with the library's own NCCL communicator (fmm_comm_init; the exchange runs
+    under the P2P kernel), then M2L / P2P / L2L / L2P for its Morton range of target leaves.
+    torch.distributed only bootstraps: it ships the NCCL unique id and takes max-over-ranks.
+    Strong scaling (default): N fixed at the config's N at every world size."""
     import torch.distributed as dist
+    os.environ.setdefault("NCCL_DEBUG", "INFO")  # the driver checks the communicator's rank count
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    gen, n1, p, n_crit, theta = CONFIGS[args.config]
-    n = n1 * world
+    gen, n_cfg, p, n_crit, theta = CONFIGS[args.config]
+    strong = args.scaling == "strong"
+    n = n_cfg if strong else n_cfg * world
     bodies = fb.generate_bodies(gen, n, 1)
     ctx = fb.Context(order=p, n_crit=n_crit, theta=theta, precision=args.precision, device=local, with_acc=True)
-    stream = torch.cuda.current_stream()
-    ctx.set_stream(stream.cuda_stream)  # NCCL and the FMM kernels share one stream
+    uid = [fb.fmm.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    ctx.comm_init(uid[0], rank, world)
     d_bodies = torch.from_numpy(bodies).cuda()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-
-    class Buf:
-        def __init__(self, k):
-            self.t = torch.empty(int(k), dtype=torch.float64, device="cuda")
-            self.ptr = self.t.data_ptr()
-
-    def all_gather(recv, send):
-        dist.all_gather_into_tensor(recv.t, send.t)
-
-    def step():
-        ctx.set_bodies_device(d_bodies.data_ptr(), n)
-        return fb.fmm.sharded_step(ctx, rank, world, all_gather, Buf)
-
+    ctx.set_bodies_device(d_bodies.data_ptr(), n)
+    n_m2l_problem = None
     for w in range(args.warmup):
-        step()
-        if w == 0:  # the first step traverses in full (and plans): the problem's unique M2L pairs
+        ctx.evaluate_sharded()
+        if w == 0:  # the first step traverses in full (and plans): the problem's M2L pairs
             n_m2l_problem = int(ctx.tree_info().n_m2l)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    times = []
-    launches = 0
+    times, launches, stage_acc = [], 0, {}
+    keys = ("build_ms", "traverse_ms", "upward_ms", "m2l_ms", "p2p_ms", "downward_ms", "exchange_ms",
+            "p2p_kernel_ms", "m2l_kernel_ms")
     dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
-            e0.record(stream)
-            info = step()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-            launches += ctx.stage_times().kernel_launches
+            info = ctx.evaluate_sharded()
+            t = ctx.stage_times()
+            times.append(t.total_ms)
+            launches += t.kernel_launches
+            for k in keys:
+                stage_acc[k] = stage_acc.get(k, 0.0) + getattr(t, k)
     torch.cuda.synchronize()
     dist.barrier()
     total = torch.tensor([float(np.sum(times))], device="cuda")
@@ -329,64 +324,67 @@ def run_sharded(args, fb, torch, world, rank, local):
     tinfo = ctx.tree_info()
     own_p2p = torch.tensor([float(tinfo.p2p_body_pairs)], device="cuda", dtype=torch.float64)
     dist.all_reduce(own_p2p)
-    inter = int(own_p2p.item()) + n_m2l_problem  # M2L pairs of shared targets counted once
+    p2p_total = int(own_p2p.item())
+    inter = p2p_total + n_m2l_problem  # M2L pairs of shared targets counted once
+    mine = {"rank": rank, "body_range": [int(info.body_begin), int(info.body_end)],
+            "own_leaves": int(info.own_leaves), "own_cells": int(info.own_cells),
+            "p2p_body_pairs": int(tinfo.p2p_body_pairs), "n_m2l_rank": int(tinfo.n_m2l),
+            "stage_ms": {k: v / args.steps for k, v in stage_acc.items()}}
+    per_rank = [None] * world
+    dist.all_gather_object(per_rank, mine)
 
-    # e2e through the public API, per rank and step: H2D of this rank's 1/world share of the
-    # bodies from pinned memory, NCCL all-gather of the shares over NVLink (every rank builds the
-    # full tree), the sharded step, and D2H of the results this rank owns (its contiguous
-    # tree-order body range, read from the context's result buffers); max over ranks
     e2e = None
     if not args.no_e2e:
-        chunk = n // world  # n = 2^20 * world
-        h_in = torch.from_numpy(np.ascontiguousarray(bodies[rank * chunk:(rank + 1) * chunk])).pin_memory()
-        d_part = torch.empty_like(h_in, device="cuda")
-        h_phi = torch.empty(n, dtype=torch.float64).pin_memory()  # own range <= n
-        h_acc = torch.empty((n, 3), dtype=torch.float64).pin_memory()
-
-        class _Dev:  # zero-copy torch view of a context result buffer
-            def __init__(self, ptr, shape):
-                self.__cuda_array_interface__ = {"shape": shape, "typestr": "<f8", "data": (ptr, False),
-                                                 "version": 3, "strides": None}
-
-        ts = []
+        # through the library per rank and step: H2D of the rank's 1/world share from pinned
+        # memory + NCCL all-gather of the shares (fmm_set_bodies_shard), the sharded step, D2H of
+        # the own results and their input indices (fmm_get_owned_results); max over ranks
+        chunk = (n + world - 1) // world
+        b0, b1 = min(n, rank * chunk), min(n, (rank + 1) * chunk)
+        h_in = torch.from_numpy(np.ascontiguousarray(bodies[b0:b1])).pin_memory()
+        ts, nres = [], 0
         dist.barrier()
         torch.cuda.synchronize()
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            d_part.copy_(h_in, non_blocking=True)
-            dist.all_gather_into_tensor(d_bodies, d_part)
-            sinfo = step()
-            b0, b1 = int(sinfo.body_begin), int(sinfo.body_end)
-            pphi, pacc = ctx.results_device()
-            d_phi = torch.as_tensor(_Dev(pphi, (n,)), device="cuda")
-            d_acc = torch.as_tensor(_Dev(pacc, (n, 3)), device="cuda")
-            h_phi[:b1 - b0].copy_(d_phi[b0:b1], non_blocking=True)
-            h_acc[:b1 - b0].copy_(d_acc[b0:b1], non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+            ctx.set_bodies_shard_ptr(h_in.data_ptr(), b1 - b0, n)
+            sinfo = ctx.evaluate_sharded()
+            phi, acc, idx = ctx.owned_results(sinfo)
             ts.append(time.perf_counter() - t0)
-        assert np.isfinite(h_phi[:b1 - b0].numpy()).all()
+            nres = len(phi)
+        assert np.isfinite(phi).all()
         e2e_ms = torch.tensor([float(np.mean(ts)) * 1e3], device="cuda")
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": inter / (e2e_ms.item() * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms.item(),
-               "h2d_bytes_per_step": int(chunk * 32), "d2h_bytes_per_step": int((b1 - b0) * 32),
-               "per": "rank 0 (each rank copies its own share; bodies all-gathered over NVLink: "
-                      f"{int(n * 32)} bytes per rank)"}
+               "h2d_bytes_per_step": int((b1 - b0) * 32), "d2h_bytes_per_step": int(nres * (32 + 8)),
+               "path": "fmm_set_bodies_shard (H2D share + NCCL all-gather) + fmm_evaluate_sharded + "
+                       "fmm_get_owned_results", "per": "rank 0's copies; time = max over ranks"}
     if rank == 0:
+        peaks = load_peaks()
+        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        fp32 = args.precision == "fp32"
+        peak = sms * (128 if fp32 else 64) * 2 * sm_max * 1e6 / 1e12
+        worst_p2p = max(r["stage_ms"]["p2p_kernel_ms"] for r in per_rank)
+        achieved = FLOPS_PER_PAIR * p2p_total / (worst_p2p * 1e-3) / 1e12 / world
         line = {"metric": METRIC, "value": inter / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None,
-                "dtype": "f32 P2P / f64 expansions" if args.precision == "fp32" else "f64",
-                "data": "synthetic (BASELINE generator, seed 1)",
-                "config": {"workload": f"{args.config} distribution, N={n} (2^20 per GPU), p={p}, n_crit={n_crit}, "
-                                       f"theta={theta}, potential+acceleration",
-                           "n_bodies": n, "order": p, "n_crit": n_crit, "theta": theta, "precision": args.precision,
-                           "parallelism": f"dp{world}: target leaves sharded by cost-balanced Morton range, "
-                                          "NCCL all-gather of owned multipoles",
-                           "l2": "flushed (256 MB write) between steps"},
-                "interactions_per_step": inter, "e2e": e2e, "cpu_baseline": None, "clocks": clk.summary(),
-                "gpu_launches": launches, "own_body_range_rank0": [int(info.body_begin), int(info.body_end)]}
+                "scaling": "strong" if strong else "weak", "vs_baseline": None,
+                "dtype": "f32 P2P / f64 expansions" if fp32 else "f64",
+                "data": "synthetic (BASELINE generator: reference xorshift64*, seed 1)",
+                "config": workload_config(args.config, n, world, strong), "precision": args.precision,
+                "interactions_per_step": inter, "p2p_body_pairs": p2p_total, "m2l_pairs": n_m2l_problem,
+                "roofline": {"bound": "fp32" if fp32 else "fp64", "achieved": achieved, "peak": peak,
+                             "unit": "TFLOP/s per GPU", "frac": achieved / peak, "traffic": None,
+                             "kernel": "k_p2p_fp32_ws" if fp32 else "k_p2p_fp64", "flops_per_unit": FLOPS_PER_PAIR,
+                             "timing": "all ranks' P2P pairs x 20 flops / the slowest rank's P2P kernel "
+                                       "(CUDA events, in the step) / world"},
+                "per_rank": per_rank, "e2e": e2e,
+                "cpu_baseline": None, "cpu_baseline_note": "the CPU baseline is timed at N=1 only (rank 0)",
+                "clocks": clk.summary(), "gpu_launches": launches,
+                "nccl": {"comm": "library-owned (fmm_comm_init, NCCL loaded at run time)",
+                         "collective": "ncclAllGather of owned multipoles, one per step"}}
         print(json.dumps(line))
     ctx.close()
     dist.destroy_process_group()
@@ -403,6 +401,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C2", choices=list(CONFIGS))
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="multi-GPU: strong = the config's N at every world size; weak = N x world")
     ap.add_argument("--ref-n", type=int, default=0,
                     help="CPU reference N (default: the config's N up to 2^20; C4/C5 sample 2^20)")
     ap.add_argument("--no-single-core", action="store_true",

@@ -182,8 +182,11 @@ int fmm_load_multipoles(fmm_ctx* ctx, const double* multipole); /* ncells x n_co
 int fmm_reset_accumulators(fmm_ctx* ctx);
 
 /* ---- single-operator entry points (kernels.hpp:69-103), batched, host buffers --------
- * Each runs the same device code as the tree stages, over `count` independent instances;
- * outputs ACCUMULATE (+=) like the reference operators. Coefficient vectors are n_coef(p)
+ * Thread-per-instance kernels (csrc/ops.cu, k_op / k_op_p2p) over `count` independent
+ * instances: the same coefficient order, compile-time term tables and derivative recurrence
+ * (expansions.cuh) as the stage kernels, but NOT the stage kernels themselves (those are checked
+ * by the stage-isolated tests: injected tree / lists / multipoles, tests/test_gpu_parity.py).
+ * Outputs ACCUMULATE (+=) like the reference operators. Coefficient vectors are n_coef(p)
  * doubles each, contiguous per instance. Return FMM_ERR_SINGULAR_* like the reference. */
 int fmm_op_p2m(int order, int64_t count, const int32_t* body_offsets /*count+1*/,
                const double* xyzq, const double* centers3, double* M);

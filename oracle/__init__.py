@@ -202,6 +202,8 @@ class Oracle:
         L.orc_n_coef.restype = C.c_int64
         L.orc_n_coef.argtypes = [C.c_int64]
         L.orc_index_of.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.orc_apply_lists.argtypes = [C.POINTER(_Tree), C.c_void_p, C.c_int64, _i32p, C.c_int64, _i32p,
+                                      C.c_int, _u64p]
         L.orc_evaluate_par.argtypes = [C.POINTER(_Tree), C.c_double, C.c_int, C.c_void_p, _u64p,
                                        _i64p, _i64p]
         L.orc_group_by_target.argtypes = [C.c_int64, C.c_int64, _i32p, _i64p, _i32p, C.c_int]
@@ -258,6 +260,20 @@ class Oracle:
         if rc:
             raise OracleError(ERRORS.get(rc, str(rc)))
         return ev.value, nm.value, npp.value
+
+    def apply_lists(self, tree: OracleTree, m2l: np.ndarray, p2p: np.ndarray, mutual: bool = False):
+        """KernelVisitor over given lists (traversal.hpp:138-164): M2L into the locals, P2P (+ acc)
+        into the body accumulators, in list order; no upward / downward pass. Returns evals."""
+        m2l = np.ascontiguousarray(m2l, dtype=np.int32).reshape(-1, 2)
+        p2p = np.ascontiguousarray(p2p, dtype=np.int32).reshape(-1, 2)
+        ops = OracleOps(self, tree.order)
+        ev = C.c_uint64()
+        rc = self.lib.orc_apply_lists(C.byref(tree._t), C.cast(C.byref(ops.kt), C.c_void_p), len(m2l),
+                                      _ptr(m2l, _i32p), len(p2p), _ptr(p2p, _i32p), int(mutual), C.byref(ev))
+        del ops
+        if rc:
+            raise OracleError(ERRORS.get(rc, str(rc)))
+        return ev.value
 
     def group_by_target(self, ncells: int, pairs: np.ndarray, sort_sources: bool = True):
         """(offsets[ncells+1], sources): CSR by target; sources ascending per target when

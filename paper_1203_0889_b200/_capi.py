@@ -60,7 +60,8 @@ class StageTimes(C.Structure):
                 ("m2l_ms", C.c_float), ("p2p_ms", C.c_float), ("downward_ms", C.c_float),
                 ("total_ms", C.c_float), ("p2p_kernel_ms", C.c_float),
                 ("m2l_kernel_ms", C.c_float), ("p2p_launches", C.c_int32),
-                ("m2l_launches", C.c_int32), ("kernel_launches", C.c_int32)]
+                ("m2l_launches", C.c_int32), ("kernel_launches", C.c_int32),
+                ("exchange_ms", C.c_float)]
 
 
 class TraceRow(C.Structure):
@@ -134,7 +135,14 @@ SIGNATURES = {
     "fmm_upward_finish": (C.c_int, [_vp, _vp]),
     "fmm_set_stream": (C.c_int, [_vp, _vp]),
     "fmm_plan_partition": (C.c_int, [C.c_int64, _i32p, _i32p, _i32p, _dp, C.c_int, _i64p, _i32p]),
+    "fmm_comm_unique_id": (C.c_int, [_vp]),
+    "fmm_comm_init": (C.c_int, [_vp, _vp, C.c_int, C.c_int]),
+    "fmm_comm_destroy": (C.c_int, [_vp]),
+    "fmm_set_bodies_shard": (C.c_int, [_vp, _dp, C.c_int64, C.c_int64]),
+    "fmm_evaluate_sharded": (C.c_int, [_vp, C.POINTER(ShardInfo)]),
+    "fmm_get_owned_results": (C.c_int, [_vp, _dp, _dp, _i64p]),
 }
+COMM_ID_BYTES = 128
 
 _lib = None
 

@@ -257,6 +257,38 @@ class Context:
         self._c(self.lib.fmm_get_expansions(self.h, _ptr(M, _dp), _ptr(L, _dp)))
         return M, L
 
+    # sharding with the NCCL exchange inside the library (comm.cu, fmm_b200.h)
+    def comm_init(self, uid: bytes, rank: int, world: int) -> None:
+        buf = C.create_string_buffer(bytes(uid), _capi.COMM_ID_BYTES)
+        self._c(self.lib.fmm_comm_init(self.h, buf, rank, world))
+
+    def comm_destroy(self) -> None:
+        self._c(self.lib.fmm_comm_destroy(self.h))
+
+    def set_bodies_shard(self, share: np.ndarray, n_total: int) -> None:
+        share = np.ascontiguousarray(share, dtype=np.float64).reshape(-1, 4)
+        self._c(self.lib.fmm_set_bodies_shard(self.h, _ptr(share, _dp), len(share), int(n_total)))
+        self.n = int(n_total)
+
+    def set_bodies_shard_ptr(self, host_ptr: int, n_share: int, n_total: int) -> None:
+        """Same from a raw host pointer (e.g. pinned memory)."""
+        self._c(self.lib.fmm_set_bodies_shard(self.h, C.cast(host_ptr, _dp), int(n_share), int(n_total)))
+        self.n = int(n_total)
+
+    def evaluate_sharded(self) -> _capi.ShardInfo:
+        info = _capi.ShardInfo()
+        self._c(self.lib.fmm_evaluate_sharded(self.h, C.byref(info)))
+        return info
+
+    def owned_results(self, info: _capi.ShardInfo, with_acc: bool = True):
+        """(phi, acc, input_index) of the own tree-order range [body_begin, body_end)."""
+        k = int(info.body_end - info.body_begin)
+        phi = np.zeros(k)
+        acc = np.zeros((k, 3)) if with_acc else None
+        idx = np.zeros(k, np.int64)
+        self._c(self.lib.fmm_get_owned_results(self.h, _ptr(phi, _dp), _ptr(acc, _dp), _ptr(idx, _i64p)))
+        return phi, acc, idx
+
     # sharding (SURVEY.md §8e)
     def set_partition(self, rank: int, world: int) -> None:
         self._c(self.lib.fmm_set_partition(self.h, rank, world))
@@ -427,6 +459,13 @@ def plan_partition(cells: dict, cell_cost: np.ndarray, world: int):
     _check(_capi.load().fmm_plan_partition(len(bb), _ptr(bb, _i32p), _ptr(be, _i32p), _ptr(cc, _i32p),
                                            _ptr(cost, _dp), world, _ptr(bounds, _i64p), _ptr(owner, _i32p)))
     return bounds, owner
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0; ship the bytes to the other ranks)."""
+    buf = C.create_string_buffer(_capi.COMM_ID_BYTES)
+    _check(_lib().fmm_comm_unique_id(buf))
+    return buf.raw
 
 
 def sharded_step(ctx: "Context", rank: int, world: int, all_gather, alloc):

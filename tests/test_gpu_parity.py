@@ -424,6 +424,29 @@ def test_stage_isolated_m2l_and_p2p(fmmlib, orc):
     assert rel_l2(phi, t.phi()) < 1e-12 and rel_l2(acc, t.acc()) < 1e-12
 
 
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-13), ("fp32", 1e-6)])
+def test_stage_isolated_p2p_kernel(fmmlib, orc, precision, tol):
+    """The production P2P kernels alone (k_p2p_fp64 / k_p2p_fp32_ws) on injected tree and lists
+    against the oracle's P2P (kernels.cpp:181-192 + gradient) applied over the same list: the
+    locals are zero, so the downward pass adds nothing. FP64 mode differs from the reference's
+    arithmetic only by the fused r^2 and a <= 1-ulp rsqrt: agreement to ~1e-15."""
+    bodies = fmmlib.generate_bodies(5, 30000, 8)
+    t = orc.build_tree(bodies, 64, 4)
+    c = t.cells()
+    m, pp = orc.traverse(t, 0.5)
+    orc.apply_lists(t, np.zeros((0, 2), np.int32), pp)
+    ctx = fmmlib.Context(order=4, n_crit=64, theta=0.5, precision=precision)
+    ctx.set_bodies(bodies)
+    ctx.load_tree({k: getattr(c, k) for k in CELL_KEYS}, t.perm())
+    ctx.load_lists(m, pp)
+    ctx.reset_accumulators()
+    ctx.p2p()
+    ctx.downward()
+    phi, acc = ctx.results("tree")
+    e_phi, e_acc = rel_l2(phi, t.phi()), rel_l2(acc, t.acc())
+    assert e_phi < tol and e_acc < tol, (precision, e_phi, e_acc)
+
+
 # ------------------------------------------------------------------ edge cases ---------
 def test_edge_cases(fmmlib, orc):
     fb = fmmlib
