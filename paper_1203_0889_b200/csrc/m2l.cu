@@ -543,7 +543,7 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
     if constexpr (kC1) derivs_reg1<P>(rx, ry, rz, D);
     else derivs_reg<P>(rx, ry, rz, D);
     if constexpr (kBulk) {
-      mbar_wait(&bar, phase);
+      mbar_wait_sleep(&bar, phase);
       phase ^= 1u;
     } else {
       asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -592,11 +592,16 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
 #pragma unroll
         for (int j = 0; j < b1 - b0; ++j) red[lane * C::SB + j] = lam[j];
         __syncwarp();
-        if (lane < b1 - b0) {
-          double sum = 0.0;
-#pragma unroll 8
-          for (int j = 0; j < 32; ++j) sum += red[j * C::SB + lane];
-          accT[decltype(BI)::value] += sum;
+        if (lane < b1 - b0) {  // four interleaved partial sums: a chain of 8 dependent adds, not 32
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            s0 += red[j * C::SB + lane];
+            s1 += red[(j + 1) * C::SB + lane];
+            s2 += red[(j + 2) * C::SB + lane];
+            s3 += red[(j + 3) * C::SB + lane];
+          }
+          accT[decltype(BI)::value] += (s0 + s1) + (s2 + s3);
         }
         __syncwarp();
       } else {
