@@ -224,7 +224,15 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
   using T = MI<P>;
   using H = HM<P>;
   constexpr int N = T::N, NA = H::NA, NG = H::NG, S = m2l_row_stride(NA);
-  constexpr bool kBulk = (NA * 8) % 16 == 0;
+#ifndef FMM_M2L_COOP
+#define FMM_M2L_COOP 1
+#endif
+  // kCoop: the warp stages its 32 source rows cooperatively with 16-B cp.async (lane-strided
+  // pieces of every row). A bulk copy per lane serialises: the bulk-copy instruction takes
+  // uniform operands, so 32 per-lane copies become a 32-step loop of R2UR / ELECT / UBLKCP
+  // (ncu, C2: a quarter of the kernel's instructions).
+  constexpr bool kCoop = FMM_M2L_COOP && (NA % 2) == 0;
+  constexpr bool kBulk = !kCoop && (NA * 8) % 16 == 0;
   // kBulk: the rows of chunk k+1 are copied (TMA) into the other buffer while chunk k computes
   constexpr int kBufs = kBulk && FMM_M2L_DB ? 2 : 1;
   extern __shared__ double smem[];
@@ -248,6 +256,25 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
   // stage the lane's detraced source row of chunk `cbase` into buffer b (async)
   auto stage = [&](int b, int64_t cbase, int32_t s_lane) {
     double* row = sR + (size_t)b * 32 * S + lane * S;
+    if constexpr (kCoop) {
+      constexpr int PC = NA / 2;  // 16-B pieces per row
+      const int nv = l1 - cbase < 32 ? static_cast<int>(l1 - cbase) : 32;
+      double* rows = sR + (size_t)b * 32 * S;
+#pragma unroll 2
+      for (int idx = lane; idx < 32 * PC; idx += 32) {
+        const int r = idx / PC, pc = idx - r * PC;
+        const int32_t sr = __shfl_sync(0xffffffffu, s_lane, r);
+        double* d = rows + r * S + 2 * pc;
+        if (r < nv) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(d)),
+                       "l"(Mt + (int64_t)sr * NA + 2 * pc));
+        } else {
+          *reinterpret_cast<double2*>(d) = make_double2(0.0, 0.0);  // tail rows contribute nothing
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      return;
+    }
     if (cbase + lane >= l1) {
       for (int e = 0; e < NA; ++e) row[e] = 0.0;  // tail lanes contribute nothing
     } else if constexpr (kBulk) {
