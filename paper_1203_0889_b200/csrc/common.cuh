@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
@@ -13,6 +15,55 @@
 #include "fmm_b200.h"
 
 namespace fmmb {
+
+// ------------------------------------------------------------ checked build -----------
+// FMM_CHECKS=1 (tools/checked_build.sh): device-side bounds checks on the index streams the
+// kernels dereference (bodies, cells, list entries, tile offsets). A failed check prints the
+// site and traps, which the host sees as a CUDA error on the next synchronisation. The limits
+// live in this TU's constant bank (each .cu file has its own copy; set_check_limits fills it
+// before the TU's launches). compute-sanitizer is not available on the GPU pool, so this build,
+// run over the whole GPU test suite, is the memory-safety evidence (profiles/r2_checked_build.log).
+#ifndef FMM_CHECKS
+#define FMM_CHECKS 0
+#endif
+struct CheckLimits {
+  int64_t nbodies, ncells, n_m2l, n_p2p;
+};
+#if FMM_CHECKS
+static __constant__ CheckLimits g_lim;
+#define FMM_CHECK(cond, what)                                                                            \
+  do {                                                                                                 \
+    if (!(cond)) {                                                                                     \
+      printf("FMM_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, blockIdx.x, \
+             threadIdx.x);                                                                             \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#define FMM_LIM(field) (::fmmb::g_lim.field)
+// the constant bank is per process (shared by every context of this TU): it holds the maximum
+// over the contexts seen so far, so concurrent contexts (sharded ranks on host threads) never see
+// each other's smaller limits; the checks still catch any index past every live array
+// static (internal linkage): each TU's copy updates that TU's own g_lim (an inline function would
+// be merged across TUs by the linker and update only one of them)
+template <class Ctx>
+static void set_check_limits(const Ctx* c, cudaStream_t s) {
+  static std::mutex mu;
+  static CheckLimits cur{0, 0, 0, 0};
+  std::lock_guard<std::mutex> lock(mu);
+  const CheckLimits l{c->N > cur.nbodies ? c->N : cur.nbodies, c->ncells > cur.ncells ? c->ncells : cur.ncells,
+                      c->n_m2l > cur.n_m2l ? c->n_m2l : cur.n_m2l, c->n_p2p > cur.n_p2p ? c->n_p2p : cur.n_p2p};
+  if (l.nbodies == cur.nbodies && l.ncells == cur.ncells && l.n_m2l == cur.n_m2l && l.n_p2p == cur.n_p2p) return;
+  cur = l;
+  cudaMemcpyToSymbolAsync(g_lim, &cur, sizeof(cur), 0, cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+}
+#else
+#define FMM_CHECK(cond, what) \
+  do {                        \
+  } while (0)
+template <class Ctx>
+static inline void set_check_limits(const Ctx*, cudaStream_t) {}
+#endif
 
 // ---------------------------------------------------------------- errors --------------
 struct Error : std::runtime_error {

@@ -39,8 +39,10 @@ k_p2m(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __rest
   const int64_t wid = blockIdx.x * 4ll + w;
   if (wid >= nleaves) return;
   const int32_t leaf = leaves[wid];
+  FMM_CHECK(leaf >= 0 && leaf < FMM_LIM(ncells), "k_p2m: leaf index");
   const double4 c = cr[leaf];
   const int32_t b0 = bb[leaf], b1 = be[leaf];
+  FMM_CHECK(b0 >= 0 && b0 <= b1 && b1 <= FMM_LIM(nbodies), "k_p2m: body range");
   constexpr int KPL = (N + 31) / 32;  // coefficients per lane
   double acc[KPL];
 #pragma unroll
@@ -397,6 +399,7 @@ struct Downward {
 
 void run_upward(fmm_ctx* c, cudaStream_t s, int mode) {
   if (!c->have_tree) fail(FMM_ERR_STATE, "upward: no tree");
+  set_check_limits(c, s);
   if (mode != 0 && !c->shard_planned) fail(FMM_ERR_STATE, "sharded upward before the partition (run traverse)");
   dispatch_order<Upward>(c->cfg.order, c, s, mode);
   c->have_M = true;
@@ -404,6 +407,7 @@ void run_upward(fmm_ctx* c, cudaStream_t s, int mode) {
 
 void run_downward(fmm_ctx* c, cudaStream_t s, int part) {
   if (!c->have_tree) fail(FMM_ERR_STATE, "downward: no tree");
+  set_check_limits(c, s);
   dispatch_order<Downward>(c->cfg.order, c, s, part);
   if (part & 2) c->have_out = true;
 }

@@ -248,8 +248,10 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
   const int64_t wid = blockIdx.x * (int64_t)kM2LWarps + w;
   if (wid >= ntargets) return;
   const int32_t t = targets[wid];
+  FMM_CHECK(t >= 0 && t < FMM_LIM(ncells), "k_m2l_reg: target index");
   const double4 ct = cr[t];
   const int64_t l0 = off[t], l1 = off[t + 1];
+  FMM_CHECK(l0 >= 0 && l0 <= l1 && l1 <= FMM_LIM(n_m2l), "k_m2l_reg: list range");
   double lam[NA];
 #pragma unroll
   for (int i = 0; i < NA; ++i) lam[i] = 0.0;
@@ -309,6 +311,7 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
       stage(0, base, s_cur);  // hidden behind the Dt recurrence only
     }
     const int32_t s_nn = (base + 64 + lane < l1) ? src[base + 64 + lane] : t;
+    FMM_CHECK(s_cur >= 0 && s_cur < FMM_LIM(ncells), "k_m2l_reg: source index");
     const double4 cs = valid ? cr[s_cur] : ct;
     double rx = 1.0, ry = 0.0, rz = 0.0;
     if (valid) {
@@ -505,8 +508,10 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
   const int64_t wid = blockIdx.x * (int64_t)W + w;
   const bool have = wid < ntargets;
   const int32_t t = have ? targets[wid] : 0;
+  FMM_CHECK(t >= 0 && t < FMM_LIM(ncells), "k_m2l_big2: target index");
   const double4 ct = cr[t];
   const int64_t l0 = have ? off[t] : 0, l1 = have ? off[t + 1] : 0;
+  FMM_CHECK(l0 >= 0 && l0 <= l1 && l1 <= FMM_LIM(n_m2l), "k_m2l_big2: list range");
   if (W > 1 && lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&cta_chunks),
                                     static_cast<unsigned long long>((l1 - l0 + 31) / 32));
   if (W > 1) __syncthreads();
@@ -529,6 +534,7 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
     const int64_t k = base + lane;
     const bool valid = k < l1;
     const int32_t s = s_next;
+    FMM_CHECK(!valid || (s >= 0 && s < FMM_LIM(ncells)), "k_m2l_big2: source index");
     if (!valid) {
       for (int e = 0; e < NA; ++e) myM[e] = 0.0;  // tail lanes contribute nothing
     } else if constexpr (kBulk) {
@@ -723,6 +729,7 @@ struct M2L {
 
 void run_m2l(fmm_ctx* c, cudaStream_t s) {
   if (!c->have_lists) fail(FMM_ERR_STATE, "m2l: no interaction lists");
+  set_check_limits(c, s);
   if (!c->have_M) fail(FMM_ERR_STATE, "m2l: no multipoles (run upward first)");
   dispatch_order<M2L>(c->cfg.order, c, s);
   c->have_L = true;

@@ -54,6 +54,7 @@ __device__ __forceinline__ void tile_setup(int tid, int32_t le, int32_t cursor, 
   int32_t n = 0, s = -1, boff = 0;
   if (k < le) {
     s = src_list[k];
+    FMM_CHECK(s >= 0 && s < FMM_LIM(ncells), "p2p (fp64) tile: source cell index");
     n = be[s] - bb[s];
     if (tid == 0) {
       boff = cur_off;
@@ -137,6 +138,7 @@ __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cur
       const int4 e1 = reinterpret_cast<const int4*>(e)[2 * (h * 32 + lane) + 1];
       b[h] = e0.x;
       n[h] = e0.y & 0x3fffffff;
+      FMM_CHECK(b[h] >= 0 && n[h] > 0 && b[h] + n[h] <= FMM_LIM(nbodies), "p2p tile: entry body range");
       kind[h] = static_cast<int>(static_cast<uint32_t>(e0.y) >> 30);
       sh[h][0] = __int_as_float(e0.z);
       sh[h][1] = __int_as_float(e0.w);
@@ -223,6 +225,8 @@ __device__ __forceinline__ void tile_tma(int lane, const TileTab& tt, const floa
   if (lane == 0) mbar_arrive_expect_tx(bar, static_cast<unsigned>(tt.off[nseg]) * (prec ? 32u : 16u));
   for (int idx = lane; idx < nseg; idx += 32) {
     const int32_t o0 = tt.off[idx];
+    FMM_CHECK(o0 >= 0 && tt.off[idx + 1] > o0 && tt.off[idx + 1] <= (prec ? kHalfTile : kTileBodies),
+              "p2p tile: staged bodies beyond the tile buffer");
     const unsigned bytes = static_cast<unsigned>(tt.off[idx + 1] - o0) * 16u;
     bulk_g2s(buf + o0, bodyf + tt.bb[idx], bytes, bar);
     if (prec) bulk_g2s(buf + kHalfTile + o0, bodyl + tt.bb[idx], bytes, bar);
@@ -466,6 +470,8 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
 
   // ---- consumer warps
   const int nt = it.te - it.tb;
+  FMM_CHECK(it.tb >= 0 && nt >= 1 && nt <= kThreads && it.te <= FMM_LIM(nbodies), "k_p2p_fp32_ws: target range");
+  FMM_CHECK(it.lb >= 0 && it.lb <= it.le && it.le <= FMM_LIM(n_p2p), "k_p2p_fp32_ws: list range");
   const int slots = (nt + 1) >> 1;
   const int G = kThreads / slots;
   const int g = tid / slots, t = tid - g * slots;
@@ -584,6 +590,8 @@ k_p2p_fp64(const P2PItem* __restrict__ items, const int32_t* __restrict__ src_li
   const P2PItem it = items[blockIdx.x];
   const int tid = threadIdx.x;
   const int nt = it.te - it.tb;
+  FMM_CHECK(it.tb >= 0 && nt >= 1 && nt <= kThreads && it.te <= FMM_LIM(nbodies), "k_p2p_fp64: target range");
+  FMM_CHECK(it.lb >= 0 && it.lb <= it.le && it.le <= FMM_LIM(n_p2p), "k_p2p_fp64: list range");
   const int nh = (nt + 1) >> 1;
   const int G = kThreads / nh;
   const int g = tid / nh, t = tid - g * nh;
@@ -875,7 +883,9 @@ __global__ void k_ent_write(const int32_t* __restrict__ tgt, const int32_t* __re
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= ne) return;
   const int32_t t = tgt[k], s = src[k];
+  FMM_CHECK(t >= 0 && t < FMM_LIM(ncells) && s >= 0 && s < FMM_LIM(ncells), "k_ent_write: cell index");
   const int64_t l0 = off[t], l1 = off[t + 1];
+  FMM_CHECK(l0 <= k && k < l1, "k_ent_write: entry outside its target's list");
   const int64_t v = cls[k], P0 = pre[l0], Pk = pre[k];
   const int64_t lo0 = P0 & 0xffffffffll, hi0 = P0 >> 32;
   int64_t pos;
@@ -905,6 +915,7 @@ __global__ void k_ent_write(const int32_t* __restrict__ tgt, const int32_t* __re
   e.lx = static_cast<float>(dx - hx);
   e.ly = static_cast<float>(dy - hy);
   e.lz = static_cast<float>(dz - hz);
+  FMM_CHECK(pos >= l0 && pos < l1, "k_ent_write: entry position");
   ent[pos] = e;
 }
 
@@ -925,6 +936,7 @@ void exclusive_scan_i32(fmm_ctx* c, const int32_t* in, int32_t* out, int64_t n, 
 // through the near test, on the bodies' tight leaf boxes (rebuilt by a tree-reuse step)
 void build_p2p_entries(fmm_ctx* c) {
   cudaStream_t s = c->pstream;
+  set_check_limits(c, s);
   const int64_t ne = c->n_p2p;
   P2PEnt* ent = reinterpret_cast<P2PEnt*>(c->p2p_ent.ensure(2 * (ne + 1)));
   double4* blo = c->leaf_lo.ensure(c->ncells);
@@ -1041,6 +1053,7 @@ void build_p2p_worklist(fmm_ctx* c) {
 
 void run_p2p(fmm_ctx* c, cudaStream_t s) {
   if (!c->have_lists) fail(FMM_ERR_STATE, "p2p: no interaction lists");
+  set_check_limits(c, s);
   if (c->p2p_pending) fail(FMM_ERR_STATE, "p2p: work list not finished");
   const int64_t n = c->N;
   const int wa = c->cfg.with_acc ? 1 : 0;

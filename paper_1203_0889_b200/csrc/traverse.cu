@@ -147,6 +147,8 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
       pr[j] = make_int2(0, 0);
       if (i < n) {
         pr[j] = fr[i];
+        FMM_CHECK(pr[j].x >= 0 && pr[j].x < FMM_LIM(ncells) && pr[j].y >= 0 && pr[j].y < FMM_LIM(ncells),
+                  "k_step: frontier pair outside the cell array");
         classify(pr[j], cr, cc, theta, theta2, mutual, kind[j], nch[j]);
         if (filter && kind[j] == 2) {  // sharded: keep only target children meeting [tb0, tb1)
           const int32_t b = cb[pr[j].x];
@@ -453,6 +455,7 @@ void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
 
 void traverse(fmm_ctx* c) {
   if (!c->have_tree) fail(FMM_ERR_STATE, "traverse: no tree");
+  set_check_limits(c, c->stream);
   const double theta = c->cfg.theta;
   if (!(theta > 0.0 && theta < 1.0)) fail(FMM_ERR_THETA, "theta must be in (0,1)");
   cudaStream_t s = c->stream;

@@ -275,6 +275,8 @@ __global__ void k_gather(const double4* __restrict__ in, const int32_t* __restri
                          float4* __restrict__ bodyl) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  FMM_CHECK(perm[i] >= 0 && perm[i] < n && leaf_of_body[i] >= 0 && leaf_of_body[i] < FMM_LIM(ncells),
+            "k_gather: permutation / leaf index out of range");
   const double4 b = in[perm[i]];
   bodies[i] = b;
   const double4 c = c_cr[leaf_of_body[i]];
@@ -508,6 +510,7 @@ void build_tree(fmm_ctx* c) {
   }
   c->kernel_launches += launches;
   c->have_tree = true;
+  set_check_limits(c, s);
   k_gather<<<ceil_div(n, 256), 256, 0, s>>>(c->xyzq_in.p, perm, leaf_of_body, c->c_cr.p, n, c->bodies.ensure(n),
                                             c->bodyf.ensure(n), c->bodyl.ensure(n));
   CK_LAUNCH("k_gather");
@@ -571,6 +574,7 @@ void gather_bodies(fmm_ctx* c) {
   int32_t* leaf_of_body = c->leaf_of_body.ensure(n);
   k_leaf_map<<<ceil_div(c->nleaves * 32, 256), 256, 0, s>>>(c->leaves.p, c->nleaves, c->c_body_begin.p,
                                                               c->c_body_end.p, nullptr, leaf_of_body, nullptr);
+  set_check_limits(c, s);
   k_gather<<<ceil_div(n, 256), 256, 0, s>>>(c->xyzq_in.p, c->perm.p, leaf_of_body, c->c_cr.p, n,
                                             c->bodies.ensure(n), c->bodyf.ensure(n), c->bodyl.ensure(n));
   CK_LAUNCH("k_gather");
