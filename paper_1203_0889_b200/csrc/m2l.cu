@@ -210,7 +210,7 @@ constexpr int m2l_row_stride(int n) {
 #define FMM_M2L_DB 0  // measured slower at p = 6 (1.07 -> 1.14 ms): register pressure
 #endif
 #ifndef FMM_M2L_MINB
-#define FMM_M2L_MINB 10
+#define FMM_M2L_MINB 12
 #endif
 #ifndef FMM_M2L_WARPS
 #define FMM_M2L_WARPS 1
@@ -232,6 +232,10 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
   // uniform operands, so 32 per-lane copies become a 32-step loop of R2UR / ELECT / UBLKCP
   // (ncu, C2: a quarter of the kernel's instructions).
   constexpr bool kCoop = FMM_M2L_COOP && (NA % 2) == 0;
+#ifndef FMM_M2L_REG_C1
+#define FMM_M2L_REG_C1 1
+#endif
+  constexpr bool kRegC1 = FMM_M2L_REG_C1 != 0;
   constexpr bool kBulk = !kCoop && (NA * 8) % 16 == 0;
   // kBulk: the rows of chunk k+1 are copied (TMA) into the other buffer while chunk k computes
   constexpr int kBufs = kBulk && FMM_M2L_DB ? 2 : 1;
@@ -319,8 +323,11 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
       ry = cs.y - ct.y;
       rz = cs.z - ct.z;
     }
-    double D[NG];
-    derivs_reg<P>(rx, ry, rz, D);
+    // kRegC1: Dt over g_c <= 1 only (NA values instead of NG), the g_c = 2 entries from the trace
+    // identity in the contraction: fewer registers (occupancy) for a few more FMAs
+    double D[kRegC1 ? NA : NG];
+    if constexpr (kRegC1) derivs_reg1<P>(rx, ry, rz, D);
+    else derivs_reg<P>(rx, ry, rz, D);
     if constexpr (kBulk) {
       mbar_wait(&bars[w][b], kBufs == 2 ? ((k >> 1) & 1u) : (k & 1u));
     } else {
@@ -335,8 +342,15 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
         constexpr int kb = decltype(KB)::value;
         constexpr int ib = H::a_full(kb);
         if constexpr (da + T::deg(ib) <= P - 1) {
-          constexpr int ig = H::g_of(index_of(aa + T::ea(ib), ab + T::eb(ib), ac + T::ec(ib)));
-          lam[kb] = fma(m, D[ig], lam[kb]);
+          constexpr int gx = aa + T::ea(ib), gy = ab + T::eb(ib), gz = ac + T::ec(ib);
+          if constexpr (!kRegC1) {
+            lam[kb] = fma(m, D[H::g_of(index_of(gx, gy, gz))], lam[kb]);
+          } else if constexpr (gz <= 1) {
+            lam[kb] = fma(m, D[H::a_of(index_of(gx, gy, gz))], lam[kb]);
+          } else {  // gz == 2: Dt_{x,y,2} = -Dt_{x+2,y,0} - Dt_{x,y+2,0}
+            lam[kb] = fma(-m, D[H::a_of(index_of(gx + 2, gy, 0))], lam[kb]);
+            lam[kb] = fma(-m, D[H::a_of(index_of(gx, gy + 2, 0))], lam[kb]);
+          }
         }
       });
     };
