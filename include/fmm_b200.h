@@ -251,6 +251,15 @@ int fmm_set_stream(fmm_ctx* ctx, void* stream);
 int fmm_comm_unique_id(void* id);
 int fmm_comm_init(fmm_ctx* ctx, const void* id, int rank, int world);
 int fmm_comm_destroy(fmm_ctx* ctx);
+/* Exchange override: a host callback that all-gathers `count` doubles per rank from d_send into
+ * d_recv (rank-major, device pointers) for work queued on `stream` (a cudaStream_t the callback
+ * must synchronise or enqueue on). When set, fmm_set_bodies_shard / fmm_evaluate_sharded use it
+ * instead of NCCL and need no communicator (fmm_set_partition gives rank / world): hosts with
+ * their own transport, and the multi-process test on one GPU (NCCL refuses two ranks on one
+ * device). The callback returns 0 on success. fn = NULL restores NCCL. */
+typedef int (*fmm_allgather_fn)(const double* d_send, double* d_recv, int64_t count, void* stream,
+                                void* user);
+int fmm_set_allgather(fmm_ctx* ctx, fmm_allgather_fn fn, void* user);
 /* Bodies of all ranks from each rank's share: rank r passes bodies [r*chunk, min(n_total,
  * (r+1)*chunk)) of the input order, chunk = ceil(n_total / world); the shares are all-gathered
  * over NVLink into the full input array (one H2D of the share per rank). */

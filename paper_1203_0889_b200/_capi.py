@@ -141,7 +141,10 @@ SIGNATURES = {
     "fmm_set_bodies_shard": (C.c_int, [_vp, _dp, C.c_int64, C.c_int64]),
     "fmm_evaluate_sharded": (C.c_int, [_vp, C.POINTER(ShardInfo)]),
     "fmm_get_owned_results": (C.c_int, [_vp, _dp, _dp, _i64p]),
+    "fmm_set_allgather": (C.c_int, [_vp, _vp, _vp]),
 }
+# fmm_allgather_fn(d_send, d_recv, count, stream, user) -> int
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
 COMM_ID_BYTES = 128
 
 _lib = None

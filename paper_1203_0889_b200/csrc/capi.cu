@@ -822,12 +822,19 @@ int fmm_comm_destroy(fmm_ctx* c) {
   return guard(c, [&] { fmmb::comm_destroy(c); });
 }
 
+int fmm_set_allgather(fmm_ctx* c, fmm_allgather_fn fn, void* user) {
+  if (!c) return FMM_ERR_ARG;
+  c->ag_fn = fn;
+  c->ag_user = user;
+  return FMM_OK;
+}
+
 int fmm_set_bodies_shard(fmm_ctx* c, const double* share, int64_t n_share, int64_t n_total) {
   if (!c) return FMM_ERR_ARG;
   return guard(c, [&] {
     if (n_total <= 0) fail(FMM_ERR_EMPTY_INPUT, "empty input");
-    if (!c->nccl_comm) fail(FMM_ERR_STATE, "set_bodies_shard: no communicator (fmm_comm_init)");
-    const int world = c->comm_world, rank = c->comm_rank;
+    if (!c->nccl_comm && !c->ag_fn) fail(FMM_ERR_STATE, "set_bodies_shard: no communicator (fmm_comm_init)");
+    const int world = c->ag_fn ? c->world : c->comm_world, rank = c->ag_fn ? c->rank : c->comm_rank;
     const int64_t chunk = (n_total + world - 1) / world;
     const int64_t b0 = std::min<int64_t>(n_total, rank * chunk), b1 = std::min<int64_t>(n_total, b0 + chunk);
     if (n_share != b1 - b0) fail(FMM_ERR_ARG, "set_bodies_shard: share size != this rank's chunk");
@@ -857,7 +864,7 @@ int fmm_evaluate_sharded(fmm_ctx* c, fmm_shard_info* info) {
       evaluate_impl(c, false);
       c->times.exchange_ms = 0.f;
     } else {
-      if (!c->nccl_comm || c->comm_world != c->world)
+      if (!c->ag_fn && (!c->nccl_comm || c->comm_world != c->world))
         fail(FMM_ERR_STATE, "evaluate_sharded: no communicator for this partition (fmm_comm_init)");
       cudaStream_t s = c->stream, x = c->stream2;
       CK(cudaEventRecord(c->ev[EV_BUILD0], s));

@@ -101,6 +101,11 @@ void comm_destroy(fmm_ctx* c) {
 }
 
 void comm_all_gather(fmm_ctx* c, const double* send, double* recv, size_t count, cudaStream_t s) {
+  if (c->ag_fn) {
+    if (c->ag_fn(send, recv, static_cast<int64_t>(count), s, c->ag_user) != 0)
+      fail(FMM_ERR_CUDA, "all-gather callback failed");
+    return;
+  }
   if (!c->nccl_comm) fail(FMM_ERR_STATE, "no communicator (fmm_comm_init)");
   nccl_check(nccl().all_gather(send, recv, count, ncclFloat64, static_cast<ncclComm_t>(c->nccl_comm), s),
              "ncclAllGather");

@@ -137,6 +137,8 @@ struct fmm_ctx {
   fmmb::DBuf<int64_t> shard_bounds;        // device copy of the world + 1 body bounds
   // NCCL (comm.cu): the communicator of fmm_comm_init and the exchange buffers of the step
   void* nccl_comm = nullptr;               // ncclComm_t
+  fmm_allgather_fn ag_fn = nullptr;        // exchange override (fmm_set_allgather)
+  void* ag_user = nullptr;
   int comm_rank = 0, comm_world = 0;
   fmmb::DBuf<double> shard_send, shard_recv;
   fmmb::DBuf<double4> body_share;          // fmm_set_bodies_shard staging (one chunk)

@@ -262,6 +262,26 @@ class Context:
         buf = C.create_string_buffer(bytes(uid), _capi.COMM_ID_BYTES)
         self._c(self.lib.fmm_comm_init(self.h, buf, rank, world))
 
+    def set_allgather(self, fn) -> None:
+        """Exchange override: fn(d_send, d_recv, count, stream) all-gathers `count` doubles per
+        rank between device pointers (see fmm_set_allgather); None restores NCCL."""
+        if fn is None:
+            self._ag = None
+            self._c(self.lib.fmm_set_allgather(self.h, None, None))
+            return
+
+        def tramp(d_send, d_recv, count, stream, user):
+            try:
+                fn(int(d_send or 0), int(d_recv or 0), int(count), int(stream or 0))
+                return 0
+            except Exception:  # reported as a CUDA-class error by the library
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._ag = _capi.ALLGATHER_FN(tramp)  # keep the trampoline alive
+        self._c(self.lib.fmm_set_allgather(self.h, C.cast(self._ag, C.c_void_p), None))
+
     def comm_destroy(self) -> None:
         self._c(self.lib.fmm_comm_destroy(self.h))
 
