@@ -194,6 +194,54 @@ __device__ __forceinline__ void derivs_reg1(double rx, double ry, double rz, dou
   });
 }
 
+// Lambda epilogue driven by tables in constant memory: lanes take the coefficients lane,
+// lane + 32, ... with runtime indices, instead of one predicated static branch per coefficient
+// (p = 10: 320 branches per target; ncu C5: ~15 % of the kernel's stall samples were
+// branch_resolving in that epilogue, with ~3 source chunks per target).
+template <int P>
+struct TraceTab {
+  static constexpr int N = n_coef(P), NA = HM<P>::NA;
+  int16_t a_full[NA];      // compact index -> full index
+  int16_t fill[N][3];      // c >= 2 entries in increasing c: target, j1, j2 (full = -full[j1] - full[j2])
+  int16_t cstart[P + 1];   // fill entries of c are [cstart[c], cstart[c + 1])
+  double w[N];             // (-1)^|b| / b!
+};
+template <int P>
+constexpr TraceTab<P> make_trace_tab() {
+  using T = MI<P>;
+  TraceTab<P> t{};
+  for (int k = 0; k < HM<P>::NA; ++k) t.a_full[k] = static_cast<int16_t>(HM<P>::a_full(k));
+  int m = 0;
+  for (int c = 0; c <= P; ++c) {
+    t.cstart[c] = static_cast<int16_t>(m);
+    if (c >= 2 && c < P)
+      for (int i = 0; i < T::N; ++i)
+        if (T::ec(i) == c) {
+          t.fill[m][0] = static_cast<int16_t>(i);
+          t.fill[m][1] = static_cast<int16_t>(index_of(T::ea(i) + 2, T::eb(i), c - 2));
+          t.fill[m][2] = static_cast<int16_t>(index_of(T::ea(i), T::eb(i) + 2, c - 2));
+          ++m;
+        }
+  }
+  for (int i = 0; i < T::N; ++i) t.w[i] = ((T::deg(i) & 1) ? -1.0 : 1.0) / T::fact(i);
+  return t;
+}
+template <int P>
+__constant__ TraceTab<P> g_trace = make_trace_tab<P>();
+
+template <int P>
+__device__ __forceinline__ void trace_fill_store_tab(int lane, const double* cmp, double* full, double* Lt) {
+  const TraceTab<P>& tt = g_trace<P>;
+  for (int k = lane; k < TraceTab<P>::NA; k += 32) full[tt.a_full[k]] = cmp[k];
+  __syncwarp();
+  for (int c = 2; c < P; ++c) {
+    for (int m = tt.cstart[c] + lane; m < tt.cstart[c + 1]; m += 32)
+      full[tt.fill[m][0]] = -full[tt.fill[m][1]] - full[tt.fill[m][2]];
+    __syncwarp();
+  }
+  for (int i = lane; i < TraceTab<P>::N; i += 32) Lt[i] += tt.w[i] * full[i];
+}
+
 // Row stride (doubles) of the staged rows: even (16-B aligned rows) with an odd half, so a
 // quarter-warp's LDS.128 of 8 distinct rows hits 8 distinct bank groups.
 constexpr int m2l_row_stride(int n) {
@@ -225,7 +273,7 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
   using H = HM<P>;
   constexpr int N = T::N, NA = H::NA, NG = H::NG, S = m2l_row_stride(NA);
 #ifndef FMM_M2L_COOP
-#define FMM_M2L_COOP 1
+#define FMM_M2L_COOP 0
 #endif
   // kCoop: the warp stages its 32 source rows cooperatively with 16-B cp.async (lane-strided
   // pieces of every row). A bulk copy per lane serialises: the bulk-copy instruction takes
@@ -375,41 +423,28 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int kk = lane + 32 * r;
-    double acc = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // four chains of 8 dependent adds
     if (kk < NA) {
-#pragma unroll 8
-      for (int j = 0; j < 32; ++j) acc += sR[j * S + kk];
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        a0 += sR[j * S + kk];
+        a1 += sR[(j + 1) * S + kk];
+        a2 += sR[(j + 2) * S + kk];
+        a3 += sR[(j + 3) * S + kk];
+      }
     }
-    red[r] = acc;
+    red[r] = (a0 + a1) + (a2 + a3);
   }
   __syncwarp();
-  // ... place at the full (reference-order) index, fill c >= 2 by the trace identity ...
-  double* full = sR;  // N doubles
-  static_for<NA>([&](auto K) {
-    constexpr int kk = decltype(K)::value;
-    if (lane == kk % 32) full[H::a_full(kk)] = red[kk / 32];
-  });
+  // ... place at the full (reference-order) index, fill c >= 2 by the trace identity, then
+  // L_b += (-1)^{|b|}/b! Lambda_b (table-driven epilogue: trace_fill_store_tab below)
+  double* full = sR;             // N doubles
+  double* cmp = sR + 2 * N + 2;  // NA reduced values (32 * S >= 2N + 2 + NA)
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (lane + 32 * r < NA) cmp[lane + 32 * r] = red[r];
   __syncwarp();
-  static_for<P>([&](auto C) {
-    constexpr int c = decltype(C)::value;
-    if constexpr (c >= 2) {
-      static_for<N>([&](auto I) {
-        constexpr int i = decltype(I)::value;
-        if constexpr (T::ec(i) == c) {
-          constexpr int a = T::ea(i), b = T::eb(i);
-          if (lane == i % 32) full[i] = -full[index_of(a + 2, b, c - 2)] - full[index_of(a, b + 2, c - 2)];
-        }
-      });
-      __syncwarp();
-    }
-  });
-  // ... then L_b += (-1)^{|b|}/b! Lambda_b
-  double* Lt = L + (int64_t)t * N;
-  static_for<N>([&](auto I) {
-    constexpr int i = decltype(I)::value;
-    constexpr double w = ((T::deg(i) & 1) ? -1.0 : 1.0) / T::fact(i);
-    if (lane == i % 32) Lt[i] += w * full[i];
-  });
+  trace_fill_store_tab<P>(lane, cmp, full, L + (int64_t)t * N);
 }
 
 // Lambda (compact, lanes reduced) -> full reference-order Lambda by the trace identity, then
@@ -500,7 +535,10 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
   using H = HM<P>;
   using C = BigCfg2<P>;
   constexpr int N = T::N, NA = C::NA, NG = C::NG, SA = C::SA, SL = C::SL;
-  constexpr bool kBulk = (NA * 8) % 16 == 0;
+  // warp-cooperative 16-B cp.async staging of the 32 source rows (a bulk copy per lane compiles
+  // to a 32-step R2UR / ELECT / UBLKCP loop: ncu C5, ~9 % of the stall samples)
+  constexpr bool kCoop = FMM_M2L_COOP && (NA % 2) == 0;
+  constexpr bool kBulk = !kCoop && (NA * 8) % 16 == 0;
   constexpr int W = C::kWarps;
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t bars[W];
@@ -549,7 +587,22 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
     const bool valid = k < l1;
     const int32_t s = s_next;
     FMM_CHECK(!valid || (s >= 0 && s < FMM_LIM(ncells)), "k_m2l_big2: source index");
-    if (!valid) {
+    if constexpr (kCoop) {  // committed below with the other cp.async paths
+      constexpr int PC = NA / 2;  // 16-B pieces per row
+      const int nv = l1 - base < 32 ? static_cast<int>(l1 - base) : 32;
+#pragma unroll 2
+      for (int idx = lane; idx < 32 * PC; idx += 32) {
+        const int r = idx / PC, pc = idx - r * PC;
+        const int32_t sr = __shfl_sync(0xffffffffu, s, r);
+        double* d = rowsM + r * SA + 2 * pc;
+        if (r < nv) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(d)),
+                       "l"(Mt + (int64_t)sr * NA + 2 * pc));
+        } else {
+          *reinterpret_cast<double2*>(d) = make_double2(0.0, 0.0);  // tail rows contribute nothing
+        }
+      }
+    } else if (!valid) {
       for (int e = 0; e < NA; ++e) myM[e] = 0.0;  // tail lanes contribute nothing
     } else if constexpr (kBulk) {
       fence_proxy_async_smem();
@@ -675,7 +728,11 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
     }
   }
   __syncwarp();
-  trace_fill_store<P>(lane, cmp, full, L + (int64_t)t * N);
+#ifndef FMM_M2L_TAB_EPILOGUE
+#define FMM_M2L_TAB_EPILOGUE 1
+#endif
+  if constexpr (FMM_M2L_TAB_EPILOGUE) trace_fill_store_tab<P>(lane, cmp, full, L + (int64_t)t * N);
+  else trace_fill_store<P>(lane, cmp, full, L + (int64_t)t * N);
 }
 
 // lockstep CTAs: targets ordered by descending chunk count (stable), so the warps of a CTA carry
