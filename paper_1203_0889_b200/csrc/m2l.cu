@@ -496,7 +496,7 @@ struct BigCfg2 {
   static constexpr int SA = m2l_row_stride(NA);  // staged M' rows (TMA: 16-B multiples)
   static constexpr int SL = odd_stride(NA);      // Lambda rows
 #ifndef FMM_BIG2_BLK
-#define FMM_BIG2_BLK 20
+#define FMM_BIG2_BLK 25
 #endif
   static constexpr int kBlk = FMM_BIG2_BLK;
   static constexpr int kBlocks = (NA + kBlk - 1) / kBlk;
