@@ -19,6 +19,9 @@
 #ifndef FMM_M2L_PREFETCH
 #define FMM_M2L_PREFETCH 0
 #endif
+#ifndef FMM_M2L_SPLIT_EPILOGUE  // p >= 7: compact Lambda to global, expanded by k_m2l_expand
+#define FMM_M2L_SPLIT_EPILOGUE 1
+#endif
 
 namespace fmmb {
 namespace {
@@ -240,6 +243,56 @@ __device__ __forceinline__ void trace_fill_store_tab(int lane, const double* cmp
     __syncwarp();
   }
   for (int i = lane; i < TraceTab<P>::N; i += 32) Lt[i] += tt.w[i] * full[i];
+}
+
+// Split epilogue (p >= 7): the M2L kernel stores each target's compact Lambda (b_c <= 1) and a
+// second, fully parallel kernel expands it: iterating the trace identity gives the closed form
+//   Lambda_{a,b,c} = (-1)^k sum_j C(k,j) Lambda_{a+2j, b+2(k-j), c-2k},  k = c div 2,
+// at most 5 compact terms per coefficient at p = 10. The serial, table-driven fill (8 warp
+// barriers and ~900 dependent constant/shared loads per target) took 17 % of the p = 10 kernel's
+// stall samples on a 7-warp SM (ncu, C5); here it runs one thread per (target, coefficient).
+template <int P>
+struct ExpandTab {
+  static constexpr int N = n_coef(P), K = (P + 1) / 2;
+  int8_t n[N];
+  int16_t idx[N][K];  // compact index of each term
+  double w[N][K];     // (-1)^k C(k,j) * (-1)^{|b|} / b!
+};
+template <int P>
+constexpr ExpandTab<P> make_expand_tab() {
+  using T = MI<P>;
+  ExpandTab<P> t{};
+  for (int i = 0; i < T::N; ++i) {
+    const int a = T::ea(i), b = T::eb(i), c = T::ec(i), k = c / 2;
+    const double w = ((T::deg(i) & 1) ? -1.0 : 1.0) / T::fact(i);
+    t.n[i] = static_cast<int8_t>(k + 1);
+    double binom = 1.0;
+    for (int j = 0; j <= k; ++j) {
+      t.idx[i][j] = static_cast<int16_t>(HM<P>::a_of(index_of(a + 2 * j, b + 2 * (k - j), c - 2 * k)));
+      t.w[i][j] = ((k & 1) ? -binom : binom) * w;
+      binom = binom * double(k - j) / double(j + 1);
+    }
+  }
+  return t;
+}
+// global (not constant) memory: the lanes of a warp read different entries
+template <int P>
+__device__ const ExpandTab<P> g_expand = make_expand_tab<P>();
+
+template <int P>
+__global__ void __launch_bounds__(256) k_m2l_expand(const int32_t* __restrict__ targets, int64_t ntargets,
+                                                    const double* __restrict__ Lc, double* __restrict__ L) {
+  constexpr int N = n_coef(P), NA = HM<P>::NA;
+  const int64_t g = blockIdx.x * (int64_t)256 + threadIdx.x;
+  if (g >= ntargets * N) return;
+  const int64_t r = g / N;
+  const int i = static_cast<int>(g - r * N);
+  const ExpandTab<P>& et = g_expand<P>;
+  const double* row = Lc + r * NA;
+  double v = 0.0;
+  const int n = et.n[i];
+  for (int j = 0; j < n; ++j) v = fma(et.w[i][j], row[et.idx[i][j]], v);
+  L[(int64_t)targets[r] * N + i] += v;
 }
 
 // Row stride (doubles) of the staged rows: even (16-B aligned rows) with an odd half, so a
@@ -524,13 +577,17 @@ struct BigCfg2 {
   // the fully unrolled contraction (p = 10: ~45 KB of SASS per chunk) is then fetched once per
   // SM position instead of once per warp (ncu at 1 warp/CTA: 40 % no_instruction stalls)
   static constexpr int kWarps = P >= 10 ? FMM_BIG2_WARPS_P10 : FMM_BIG2_WARPS;
+#ifndef FMM_BIG2_MINB_P10
+#define FMM_BIG2_MINB_P10 1
+#endif
+  static constexpr int kMinBlocks = P >= 10 ? FMM_BIG2_MINB_P10 : 1;
 };
 
 template <int P>
-__global__ void __launch_bounds__(32 * BigCfg2<P>::kWarps, 1)
+__global__ void __launch_bounds__(32 * BigCfg2<P>::kWarps, BigCfg2<P>::kMinBlocks)
 k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* __restrict__ off,
            const int32_t* __restrict__ src, const double4* __restrict__ cr, const double* __restrict__ Mt,
-           double* __restrict__ L) {
+           double* __restrict__ L, double* __restrict__ Lc) {
   using T = MI<P>;
   using H = HM<P>;
   using C = BigCfg2<P>;
@@ -713,6 +770,22 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
     if (W > 1) __syncthreads();
   }
   if (!have) return;
+  if constexpr (FMM_M2L_SPLIT_EPILOGUE) {
+    // the target's compact Lambda row goes to Lc[wid] (k_m2l_expand finishes it)
+    double* out = Lc + wid * NA;
+    if constexpr (kLR) {
+#pragma unroll
+      for (int q = 0; q < C::kBlocks; ++q)
+        if (q * C::kBlk + lane < NA && lane < C::kBlk) out[q * C::kBlk + lane] = accT[q];
+    } else {
+      for (int kk = lane; kk < NA; kk += 32) {  // column sums in fixed order
+        double acc = 0.0;
+        for (int j = 0; j < 32; ++j) acc += rowsL[j * SL + kk];
+        out[kk] = acc;
+      }
+    }
+    return;
+  }
   // reduce the 32 lane rows (column sums, fixed order) ...
   double* cmp = rowsM;            // NA reduced values
   double* full = rowsM + NA + 1;  // N values (32 * SA >= NA + N + 1)
@@ -788,10 +861,17 @@ struct M2L {
       tg = tout;
       c->kernel_launches += 4;
     }
+    double* Lc = FMM_M2L_SPLIT_EPILOGUE ? c->m2l_scratch.ensure(c->n_m2l_targets * C2::NA + 1) : nullptr;
     k_m2l_big2<P><<<(unsigned)ceil_div(c->n_m2l_targets, C2::kWarps), 32 * C2::kWarps, smem2, s>>>(
-        tg, c->n_m2l_targets, c->m2l_off.p, c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
+        tg, c->n_m2l_targets, c->m2l_off.p, c->m2l_src.p, c->c_cr.p, Mt, c->L.p, Lc);
     CK_LAUNCH("k_m2l_big2");
     c->kernel_launches += 2;
+    if (FMM_M2L_SPLIT_EPILOGUE) {
+      k_m2l_expand<P><<<(unsigned)ceil_div(c->n_m2l_targets * MI<P>::N, 256), 256, 0, s>>>(tg, c->n_m2l_targets, Lc,
+                                                                                         c->L.p);
+      CK_LAUNCH("k_m2l_expand");
+      c->kernel_launches += 1;
+    }
     }
   }
 };
