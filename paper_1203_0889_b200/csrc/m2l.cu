@@ -80,6 +80,31 @@ struct HM {
   static constexpr int g_of(int i) { return tab.g_of[i]; }
 };
 
+// Row stride (doubles) of the staged rows: even (16-B aligned rows) with an odd half, so a
+// quarter-warp's LDS.128 of 8 distinct rows hits 8 distinct bank groups.
+constexpr int m2l_row_stride(int n) {
+  int s = n + (n & 1);
+  return (s / 2) % 2 == 1 ? s : s + 2;
+}
+
+// One bulk copy per RUN of consecutive source cells instead of one per lane. A per-lane bulk copy
+// compiles to a serial loop over the active lanes (R2UR / ELECT / UBLKCP: the instruction takes
+// uniform operands): 32 steps per chunk, 20 % of the p = 10 kernel's and 48 % of the p = 6 kernel's
+// stall samples (ncu, C5 / C2). The sources of a list ascend and siblings are adjacent cells, so
+// most chunks are a handful of runs. The detraced rows are stored with the staged stride (padded)
+// in global memory, so a run is contiguous on both sides. Valid lanes are a prefix [0, nv).
+__device__ __forceinline__ void stage_runs(int lane, bool valid, int nv, int32_t s, double* rows, const double* Mt,
+                                           int S, uint64_t* bar) {
+  const int32_t sp = __shfl_up_sync(0xffffffffu, s, 1);
+  const bool head = valid && (lane == 0 || s != sp + 1);
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  if (head) {
+    const unsigned above = (heads >> 1) >> lane;  // run heads above this lane
+    const int next = above ? lane + __ffs(above) : nv;
+    bulk_g2s(rows + lane * S, Mt + (int64_t)s * S, static_cast<unsigned>(next - lane) * S * 8u, bar);
+  }
+}
+
 // M' = detraced multipoles (HM<P>::NA per cell, compact a_c <= 1 order); thread per cell, the
 // row in a per-thread shared-memory slice (odd stride: the lanes always touch the same entry, so
 // the accesses are conflict-free). Fold c >= 2 onto c - 2, highest c first.
@@ -109,10 +134,12 @@ __global__ void __launch_bounds__(kDetraceThreads) k_detrace(const double* __res
       });
     }
   });
+  constexpr int MS = m2l_row_stride(H::NA);  // rows padded to the staged stride
   static_for<H::NA>([&](auto K) {
     constexpr int k = decltype(K)::value;
-    Mt[cell * H::NA + k] = m[H::a_full(k)];
+    Mt[cell * MS + k] = m[H::a_full(k)];
   });
+  for (int k = H::NA; k < MS; ++k) Mt[cell * MS + k] = 0.0;
 }
 
 template <int P>
@@ -295,12 +322,6 @@ __global__ void __launch_bounds__(256) k_m2l_expand(const int32_t* __restrict__ 
   L[(int64_t)targets[r] * N + i] += v;
 }
 
-// Row stride (doubles) of the staged rows: even (16-B aligned rows) with an odd half, so a
-// quarter-warp's LDS.128 of 8 distinct rows hits 8 distinct bank groups.
-constexpr int m2l_row_stride(int n) {
-  int s = n + (n & 1);
-  return (s / 2) % 2 == 1 ? s : s + 2;
-}
 
 // Lane = source, warp = target. Dt (g_c <= 2) in registers; the contraction
 // Lambda_b += M'_a Dt_{a+b} over a_c, b_c <= 1 (one FMA per term) with Lambda in registers. Each
@@ -337,7 +358,7 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
 #define FMM_M2L_REG_C1 1
 #endif
   constexpr bool kRegC1 = FMM_M2L_REG_C1 != 0;
-  constexpr bool kBulk = !kCoop && (NA * 8) % 16 == 0;
+  constexpr bool kBulk = !kCoop;  // rows are padded to S doubles (16-B multiples) in global memory too
   // kBulk: the rows of chunk k+1 are copied (TMA) into the other buffer while chunk k computes
   constexpr int kBufs = kBulk && FMM_M2L_DB ? 2 : 1;
   extern __shared__ double smem[];
@@ -374,7 +395,7 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
         double* d = rows + r * S + 2 * pc;
         if (r < nv) {
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(d)),
-                       "l"(Mt + (int64_t)sr * NA + 2 * pc));
+                       "l"(Mt + (int64_t)sr * S + 2 * pc));
         } else {
           *reinterpret_cast<double2*>(d) = make_double2(0.0, 0.0);  // tail rows contribute nothing
         }
@@ -382,13 +403,15 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
       asm volatile("cp.async.commit_group;\n" ::: "memory");
       return;
     }
-    if (cbase + lane >= l1) {
+    const bool valid_l = cbase + lane < l1;
+    if (!valid_l)
       for (int e = 0; e < NA; ++e) row[e] = 0.0;  // tail lanes contribute nothing
-    } else if constexpr (kBulk) {
+    if constexpr (kBulk) {
       fence_proxy_async_smem();  // earlier generic reads of this row before the async write
-      bulk_g2s(row, Mt + (int64_t)s_lane * NA, NA * 8, &bars[w][b]);
-    } else {
-      const char* g = reinterpret_cast<const char*>(Mt + (int64_t)s_lane * NA);
+      const int nvl = l1 - cbase < 32 ? static_cast<int>(l1 - cbase) : 32;
+      stage_runs(lane, valid_l, nvl, s_lane, sR + (size_t)b * 32 * S, Mt, S, &bars[w][b]);
+    } else if (valid_l) {
+      const char* g = reinterpret_cast<const char*>(Mt + (int64_t)s_lane * S);
       const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(row));
 #pragma unroll
       for (int e = 0; e < NA * 8; e += 8)
@@ -397,7 +420,7 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
     if constexpr (kBulk) {
       if (lane == 0) {
         const int64_t nv = l1 - cbase < 32 ? l1 - cbase : 32;
-        mbar_arrive_expect_tx(&bars[w][b], static_cast<unsigned>(nv * NA * 8));
+        mbar_arrive_expect_tx(&bars[w][b], static_cast<unsigned>(nv * S * 8));
       }
     } else {
       asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -566,7 +589,15 @@ struct BigCfg2 {
   // 24.5 -> 19.6 ms; at p = 8 the extra reductions cost more than the occupancy gains)
   static constexpr bool kLR = P >= FMM_BIG2_LR_MIN_P;
   static constexpr int SB = odd_stride(kBlk);
-  static constexpr size_t kSmemPerWarp = sizeof(double) * 32 * (SA + (kLR ? SB : SL));
+#ifndef FMM_BIG2_SHFL
+#define FMM_BIG2_SHFL 0
+#endif
+  // kShfl: the per-block lane reduction as a register butterfly (reduce-scatter by shuffles: lane
+  // j ends with the sum of value j) instead of a transpose through shared memory: no block
+  // buffer (26 instead of 32.5 KB per warp at p = 10: 8 warps per SM), no warp barriers, and the
+  // shuffles are free to interleave with the next block's FMAs
+  static constexpr bool kShfl = kLR && FMM_BIG2_SHFL && kBlk <= 32;
+  static constexpr size_t kSmemPerWarp = sizeof(double) * 32 * (SA + (kLR ? (kShfl ? 0 : SB) : SL));
 #ifndef FMM_BIG2_WARPS
 #define FMM_BIG2_WARPS 1
 #endif
@@ -595,7 +626,7 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
   // warp-cooperative 16-B cp.async staging of the 32 source rows (a bulk copy per lane compiles
   // to a 32-step R2UR / ELECT / UBLKCP loop: ncu C5, ~9 % of the stall samples)
   constexpr bool kCoop = FMM_M2L_COOP && (NA % 2) == 0;
-  constexpr bool kBulk = !kCoop && (NA * 8) % 16 == 0;
+  constexpr bool kBulk = !kCoop;  // padded rows: always 16-B multiples
   constexpr int W = C::kWarps;
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t bars[W];
@@ -654,18 +685,20 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
         double* d = rowsM + r * SA + 2 * pc;
         if (r < nv) {
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(d)),
-                       "l"(Mt + (int64_t)sr * NA + 2 * pc));
+                       "l"(Mt + (int64_t)sr * SA + 2 * pc));
         } else {
           *reinterpret_cast<double2*>(d) = make_double2(0.0, 0.0);  // tail rows contribute nothing
         }
       }
-    } else if (!valid) {
-      for (int e = 0; e < NA; ++e) myM[e] = 0.0;  // tail lanes contribute nothing
     } else if constexpr (kBulk) {
+      if (!valid)
+        for (int e = 0; e < NA; ++e) myM[e] = 0.0;  // tail lanes contribute nothing
       fence_proxy_async_smem();
-      bulk_g2s(myM, Mt + (int64_t)s * NA, NA * 8, &bar);
+      stage_runs(lane, valid, l1 - base < 32 ? static_cast<int>(l1 - base) : 32, s, rowsM, Mt, SA, &bar);
+    } else if (!valid) {
+      for (int e = 0; e < NA; ++e) myM[e] = 0.0;
     } else {
-      const char* row = reinterpret_cast<const char*>(Mt + (int64_t)s * NA);
+      const char* row = reinterpret_cast<const char*>(Mt + (int64_t)s * SA);
       const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(myM));
 #pragma unroll 1
       for (int e = 0; e < NA * 8; e += 8)
@@ -674,7 +707,7 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
     if constexpr (kBulk) {
       if (lane == 0) {
         const int64_t nv = l1 - base < 32 ? l1 - base : 32;
-        mbar_arrive_expect_tx(&bar, static_cast<unsigned>(nv * NA * 8));
+        mbar_arrive_expect_tx(&bar, static_cast<unsigned>(nv * SA * 8));
       }
     } else {
       asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -744,7 +777,27 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
           });
         }
       });
-      if constexpr (kLR) {
+      if constexpr (C::kShfl) {
+        // butterfly reduce-scatter over the 32 lanes: at mask m a lane keeps the half of its values
+        // selected by its bit m and receives the partner's partials of that half
+        double v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = j < b1 - b0 ? lam[j] : 0.0;
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) {
+          const bool up = (lane & m) != 0;
+#pragma unroll
+          for (int i = 0; i < m; ++i) {
+            if (i < b1 - b0) {  // v[i + m] may be a structural zero, v[i] never is for i < width
+              const double lo = v[i], hi = v[i + m];
+              const double send = up ? lo : hi;
+              const double keep = up ? hi : lo;
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+            }
+          }
+        }
+        accT[decltype(BI)::value] += v[0];  // lane j: value j (zero for j >= width)
+      } else if constexpr (kLR) {
         double* red = rowsL;  // [32][SB]
 #pragma unroll
         for (int j = 0; j < b1 - b0; ++j) red[lane * C::SB + j] = lam[j];
@@ -808,6 +861,258 @@ k_m2l_big2(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t*
   else trace_fill_store<P>(lane, cmp, full, L + (int64_t)t * N);
 }
 
+// ------------------------------------------- staged-row M2L, flat pair partition (p >= 10) ----
+// The CSR source array is one flat sequence of (target, source) pairs ordered by target. Warp wg
+// takes the kFlatK * 32 consecutive pairs from position wg * 32 * K, whichever targets they belong
+// to: every chunk is full (C5's lists have a median of 70 sources, i.e. 32 + 32 + 6: per-target
+// chunks are 85 % full), every warp of a lockstep CTA has the same number of chunks (no sort by
+// chunk count), and a chunk may hold the tail of one target and the head of the next. Lane =
+// pair: its own target centre, the same Dt recurrence and contraction as k_m2l_big2; the
+// per-block lane reduction runs per segment (lanes of one target). A finished target's compact
+// Lambda goes to row (t + wg) of Lc; a target cut by a warp boundary leaves one row per warp,
+// (t + w) for w = w1..w2 (consecutive, collision-free because targets ascend with the warp id),
+// which k_m2l_expand_flat sums in that fixed order: deterministic, no atomics.
+// Chunk metadata (one thread per 32-pair chunk): rank of the target holding the chunk's first
+// pair (targets = the cells with a non-empty list, ascending), the lanes at which a list starts
+// inside the chunk (bit 0 always set), and whether the last target's list ends with the chunk.
+// tcr / toff: the targets' centres and list offsets by rank (one dependent load fewer per chunk).
+__global__ void k_flat_targets(const int32_t* __restrict__ targets, int64_t nt, const int64_t* __restrict__ off,
+                               const double4* __restrict__ cr, int64_t npairs, double4* __restrict__ tcr,
+                               int64_t* __restrict__ toff) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r > nt) return;
+  if (r == nt) {
+    toff[r] = npairs;
+    return;
+  }
+  tcr[r] = cr[targets[r]];
+  toff[r] = off[targets[r]];
+}
+
+__global__ void k_flat_meta(const int64_t* __restrict__ toff, int64_t nt, int64_t nchunks, int4* __restrict__ meta) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nchunks) return;
+  const int64_t pos0 = 32 * c;
+  int64_t lo = 0, hi = nt;  // largest r with toff[r] <= pos0 (toff[nt] = npairs > pos0)
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (toff[mid] <= pos0) lo = mid;
+    else hi = mid;
+  }
+  unsigned heads = 1u;
+  int64_t r = lo + 1;
+  while (r < nt && toff[r] < pos0 + 32) {
+    heads |= 1u << static_cast<int>(toff[r] - pos0);
+    ++r;
+  }
+  // r - 1 = the chunk's last target; its list ends here iff the next list (or the end) starts at pos0 + 32
+  // (a final, partly filled chunk ends its target as well)
+  const int last_ends = toff[r] <= pos0 + 32 ? 1 : 0;
+  meta[c] = make_int4(static_cast<int>(lo), static_cast<int>(heads), last_ends, 0);
+}
+
+template <int P>
+__global__ void __launch_bounds__(32 * BigCfg2<P>::kWarps, 1)
+k_m2l_flat(const int4* __restrict__ meta, int64_t nwarps, int K, int64_t npairs, const double4* __restrict__ tcr,
+           const int32_t* __restrict__ src, const double4* __restrict__ cr, const double* __restrict__ Mt,
+           double* __restrict__ Lc) {
+  using T = MI<P>;
+  using H = HM<P>;
+  using C = BigCfg2<P>;
+  constexpr int NA = C::NA, SA = C::SA, W = C::kWarps;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) uint64_t bars[W];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double* wsm = smem + (size_t)w * (C::kSmemPerWarp / sizeof(double));
+  double* rowsM = wsm;            // [32][SA]
+  double* red = wsm + 32 * SA;    // [32][SB] block buffer
+  double* myM = rowsM + lane * SA;
+  uint64_t& bar = bars[w];
+  if (lane == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  unsigned phase = 0;
+  const int64_t wg = blockIdx.x * (int64_t)W + w;
+  const bool have = wg < nwarps;
+  const int64_t c0 = wg * (int64_t)K;  // first chunk
+  const int64_t nchunks = (npairs + 31) >> 5;
+  double accT[C::kBlocks];
+#pragma unroll
+  for (int q = 0; q < C::kBlocks; ++q) accT[q] = 0.0;
+  int r_open = -1;  // rank of the unfinished target held in accT, or -1
+  int4 mt_next = have && c0 < nchunks ? meta[c0] : make_int4(0, 1, 1, 0);
+  int32_t s_next = have && 32 * c0 + lane < npairs ? src[32 * c0 + lane] : 0;
+  for (int c = 0; c < K; ++c) {
+    const int64_t pos0 = 32 * (c0 + c);
+    if (!have || pos0 >= npairs) {  // keep the CTA's chunk barriers
+      if (W > 1) __syncthreads();
+      continue;
+    }
+    const int4 mt = mt_next;
+    const int32_t s = s_next;
+    const bool valid = pos0 + lane < npairs;
+    FMM_CHECK(!valid || (s >= 0 && s < FMM_LIM(ncells)), "k_m2l_flat: source index");
+    const int nv = npairs - pos0 < 32 ? static_cast<int>(npairs - pos0) : 32;
+    if (!valid)
+      for (int e = 0; e < NA; ++e) myM[e] = 0.0;  // tail lanes contribute nothing
+    fence_proxy_async_smem();
+    stage_runs(lane, valid, nv, s, rowsM, Mt, SA, &bar);
+    if (lane == 0) mbar_arrive_expect_tx(&bar, static_cast<unsigned>(nv * SA * 8));
+    if (c + 1 < K && pos0 + 32 < npairs) {  // next chunk's metadata and sources: latency behind this chunk
+      mt_next = meta[c0 + c + 1];
+      if (pos0 + 32 + lane < npairs) s_next = src[pos0 + 32 + lane];
+    }
+    const unsigned heads = static_cast<unsigned>(mt.y);
+    const int r_lane = mt.x + __popc(heads & (0xffffffffu >> (31 - lane))) - 1;
+    const double4 ct = tcr[r_lane];
+    const double4 cs = valid ? cr[s] : ct;
+    double rx = 1.0, ry = 0.0, rz = 0.0;
+    if (valid) {
+      rx = cs.x - ct.x;  // R = source centre - target centre (traversal.hpp:146)
+      ry = cs.y - ct.y;
+      rz = cs.z - ct.z;
+    }
+    constexpr bool kC1 = C::kC1;
+    double D[kC1 ? NA : C::NG];
+    if constexpr (kC1) derivs_reg1<P>(rx, ry, rz, D);
+    else derivs_reg<P>(rx, ry, rz, D);
+    mbar_wait_sleep(&bar, phase);
+    phase ^= 1u;
+    __syncwarp();
+    const double* vM = myM;
+    static_for<C::kBlocks>([&](auto BI) {
+      constexpr int b0 = decltype(BI)::value * C::kBlk;
+      asm volatile("" ::: "memory");
+      constexpr int b1 = (b0 + C::kBlk < NA) ? b0 + C::kBlk : NA;
+      double lam[b1 - b0];
+#pragma unroll
+      for (int j = 0; j < b1 - b0; ++j) lam[j] = 0.0;
+      static_for<NA>([&](auto KA) {
+        constexpr int ka = decltype(KA)::value;
+        constexpr int ia = H::a_full(ka);
+        constexpr int aa = T::ea(ia), ab = T::eb(ia), ac = T::ec(ia), da = T::deg(ia);
+        if constexpr (da + T::deg(H::a_full(b0)) <= P - 1) {
+          const double m = vM[ka];
+          static_for<b1 - b0>([&](auto J) {
+            constexpr int ib = H::a_full(b0 + decltype(J)::value);
+            if constexpr (da + T::deg(ib) <= P - 1) {
+              constexpr int gx = aa + T::ea(ib), gy = ab + T::eb(ib), gz = ac + T::ec(ib);
+              if constexpr (!kC1) {
+                lam[decltype(J)::value] = fma(m, D[H::g_of(index_of(gx, gy, gz))], lam[decltype(J)::value]);
+              } else if constexpr (gz <= 1) {
+                lam[decltype(J)::value] = fma(m, D[H::a_of(index_of(gx, gy, gz))], lam[decltype(J)::value]);
+              } else {  // gz == 2: trace identity
+                lam[decltype(J)::value] = fma(-m, D[H::a_of(index_of(gx + 2, gy, 0))], lam[decltype(J)::value]);
+                lam[decltype(J)::value] = fma(-m, D[H::a_of(index_of(gx, gy + 2, 0))], lam[decltype(J)::value]);
+              }
+            }
+          });
+        }
+      });
+#pragma unroll
+      for (int j = 0; j < b1 - b0; ++j) red[lane * C::SB + j] = lam[j];
+      __syncwarp();
+      if (heads == 1u) {  // one target in the chunk: four interleaved chains over all lanes
+        if (lane < b1 - b0) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            s0 += red[j * C::SB + lane];
+            s1 += red[(j + 1) * C::SB + lane];
+            s2 += red[(j + 2) * C::SB + lane];
+            s3 += red[(j + 3) * C::SB + lane];
+          }
+          accT[decltype(BI)::value] += (s0 + s1) + (s2 + s3);
+          if (mt.z) {
+            Lc[(mt.x + wg) * NA + b0 + lane] = accT[decltype(BI)::value];
+            accT[decltype(BI)::value] = 0.0;
+          }
+        }
+      } else if (__popc(heads) == 2) {
+        // two targets: the same 32 loads, predicated onto two sets of four chains (the CTA's warps
+        // advance in lockstep, so a chunk with a boundary must not cost more than one without)
+        const int bnd = 31 - __clz(heads);  // first lane of the second target
+        if (lane < b1 - b0) {
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const double v0 = red[j * C::SB + lane], v1 = red[(j + 1) * C::SB + lane];
+            const double v2 = red[(j + 2) * C::SB + lane], v3 = red[(j + 3) * C::SB + lane];
+            if (j < bnd) s0 += v0; else u0 += v0;
+            if (j + 1 < bnd) s1 += v1; else u1 += v1;
+            if (j + 2 < bnd) s2 += v2; else u2 += v2;
+            if (j + 3 < bnd) s3 += v3; else u3 += v3;
+          }
+          Lc[(mt.x + wg) * NA + b0 + lane] = accT[decltype(BI)::value] + ((s0 + s1) + (s2 + s3));
+          accT[decltype(BI)::value] = (u0 + u1) + (u2 + u3);
+          if (mt.z) {
+            Lc[(mt.x + 1 + wg) * NA + b0 + lane] = accT[decltype(BI)::value];
+            accT[decltype(BI)::value] = 0.0;
+          }
+        }
+      } else {  // segments [a, b) of consecutive lanes, one target each, in lane order
+        unsigned rest = heads;
+        int r_seg = mt.x;
+        while (rest) {
+          const int a = __ffs(rest) - 1;
+          rest &= rest - 1;
+          const int b = rest ? __ffs(rest) - 1 : 32;
+          if (lane < b1 - b0) {
+            double s0 = 0.0, s1 = 0.0;
+            for (int j = a; j + 1 < b; j += 2) {
+              s0 += red[j * C::SB + lane];
+              s1 += red[(j + 1) * C::SB + lane];
+            }
+            if ((b - a) & 1) s0 += red[(b - 1) * C::SB + lane];
+            accT[decltype(BI)::value] += s0 + s1;
+            if (rest || mt.z) {  // every segment but the last ends inside the chunk
+              Lc[(r_seg + wg) * NA + b0 + lane] = accT[decltype(BI)::value];
+              accT[decltype(BI)::value] = 0.0;
+            }
+          }
+          ++r_seg;
+        }
+      }
+      __syncwarp();
+    });
+    r_open = mt.z ? -1 : mt.x + __popc(heads) - 1;
+    __syncwarp();  // every lane done with its M' row before the next chunk's copies land
+    if (W > 1) __syncthreads();
+  }
+  if (r_open >= 0) {  // the target cut by the end of this warp's range: its partial row
+#pragma unroll
+    for (int q = 0; q < C::kBlocks; ++q)
+      if (q * C::kBlk + lane < NA && lane < C::kBlk) Lc[(r_open + wg) * NA + q * C::kBlk + lane] = accT[q];
+  }
+}
+
+// Expansion for the flat partition: the rows of the target of rank r are (r + w), w = w1..w2,
+// the warps whose pair ranges meet its list; summed in warp order, then the closed-form trace
+// expansion.
+template <int P>
+__global__ void __launch_bounds__(256) k_m2l_expand_flat(const int32_t* __restrict__ targets, int64_t nt,
+                                                         const int64_t* __restrict__ toff, int64_t span,
+                                                         const double* __restrict__ Lc, double* __restrict__ L) {
+  constexpr int N = n_coef(P), NA = HM<P>::NA;
+  const int64_t g = blockIdx.x * (int64_t)256 + threadIdx.x;
+  if (g >= nt * N) return;
+  const int64_t r = g / N;
+  const int i = static_cast<int>(g - r * N);
+  const int64_t w1 = toff[r] / span, w2 = (toff[r + 1] - 1) / span;
+  const ExpandTab<P>& et = g_expand<P>;
+  const int n = et.n[i];
+  double v = 0.0;
+  for (int j = 0; j < n; ++j) {
+    const int k = et.idx[i][j];
+    double acc = 0.0;
+    for (int64_t w = w1; w <= w2; ++w) acc += Lc[(r + w) * NA + k];
+    v = fma(et.w[i][j], acc, v);
+  }
+  L[(int64_t)targets[r] * N + i] += v;
+}
+
 // lockstep CTAs: targets ordered by descending chunk count (stable), so the warps of a CTA carry
 // similar list lengths and few idle through the chunk barriers
 __global__ void k_target_chunks(const int32_t* __restrict__ targets, int64_t n, const int64_t* __restrict__ off,
@@ -821,14 +1126,14 @@ struct M2L {
   static void run(fmm_ctx* c, cudaStream_t s) {
     if constexpr (P <= 6) {
       constexpr int S = m2l_row_stride(HM<P>::NA);
-      constexpr int kBufs = (HM<P>::NA * 8) % 16 == 0 && FMM_M2L_DB ? 2 : 1;
+      constexpr int kBufs = FMM_M2L_DB && !(FMM_M2L_COOP && HM<P>::NA % 2 == 0) ? 2 : 1;  // as in the kernel
       const size_t smem = sizeof(double) * kM2LWarps * kBufs * 32 * S;
       static std::atomic<uint64_t> attr{0};
       once_per_device(attr, c->cfg.device, [&] {
         CK(cudaFuncSetAttribute(k_m2l_reg<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       });
       if (c->n_m2l_targets == 0) return;
-      double* Mt = c->m2l_mt.ensure(c->ncells * HM<P>::NA + 1);
+      double* Mt = c->m2l_mt.ensure(c->ncells * m2l_row_stride(HM<P>::NA) + 1);
       launch_detrace<P>(c, Mt, s);
       k_m2l_reg<P><<<ceil_div(c->n_m2l_targets, kM2LWarps), 32 * kM2LWarps, smem, s>>>(c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p,
                                                                     c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
@@ -842,8 +1147,39 @@ struct M2L {
       CK(cudaFuncSetAttribute(k_m2l_big2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     });
     if (c->n_m2l_targets == 0) return;
-    double* Mt = c->m2l_mt.ensure(c->ncells * C2::NA + 1);
+    double* Mt = c->m2l_mt.ensure(c->ncells * C2::SA + 1);
     launch_detrace<P>(c, Mt, s);
+#ifndef FMM_BIG2_FLAT
+#define FMM_BIG2_FLAT 1
+#endif
+    if constexpr (C2::kLR && !C2::kShfl && FMM_BIG2_FLAT && FMM_M2L_SPLIT_EPILOGUE) {
+      if (c->world == 1) {  // whole lists (the sharded step runs the target list of the rank)
+        const int64_t np = c->n_m2l, nt = c->n_m2l_targets;
+        // chunks per warp: about one average list, within [3, 16]
+        const int64_t avg = np / (32 * std::max<int64_t>(nt, 1));
+        const int K = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(3, avg)));
+        const int64_t span = 32 * (int64_t)K;
+        const int64_t nchunks = (np + 31) / 32, nw = (nchunks + K - 1) / K;
+        int4* meta = reinterpret_cast<int4*>(c->keys_a.ensure(2 * nchunks + 2));
+        double4* tcr = reinterpret_cast<double4*>(c->keys_b.ensure(5 * (nt + 1) + 4));
+        int64_t* toff = reinterpret_cast<int64_t*>(tcr + nt + 1);
+        double* Lc = c->m2l_scratch.ensure((nt + nw + 1) * C2::NA);
+        k_flat_targets<<<ceil_div(nt + 1, 256), 256, 0, s>>>(c->m2l_targets.p, nt, c->m2l_off.p, c->c_cr.p, np, tcr, toff);
+        k_flat_meta<<<ceil_div(nchunks, 256), 256, 0, s>>>(toff, nt, nchunks, meta);
+        static std::atomic<uint64_t> attr3{0};
+        once_per_device(attr3, c->cfg.device, [&] {
+          CK(cudaFuncSetAttribute(k_m2l_flat<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        });
+        k_m2l_flat<P><<<(unsigned)ceil_div(nw, C2::kWarps), 32 * C2::kWarps, smem2, s>>>(meta, nw, K, np, tcr, c->m2l_src.p,
+                                                                                     c->c_cr.p, Mt, Lc);
+        CK_LAUNCH("k_m2l_flat");
+        k_m2l_expand_flat<P><<<(unsigned)ceil_div(nt * MI<P>::N, 256), 256, 0, s>>>(c->m2l_targets.p, nt, toff, span, Lc,
+                                                                                  c->L.p);
+        CK_LAUNCH("k_m2l_expand_flat");
+        c->kernel_launches += 5;
+        return;
+      }
+    }
     const int32_t* tg = c->m2l_targets.p;
 #ifndef FMM_BIG2_SORT
 #define FMM_BIG2_SORT 1
