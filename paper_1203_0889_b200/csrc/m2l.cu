@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(256) k_m2l_expand(const int32_t* __restrict__ 
 #define FMM_M2L_DB 0  // measured slower at p = 6 (1.07 -> 1.14 ms): register pressure
 #endif
 #ifndef FMM_M2L_MINB
-#define FMM_M2L_MINB 12
+#define FMM_M2L_MINB 10
 #endif
 #ifndef FMM_M2L_WARPS
 #define FMM_M2L_WARPS 1
@@ -429,6 +429,17 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
   int32_t s_cur = (l0 + lane < l1) ? src[l0 + lane] : t;
   int32_t s_nxt = (l0 + 32 + lane < l1) ? src[l0 + 32 + lane] : t;
   if (kBufs == 2) stage(0, l0, s_cur);
+#ifndef FMM_M2L_REG_PF
+#define FMM_M2L_REG_PF 1  // A/B at C2: 0.806 -> 0.801 ms, with 10 CTAs/SM 0.793
+#endif
+#if FMM_M2L_REG_PF
+  // next chunk's source centre one chunk ahead (its L2 latency behind this chunk's contraction)
+  double cnx = ct.x, cny = ct.y, cnz = ct.z;
+  if (l0 + lane < l1) {
+    const double4 c0 = cr[s_cur];
+    cnx = c0.x; cny = c0.y; cnz = c0.z;
+  }
+#endif
   unsigned k = 0;
   for (int64_t base = l0; base < l1; base += 32, ++k) {
     const int b = kBufs == 2 ? (k & 1) : 0;
@@ -440,6 +451,18 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
     }
     const int32_t s_nn = (base + 64 + lane < l1) ? src[base + 64 + lane] : t;
     FMM_CHECK(s_cur >= 0 && s_cur < FMM_LIM(ncells), "k_m2l_reg: source index");
+#if FMM_M2L_REG_PF
+    double rx = 1.0, ry = 0.0, rz = 0.0;
+    if (valid) {
+      rx = cnx - ct.x;
+      ry = cny - ct.y;
+      rz = cnz - ct.z;
+    }
+    if (base + 32 + lane < l1) {
+      const double4 c1 = cr[s_nxt];
+      cnx = c1.x; cny = c1.y; cnz = c1.z;
+    }
+#else
     const double4 cs = valid ? cr[s_cur] : ct;
     double rx = 1.0, ry = 0.0, rz = 0.0;
     if (valid) {
@@ -447,6 +470,7 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
       ry = cs.y - ct.y;
       rz = cs.z - ct.z;
     }
+#endif
     // kRegC1: Dt over g_c <= 1 only (NA values instead of NG), the g_c = 2 entries from the trace
     // identity in the contraction: fewer registers (occupancy) for a few more FMAs
     double D[kRegC1 ? NA : NG];
@@ -920,6 +944,10 @@ k_m2l_flat(const int4* __restrict__ meta, int64_t nwarps, int K, int64_t npairs,
   using H = HM<P>;
   using C = BigCfg2<P>;
   constexpr int NA = C::NA, SA = C::SA, W = C::kWarps;
+#ifndef FMM_FLAT_SYNC
+#define FMM_FLAT_SYNC 1
+#endif
+  constexpr bool kSync = FMM_FLAT_SYNC != 0;  // lockstep chunk barriers
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t bars[W];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -947,7 +975,7 @@ k_m2l_flat(const int4* __restrict__ meta, int64_t nwarps, int K, int64_t npairs,
   for (int c = 0; c < K; ++c) {
     const int64_t pos0 = 32 * (c0 + c);
     if (!have || pos0 >= npairs) {  // keep the CTA's chunk barriers
-      if (W > 1) __syncthreads();
+      if (W > 1 && kSync) __syncthreads();
       continue;
     }
     const int4 mt = mt_next;
@@ -1079,7 +1107,7 @@ k_m2l_flat(const int4* __restrict__ meta, int64_t nwarps, int K, int64_t npairs,
     });
     r_open = mt.z ? -1 : mt.x + __popc(heads) - 1;
     __syncwarp();  // every lane done with its M' row before the next chunk's copies land
-    if (W > 1) __syncthreads();
+    if (W > 1 && kSync) __syncthreads();
   }
   if (r_open >= 0) {  // the target cut by the end of this warp's range: its partial row
 #pragma unroll
@@ -1155,9 +1183,11 @@ struct M2L {
     if constexpr (C2::kLR && !C2::kShfl && FMM_BIG2_FLAT && FMM_M2L_SPLIT_EPILOGUE) {
       if (c->world == 1) {  // whole lists (the sharded step runs the target list of the rank)
         const int64_t np = c->n_m2l, nt = c->n_m2l_targets;
-        // chunks per warp: about one average list, within [3, 16]
-        const int64_t avg = np / (32 * std::max<int64_t>(nt, 1));
-        const int K = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(3, avg)));
+        // chunks per warp (A/B at C5: 3 -> 10.05 ms, 6 -> 9.92, 12 -> 9.86: fewer CTA prologues)
+#ifndef FMM_FLAT_K
+#define FMM_FLAT_K 12
+#endif
+        const int K = FMM_FLAT_K;
         const int64_t span = 32 * (int64_t)K;
         const int64_t nchunks = (np + 31) / 32, nw = (nchunks + K - 1) / K;
         int4* meta = reinterpret_cast<int4*>(c->keys_a.ensure(2 * nchunks + 2));
