@@ -382,6 +382,22 @@ __device__ __forceinline__ void tile_compute_prec(const float4* __restrict__ buf
 // on the next one (the producer runs up to one tile ahead: two buffers).
 constexpr int kWsThreads = kThreads + 32;
 
+// Phase timestamps of sampled CTAs (variant builds only, tools/p2p_trace.py): clock64 at entry,
+// item loaded, producer tile-0 set up / copies issued / landed / published, producer done,
+// consumers' first tile seen / pair loops done / results written; tiles; targets.
+#ifndef FMM_P2P_TRACE
+#define FMM_P2P_TRACE 0
+#endif
+#if FMM_P2P_TRACE
+constexpr int kTraceCtas = 1 << 16, kTraceStride = 16;
+__device__ unsigned long long g_p2p_trace[kTraceCtas * 16];
+#define P2P_TR(slot) do { if (trace) trace[slot] = clock64(); } while (0)
+#define P2P_TRV(slot, v) do { if (trace) trace[slot] = (v); } while (0)
+#else
+#define P2P_TR(slot) do {} while (0)
+#define P2P_TRV(slot, v) do {} while (0)
+#endif
+
 // producer warp: shift one tile's staged bodies into the target frame and negate
 __device__ __forceinline__ void convert_warp(int lane, const TileTab& tt, float4* buf) {
   const int nseg = tt.nseg;
@@ -437,6 +453,13 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
   __shared__ TileTab tabs[2];
   __shared__ __align__(8) uint64_t full[2], tmab[2], empty[2];
 
+#if FMM_P2P_TRACE
+  unsigned long long* trace = nullptr;
+  if ((threadIdx.x == 0 || threadIdx.x == kThreads) && blockIdx.x % kTraceStride == 0 &&
+      blockIdx.x / kTraceStride < kTraceCtas)
+    trace = g_p2p_trace + (blockIdx.x / kTraceStride) * 16;
+  if (threadIdx.x == 0) P2P_TR(0);
+#endif
   const P2PItem it = items[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0) {
@@ -448,23 +471,31 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  if (tid == 0) P2P_TR(1);
 
   if (tid >= kThreads) {  // ---- producer warp
     int32_t cursor = it.lb, off = 0;
-    for (unsigned k = 0; cursor < it.le; ++k) {
+    unsigned k = 0;
+    for (; cursor < it.le; ++k) {
       const int b = k & 1;
       if (k >= 2) mbar_wait(&empty[b], ((k >> 1) - 1) & 1u);
       tile_setup_ent(lane, it.le, cursor, off, ent + cursor, tabs[b]);
       __syncwarp();
+      if (k == 0) P2P_TR(2);
       tile_tma(lane, tabs[b], bodyf, bodyl, sS[b], &tmab[b]);
+      if (k == 0) P2P_TR(3);
       mbar_wait(&tmab[b], (k >> 1) & 1u);
+      if (k == 0) P2P_TR(4);
       if (tabs[b].prec) convert_prec_warp(lane, tabs[b], sS[b]);
       else convert_warp(lane, tabs[b], sS[b]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[b]);
+      if (k == 0) P2P_TR(5);
       cursor = tabs[b].next;
       off = tabs[b].next_off;
     }
+    P2P_TR(6);
+    P2P_TRV(10, k);
     return;
   }
 
@@ -495,6 +526,7 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
     for (unsigned k = 0;; ++k) {
       const int b = k & 1;
       mbar_wait(&full[b], (k >> 1) & 1u);
+      if (k == 0) P2P_TR(7);
       const TileTab& tc = tabs[b];
       const int nb = tc.off[tc.nseg];
       const bool prec = tc.prec != 0, guard = tc.guard != 0, more = tc.next < it.le;
@@ -511,6 +543,8 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
       if (!more) break;
     }
   }
+  P2P_TR(8);
+  P2P_TRV(11, static_cast<unsigned long long>(nt));
   // reduce the G lane groups in fixed order (reusing the tile buffer: the producer is done and
   // every consumer has released its last tile once this named barrier completes) and write
   asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads) : "memory");
@@ -547,6 +581,7 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
       p[3] = v[3];
     }
   }
+  if (tid == 0) P2P_TR(9);
 }
 
 // ------------------------------------------------------------------------ FP64 kernel ----
@@ -1158,3 +1193,10 @@ void op_p2p(int64_t count, const int32_t* ranges4, const double* xyzq, int64_t n
   cudaFree(a);
 }
 }  // namespace fmmb
+
+#if FMM_P2P_TRACE
+extern "C" int fmm_debug_p2p_trace(unsigned long long* out, int nctas) {
+  const size_t bytes = sizeof(unsigned long long) * 16 * static_cast<size_t>(nctas);
+  return cudaMemcpyFromSymbol(out, fmmb::g_p2p_trace, bytes) == cudaSuccess ? 0 : 1;
+}
+#endif
