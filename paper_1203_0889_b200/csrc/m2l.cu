@@ -306,22 +306,56 @@ constexpr ExpandTab<P> make_expand_tab() {
 template <int P>
 __device__ const ExpandTab<P> g_expand = make_expand_tab<P>();
 
+// Block = one coefficient per thread (its table row in registers), looping over a range of
+// targets; each target's compact row is staged in shared memory (double-buffered: one barrier
+// per target) and the RMW of L is coalesced. (One thread per (target, coefficient) with the table
+// read from global memory per element took 1.2 ms at C5, 5x its memory time.)
+constexpr int kExpandTargets = 32;  // targets per block
+template <int P, class RowFn>
+__device__ __forceinline__ void expand_rows(const int32_t* __restrict__ targets, int64_t nt, double* __restrict__ L,
+                                            RowFn&& compact) {
+  constexpr int N = n_coef(P), NA = HM<P>::NA, K = ExpandTab<P>::K;
+  static_assert(N <= 256, "one coefficient per thread");
+  __shared__ double row[2][NA];
+  const int i = threadIdx.x;
+  const ExpandTab<P>& et = g_expand<P>;
+  int idx[K];
+  double w[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {  // unused terms: weight 0 on entry 0
+    idx[j] = 0;
+    w[j] = 0.0;
+  }
+  if (i < N) {
+    const int n = et.n[i];
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (j < n) {
+        idx[j] = et.idx[i][j];
+        w[j] = et.w[i][j];
+      }
+  }
+  const int64_t r0 = blockIdx.x * (int64_t)kExpandTargets;
+  const int64_t r1 = r0 + kExpandTargets < nt ? r0 + kExpandTargets : nt;
+  for (int64_t r = r0; r < r1; ++r) {
+    double* rw = row[(r - r0) & 1];
+    if (i < NA) rw[i] = compact(r, i);
+    __syncthreads();  // the readers of this buffer's previous row passed the barrier in between
+    if (i < N) {
+      double v = 0.0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) v = fma(w[j], rw[idx[j]], v);
+      L[(int64_t)targets[r] * N + i] += v;
+    }
+  }
+}
+
 template <int P>
 __global__ void __launch_bounds__(256) k_m2l_expand(const int32_t* __restrict__ targets, int64_t ntargets,
                                                     const double* __restrict__ Lc, double* __restrict__ L) {
-  constexpr int N = n_coef(P), NA = HM<P>::NA;
-  const int64_t g = blockIdx.x * (int64_t)256 + threadIdx.x;
-  if (g >= ntargets * N) return;
-  const int64_t r = g / N;
-  const int i = static_cast<int>(g - r * N);
-  const ExpandTab<P>& et = g_expand<P>;
-  const double* row = Lc + r * NA;
-  double v = 0.0;
-  const int n = et.n[i];
-  for (int j = 0; j < n; ++j) v = fma(et.w[i][j], row[et.idx[i][j]], v);
-  L[(int64_t)targets[r] * N + i] += v;
+  constexpr int NA = HM<P>::NA;
+  expand_rows<P>(targets, ntargets, L, [&](int64_t r, int i) { return Lc[r * NA + i]; });
 }
-
 
 // Lane = source, warp = target. Dt (g_c <= 2) in registers; the contraction
 // Lambda_b += M'_a Dt_{a+b} over a_c, b_c <= 1 (one FMA per term) with Lambda in registers. Each
@@ -1123,22 +1157,13 @@ template <int P>
 __global__ void __launch_bounds__(256) k_m2l_expand_flat(const int32_t* __restrict__ targets, int64_t nt,
                                                          const int64_t* __restrict__ toff, int64_t span,
                                                          const double* __restrict__ Lc, double* __restrict__ L) {
-  constexpr int N = n_coef(P), NA = HM<P>::NA;
-  const int64_t g = blockIdx.x * (int64_t)256 + threadIdx.x;
-  if (g >= nt * N) return;
-  const int64_t r = g / N;
-  const int i = static_cast<int>(g - r * N);
-  const int64_t w1 = toff[r] / span, w2 = (toff[r + 1] - 1) / span;
-  const ExpandTab<P>& et = g_expand<P>;
-  const int n = et.n[i];
-  double v = 0.0;
-  for (int j = 0; j < n; ++j) {
-    const int k = et.idx[i][j];
+  constexpr int NA = HM<P>::NA;
+  expand_rows<P>(targets, nt, L, [&](int64_t r, int i) {
+    const int64_t w1 = toff[r] / span, w2 = (toff[r + 1] - 1) / span;
     double acc = 0.0;
-    for (int64_t w = w1; w <= w2; ++w) acc += Lc[(r + w) * NA + k];
-    v = fma(et.w[i][j], acc, v);
-  }
-  L[(int64_t)targets[r] * N + i] += v;
+    for (int64_t w = w1; w <= w2; ++w) acc += Lc[(r + w) * NA + i];
+    return acc;
+  });
 }
 
 // lockstep CTAs: targets ordered by descending chunk count (stable), so the warps of a CTA carry
@@ -1203,7 +1228,7 @@ struct M2L {
         k_m2l_flat<P><<<(unsigned)ceil_div(nw, C2::kWarps), 32 * C2::kWarps, smem2, s>>>(meta, nw, K, np, tcr, c->m2l_src.p,
                                                                                      c->c_cr.p, Mt, Lc);
         CK_LAUNCH("k_m2l_flat");
-        k_m2l_expand_flat<P><<<(unsigned)ceil_div(nt * MI<P>::N, 256), 256, 0, s>>>(c->m2l_targets.p, nt, toff, span, Lc,
+        k_m2l_expand_flat<P><<<(unsigned)ceil_div(nt, kExpandTargets), 256, 0, s>>>(c->m2l_targets.p, nt, toff, span, Lc,
                                                                                   c->L.p);
         CK_LAUNCH("k_m2l_expand_flat");
         c->kernel_launches += 5;
@@ -1233,7 +1258,7 @@ struct M2L {
     CK_LAUNCH("k_m2l_big2");
     c->kernel_launches += 2;
     if (FMM_M2L_SPLIT_EPILOGUE) {
-      k_m2l_expand<P><<<(unsigned)ceil_div(c->n_m2l_targets * MI<P>::N, 256), 256, 0, s>>>(tg, c->n_m2l_targets, Lc,
+      k_m2l_expand<P><<<(unsigned)ceil_div(c->n_m2l_targets, kExpandTargets), 256, 0, s>>>(tg, c->n_m2l_targets, Lc,
                                                                                          c->L.p);
       CK_LAUNCH("k_m2l_expand");
       c->kernel_launches += 1;

@@ -394,11 +394,15 @@ def test_tree_reuse_across_distributions(fmmlib, orc):
     ctx.close()
 
 
-def test_stage_isolated_m2l_and_p2p(fmmlib, orc):
+@pytest.mark.parametrize("gen,n,p", [(2, 20000, 6), (4, 12000, 8), (5, 8000, 10)],
+                         ids=["p6-register", "p8-staged-rows", "p10-flat-partition"])
+def test_stage_isolated_m2l_and_p2p(fmmlib, orc, gen, n, p):
     """Inject the oracle's tree, lists and multipoles; the GPU M2L locals and P2P near field
-    then match the oracle's per coefficient / per body."""
-    bodies = fmmlib.generate_bodies(2, 20000, 5)
-    p, theta = 6, 0.5
+    then match the oracle's per coefficient / per body. One case per production M2L kernel:
+    k_m2l_reg (p <= 6), k_m2l_big2 (p = 7..9) and k_m2l_flat (p >= 10; the sphere-surface tree's
+    short lists put several targets into one 32-pair chunk and cut targets at warp ranges)."""
+    bodies = fmmlib.generate_bodies(gen, n, 5)
+    theta = 0.5
     t = oracle_run(orc, bodies, 64, p, theta)
     c = t.cells()
     m, pp = orc.traverse(t, theta)
