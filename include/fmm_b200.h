@@ -132,6 +132,11 @@ int fmm_set_mutual(fmm_ctx* ctx, int on);
  * last traversal. */
 int fmm_set_traversal_debug(fmm_ctx* ctx, int force_keys64, int64_t initial_capacity);
 int fmm_get_traversal_regrows(fmm_ctx* ctx, int* regrows);
+/* Test / tuning hook for the FP32 P2P kernel's CTA shape (the production choice is automatic, by
+ * the mean number of P2P sources per target body): shape = 0 wide CTAs (128 consumer threads,
+ * 1 024-body tiles, 6 per SM), 1 narrow CTAs (64 consumer threads, 512-body tiles, 10 per SM),
+ * -1 automatic. Results agree to FP32 rounding (the tiles, hence the FP32 partial sums, differ). */
+int fmm_set_p2p_shape(fmm_ctx* ctx, int shape);
 
 /* ---- outputs ------------------------------------------------------------------------ */
 /* order: 0 = tree (sorted) body order (potentials(), tree.cpp:121-126), 1 = input order.

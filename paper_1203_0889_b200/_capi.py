@@ -100,6 +100,7 @@ SIGNATURES = {
     "fmm_set_overlap": (C.c_int, [_vp, C.c_int]),
     "fmm_set_mutual": (C.c_int, [_vp, C.c_int]),
     "fmm_set_traversal_debug": (C.c_int, [_vp, C.c_int, C.c_int64]),
+    "fmm_set_p2p_shape": (C.c_int, [_vp, C.c_int]),
     "fmm_get_traversal_regrows": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "fmm_update_bodies": (C.c_int, [_vp, _dp, C.c_int64]),
     "fmm_evaluate_reuse": (C.c_int, [_vp, C.POINTER(C.c_int)]),

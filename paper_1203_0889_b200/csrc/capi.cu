@@ -733,6 +733,14 @@ int fmm_set_traversal_debug(fmm_ctx* c, int force_keys64, int64_t initial_capaci
   });
 }
 
+int fmm_set_p2p_shape(fmm_ctx* c, int shape) {
+  if (!c) return FMM_ERR_ARG;
+  return guard(c, [&] {
+    if (shape < -1 || shape > 1) fail(FMM_ERR_ARG, "shape must be -1, 0 or 1");
+    c->p2p_shape = shape;
+  });
+}
+
 int fmm_get_traversal_regrows(fmm_ctx* c, int* regrows) {
   if (!c || !regrows) return FMM_ERR_ARG;
   *regrows = c->trav_regrows;

@@ -106,7 +106,6 @@ struct P2PEnt {
 };
 static_assert(sizeof(P2PEnt) == 32, "P2PEnt is 32 B");
 constexpr int kKindFar = 0, kKindSelf = 1, kKindNear = 2;
-constexpr int kHalfTile = kTileBodies / 2;  // compensated tiles: hi in [0, half), lo in [half, 2 half)
 
 struct TileTab {
   int32_t off[kTileSegs + 1];
@@ -119,6 +118,7 @@ struct TileTab {
 // producer warp: take the list entries from (cursor, cur_off) that fit in one tile; e[i] is list
 // entry cursor + i, lane l holds entries l and l + 32 (small leaves, e.g. C5's median of 18
 // bodies, fill a 1 024-body tile only with ~60 entries)
+template <int TB>
 __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cursor, int32_t cur_off,
                                                const P2PEnt* e, TileTab& tt) {
   constexpr int H = kTileSegs / 32;
@@ -155,7 +155,7 @@ __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cur
   // one class per tile: the self entry alone (r^2 == 0 guard), near entries (compensated, half
   // the bodies: hi and lo staged), far entries (plain FP32)
   const int kind0 = __shfl_sync(0xffffffffu, kind[0], 0);
-  const int cap = kind0 == kKindFar ? kTileBodies : kHalfTile;
+  const int cap = kind0 == kKindFar ? TB : TB / 2;
   int32_t running = 0;
   unsigned m[H], other[H];
 #pragma unroll
@@ -217,6 +217,7 @@ __device__ __forceinline__ void tile_setup_ent(int lane, int32_t le, int32_t cur
 // producer warp: one bulk copy per list entry of the tile (lane k copies entries k, k + 32);
 // the bytes land on `bar`. The proxy fence orders earlier generic reads/writes of the buffer
 // (released to the producer through the empty barrier) before the async-proxy writes.
+template <int TB>
 __device__ __forceinline__ void tile_tma(int lane, const TileTab& tt, const float4* __restrict__ bodyf,
                                          const float4* __restrict__ bodyl, float4* buf, uint64_t* bar) {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -225,11 +226,11 @@ __device__ __forceinline__ void tile_tma(int lane, const TileTab& tt, const floa
   if (lane == 0) mbar_arrive_expect_tx(bar, static_cast<unsigned>(tt.off[nseg]) * (prec ? 32u : 16u));
   for (int idx = lane; idx < nseg; idx += 32) {
     const int32_t o0 = tt.off[idx];
-    FMM_CHECK(o0 >= 0 && tt.off[idx + 1] > o0 && tt.off[idx + 1] <= (prec ? kHalfTile : kTileBodies),
+    FMM_CHECK(o0 >= 0 && tt.off[idx + 1] > o0 && tt.off[idx + 1] <= (prec ? TB / 2 : TB),
               "p2p tile: staged bodies beyond the tile buffer");
     const unsigned bytes = static_cast<unsigned>(tt.off[idx + 1] - o0) * 16u;
     bulk_g2s(buf + o0, bodyf + tt.bb[idx], bytes, bar);
-    if (prec) bulk_g2s(buf + kHalfTile + o0, bodyl + tt.bb[idx], bytes, bar);
+    if (prec) bulk_g2s(buf + TB / 2 + o0, bodyl + tt.bb[idx], bytes, bar);
   }
 }
 
@@ -343,9 +344,10 @@ __device__ __forceinline__ void tile_compute(const float4* __restrict__ buf, int
   A.fold(ph, ax, ay, az, kAcc);
 }
 
-template <bool kAcc, bool kGuard>
+template <bool kAcc, bool kGuard, int TB>
 __device__ __forceinline__ void tile_compute_prec(const float4* __restrict__ buf, int nb, int g, int G, const Tgt& T,
                                                   Acc64& A) {
+  constexpr int kHalf = TB / 2;  // hi in [0, half), lo in [half, 2 half)
   float2 ph = make_float2(0.f, 0.f), ax = ph, ay = ph, az = ph;
   const int chunk = ((nb + G - 1) / G) | 1;
   const float4* p = buf + g * chunk;
@@ -356,12 +358,12 @@ __device__ __forceinline__ void tile_compute_prec(const float4* __restrict__ buf
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       sh[u] = p[u];
-      sl[u] = p[kHalfTile + u];
+      sl[u] = p[kHalf + u];
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) pair_body_prec<kAcc, kGuard>(sh[u], sl[u], T, ph, ax, ay, az);
   }
-  for (; p < end; ++p) pair_body_prec<kAcc, kGuard>(p[0], p[kHalfTile], T, ph, ax, ay, az);
+  for (; p < end; ++p) pair_body_prec<kAcc, kGuard>(p[0], p[kHalf], T, ph, ax, ay, az);
   A.fold(ph, ax, ay, az, kAcc);
 }
 
@@ -381,6 +383,17 @@ __device__ __forceinline__ void tile_compute_prec(const float4* __restrict__ buf
 // for each other inside the pipeline, so a warp that finishes its share of a tile early starts
 // on the next one (the producer runs up to one tile ahead: two buffers).
 constexpr int kWsThreads = kThreads + 32;
+#ifndef FMM_P2P_SMALL_SOURCES
+#define FMM_P2P_SMALL_SOURCES 2048.0
+#endif
+#ifndef FMM_P2P_SMALL_CT
+#define FMM_P2P_SMALL_CT 64
+#endif
+#ifndef FMM_P2P_SMALL_TB
+#define FMM_P2P_SMALL_TB 512
+#endif
+constexpr int kSmallCT = FMM_P2P_SMALL_CT, kSmallTB = FMM_P2P_SMALL_TB;
+constexpr double kSmallSourcesPerTarget = FMM_P2P_SMALL_SOURCES;  // mean P2P sources per target body below which the narrow CTAs run
 
 // Phase timestamps of sampled CTAs (variant builds only, tools/p2p_trace.py): clock64 at entry,
 // item loaded, producer tile-0 set up / copies issued / landed / published, producer done,
@@ -429,33 +442,43 @@ __device__ __forceinline__ void convert_warp(int lane, const TileTab& tt, float4
   }
 }
 
+template <int TB>
 __device__ __forceinline__ void convert_prec_warp(int lane, const TileTab& tt, float4* buf) {
+  constexpr int kHalf = TB / 2;
   const int nb = tt.off[tt.nseg];
   const int nseg = tt.nseg;
   int k = 0;
 #pragma unroll 1
   for (int j = lane; j < nb; j += 32) {
     while (k + 1 < nseg && tt.off[k + 1] <= j) ++k;  // j ascends: the entry index only moves forward
-    const float4 h = buf[j], l = buf[kHalfTile + j];
+    const float4 h = buf[j], l = buf[kHalf + j];
     const float2 x = two_sum(h.x, tt.sh[k][0]), y = two_sum(h.y, tt.sh[k][1]), z = two_sum(h.z, tt.sh[k][2]);
     buf[j] = make_float4(-x.x, -y.x, -z.x, h.w);
-    buf[kHalfTile + j] = make_float4(-((x.y + l.x) + tt.sl[k][0]), -((y.y + l.y) + tt.sl[k][1]),
+    buf[kHalf + j] = make_float4(-((x.y + l.x) + tt.sl[k][0]), -((y.y + l.y) + tt.sl[k][1]),
                                      -((z.y + l.z) + tt.sl[k][2]), 0.f);
   }
 }
 
-template <bool kAcc>
-__global__ void __launch_bounds__(kWsThreads, FMM_P2P_MIN_BLOCKS)
+// CT consumer threads (two targets each: up to 2 CT... an item holds at most kThreads = 128 targets,
+// so CT = 64 threads loop twice over the final write) and TB bodies per tile. The small variant
+// (CT = 64, TB = 512: 96 threads, ~20 KB) runs 10 CTAs/SM on small-leaf trees, where an item is
+// ~3 tiles and a CTA spends a third of its life in the start-up chain of its first tile
+// (profiles/r2_p2p_phase_trace.txt): more, narrower CTAs keep more of them in their pair loops.
+#ifndef FMM_P2P_MIN_BLOCKS_SMALL
+#define FMM_P2P_MIN_BLOCKS_SMALL 10
+#endif
+template <bool kAcc, int CT, int TB>
+__global__ void __launch_bounds__(CT + 32, CT == kThreads ? FMM_P2P_MIN_BLOCKS : FMM_P2P_MIN_BLOCKS_SMALL)
 k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent, const float4* __restrict__ bodyf,
               const float4* __restrict__ bodyl, double* __restrict__ phi_out, double* __restrict__ acc_out,
               double* __restrict__ partial) {
-  __shared__ __align__(16) float4 sS[2][kTileBodies];
+  __shared__ __align__(16) float4 sS[2][TB];
   __shared__ TileTab tabs[2];
   __shared__ __align__(8) uint64_t full[2], tmab[2], empty[2];
 
 #if FMM_P2P_TRACE
   unsigned long long* trace = nullptr;
-  if ((threadIdx.x == 0 || threadIdx.x == kThreads) && blockIdx.x % kTraceStride == 0 &&
+  if ((threadIdx.x == 0 || threadIdx.x == CT) && blockIdx.x % kTraceStride == 0 &&
       blockIdx.x / kTraceStride < kTraceCtas)
     trace = g_p2p_trace + (blockIdx.x / kTraceStride) * 16;
   if (threadIdx.x == 0) P2P_TR(0);
@@ -466,27 +489,27 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
     for (int b = 0; b < 2; ++b) {
       mbar_init(&full[b], 1);
       mbar_init(&tmab[b], 1);
-      mbar_init(&empty[b], kThreads / 32);
+      mbar_init(&empty[b], CT / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   if (tid == 0) P2P_TR(1);
 
-  if (tid >= kThreads) {  // ---- producer warp
+  if (tid >= CT) {  // ---- producer warp
     int32_t cursor = it.lb, off = 0;
     unsigned k = 0;
     for (; cursor < it.le; ++k) {
       const int b = k & 1;
       if (k >= 2) mbar_wait(&empty[b], ((k >> 1) - 1) & 1u);
-      tile_setup_ent(lane, it.le, cursor, off, ent + cursor, tabs[b]);
+      tile_setup_ent<TB>(lane, it.le, cursor, off, ent + cursor, tabs[b]);
       __syncwarp();
       if (k == 0) P2P_TR(2);
-      tile_tma(lane, tabs[b], bodyf, bodyl, sS[b], &tmab[b]);
+      tile_tma<TB>(lane, tabs[b], bodyf, bodyl, sS[b], &tmab[b]);
       if (k == 0) P2P_TR(3);
       mbar_wait(&tmab[b], (k >> 1) & 1u);
       if (k == 0) P2P_TR(4);
-      if (tabs[b].prec) convert_prec_warp(lane, tabs[b], sS[b]);
+      if (tabs[b].prec) convert_prec_warp<TB>(lane, tabs[b], sS[b]);
       else convert_warp(lane, tabs[b], sS[b]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[b]);
@@ -504,7 +527,7 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
   FMM_CHECK(it.tb >= 0 && nt >= 1 && nt <= kThreads && it.te <= FMM_LIM(nbodies), "k_p2p_fp32_ws: target range");
   FMM_CHECK(it.lb >= 0 && it.lb <= it.le && it.le <= FMM_LIM(n_p2p), "k_p2p_fp32_ws: list range");
   const int slots = (nt + 1) >> 1;
-  const int G = kThreads / slots;
+  const int G = CT / slots;
   const int g = tid / slots, t = tid - g * slots;
   const bool active = g < G;
   Tgt T;
@@ -534,9 +557,9 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
         if (!prec)
           tile_compute<kAcc>(sS[b], nb, g, G, T, A);
         else if (guard)
-          tile_compute_prec<kAcc, true>(sS[b], nb, g, G, T, A);
+          tile_compute_prec<kAcc, true, TB>(sS[b], nb, g, G, T, A);
         else
-          tile_compute_prec<kAcc, false>(sS[b], nb, g, G, T, A);
+          tile_compute_prec<kAcc, false, TB>(sS[b], nb, g, G, T, A);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[b]);
@@ -547,16 +570,16 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
   P2P_TRV(11, static_cast<unsigned long long>(nt));
   // reduce the G lane groups in fixed order (reusing the tile buffer: the producer is done and
   // every consumer has released its last tile once this named barrier completes) and write
-  asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads) : "memory");
+  asm volatile("bar.sync 1, %0;\n" ::"r"(CT) : "memory");
   double* red = reinterpret_cast<double*>(sS);  // [G][slots][2 targets][4]
   if (active) {
     double* r = red + 8 * (g * slots + t);
     r[0] = A.ph0; r[1] = A.ax0; r[2] = A.ay0; r[3] = A.az0;
     r[4] = A.ph1; r[5] = A.ax1; r[6] = A.ay1; r[7] = A.az1;
   }
-  asm volatile("bar.sync 1, %0;\n" ::"r"(kThreads) : "memory");
-  if (tid < nt) {
-    const int sl = tid >> 1, h = tid & 1;
+  asm volatile("bar.sync 1, %0;\n" ::"r"(CT) : "memory");
+  for (int tt = tid; tt < nt; tt += CT) {
+    const int sl = tt >> 1, h = tt & 1;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     for (int gg = 0; gg < G; ++gg) {
       const double* r = red + 8 * (gg * slots + sl) + 4 * h;
@@ -566,7 +589,7 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
       v[3] += r[3];
     }
     if (it.pbase < 0) {
-      const int32_t i = it.tb + tid;
+      const int32_t i = it.tb + tt;
       phi_out[i] = v[0];
       if (kAcc) {
         acc_out[3 * i] = v[1];
@@ -574,7 +597,7 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
         acc_out[3 * i + 2] = v[3];
       }
     } else {
-      double* p = partial + 4 * ((int64_t)it.pbase + tid);
+      double* p = partial + 4 * ((int64_t)it.pbase + tt);
       p[0] = v[0];
       p[1] = v[1];
       p[2] = v[2];
@@ -1098,12 +1121,26 @@ void run_p2p(fmm_ctx* c, cudaStream_t s) {
   if (c->n_p2p_items > 0) {
     if (c->cfg.precision == FMM_PREC_FP32_P2P) {
       const P2PEnt* ent = reinterpret_cast<const P2PEnt*>(c->p2p_ent.p);
-      if (wa)
-        k_p2p_fp32_ws<true><<<(unsigned)c->n_p2p_items, kWsThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p, phi,
-                                                                            acc, c->p2p_partial.p);
-      else
-        k_p2p_fp32_ws<false><<<(unsigned)c->n_p2p_items, kWsThreads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p, phi,
-                                                                             acc, c->p2p_partial.p);
+      // narrow CTAs (64 consumer threads, 512-body tiles, 10 per SM) when the items are short
+      // (A/B: C5 4.90 -> 4.46 ms; C3 3.73 -> 4.08, C2 2.78 -> 3.06: wide there); fmm_set_p2p_shape or
+      // FMM_P2P_SMALL=0/1 override the choice
+      static const int small_env = [] {
+        const char* e = getenv("FMM_P2P_SMALL");
+        return e ? atoi(e) : -1;
+      }();
+      // few source bodies per target body = items of ~3 tiles (C5: 1 450; C1-C4: 3 300-17 000)
+      const double targets = static_cast<double>(c->world > 1 ? c->shard_b1 - c->shard_b0 : n);
+      const bool small =
+          c->p2p_shape >= 0 ? c->p2p_shape != 0
+          : small_env >= 0 ? small_env != 0
+                           : static_cast<double>(c->p2p_body_pairs) < kSmallSourcesPerTarget * targets;
+      auto launch = [&](auto kern, int threads) {
+        kern<<<(unsigned)c->n_p2p_items, threads, 0, s>>>(items, ent, c->bodyf.p, c->bodyl.p, phi, acc, c->p2p_partial.p);
+      };
+      if (wa && small) launch(k_p2p_fp32_ws<true, kSmallCT, kSmallTB>, kSmallCT + 32);
+      else if (wa) launch(k_p2p_fp32_ws<true, kThreads, kTileBodies>, kWsThreads);
+      else if (small) launch(k_p2p_fp32_ws<false, kSmallCT, kSmallTB>, kSmallCT + 32);
+      else launch(k_p2p_fp32_ws<false, kThreads, kTileBodies>, kWsThreads);
     } else {
       k_p2p_fp64<<<(unsigned)c->n_p2p_items, kThreads, 0, s>>>(items, c->p2p_src.p, c->c_body_begin.p, c->c_body_end.p,
                                                               c->bodies.p, phi, acc, c->p2p_partial.p, wa);

@@ -177,6 +177,10 @@ class Context:
         small initial buffer capacity so the overflow regrow path runs."""
         self._c(self.lib.fmm_set_traversal_debug(self.h, int(force_keys64), int(initial_capacity)))
 
+    def set_p2p_shape(self, shape: int = -1):
+        """Test / tuning hook (fmm_set_p2p_shape): 0 wide, 1 narrow FP32 P2P CTAs, -1 automatic."""
+        self._c(self.lib.fmm_set_p2p_shape(self.h, int(shape)))
+
     def traversal_regrows(self) -> int:
         r = C.c_int(0)
         self._c(self.lib.fmm_get_traversal_regrows(self.h, C.byref(r)))

@@ -428,8 +428,9 @@ def test_stage_isolated_m2l_and_p2p(fmmlib, orc, gen, n, p):
     assert rel_l2(phi, t.phi()) < 1e-12 and rel_l2(acc, t.acc()) < 1e-12
 
 
-@pytest.mark.parametrize("precision,tol", [("fp64", 1e-13), ("fp32", 1e-6)])
-def test_stage_isolated_p2p_kernel(fmmlib, orc, precision, tol):
+@pytest.mark.parametrize("precision,tol,shape", [("fp64", 1e-13, -1), ("fp32", 1e-6, 0), ("fp32", 1e-6, 1)],
+                         ids=["fp64", "fp32-wide", "fp32-narrow"])
+def test_stage_isolated_p2p_kernel(fmmlib, orc, precision, tol, shape):
     """The production P2P kernels alone (k_p2p_fp64 / k_p2p_fp32_ws) on injected tree and lists
     against the oracle's P2P (kernels.cpp:181-192 + gradient) applied over the same list: the
     locals are zero, so the downward pass adds nothing. FP64 mode differs from the reference's
@@ -440,6 +441,7 @@ def test_stage_isolated_p2p_kernel(fmmlib, orc, precision, tol):
     m, pp = orc.traverse(t, 0.5)
     orc.apply_lists(t, np.zeros((0, 2), np.int32), pp)
     ctx = fmmlib.Context(order=4, n_crit=64, theta=0.5, precision=precision)
+    ctx.set_p2p_shape(shape)  # FP32: both CTA shapes of k_p2p_fp32_ws (the choice is automatic otherwise)
     ctx.set_bodies(bodies)
     ctx.load_tree({k: getattr(c, k) for k in CELL_KEYS}, t.perm())
     ctx.load_lists(m, pp)
