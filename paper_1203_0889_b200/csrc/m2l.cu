@@ -101,6 +101,7 @@ __device__ __forceinline__ void stage_runs(int lane, bool valid, int nv, int32_t
   if (head) {
     const unsigned above = (heads >> 1) >> lane;  // run heads above this lane
     const int next = above ? lane + __ffs(above) : nv;
+    FMM_CHECK(next > lane && next <= 32 && s >= 0 && s + (next - lane) <= FMM_LIM(ncells), "stage_runs: run of source rows");
     bulk_g2s(rows + lane * S, Mt + (int64_t)s * S, static_cast<unsigned>(next - lane) * S * 8u, bar);
   }
 }
@@ -345,6 +346,7 @@ __device__ __forceinline__ void expand_rows(const int32_t* __restrict__ targets,
       double v = 0.0;
 #pragma unroll
       for (int j = 0; j < K; ++j) v = fma(w[j], rw[idx[j]], v);
+      FMM_CHECK(targets[r] >= 0 && targets[r] < FMM_LIM(ncells), "k_m2l_expand: target index");
       L[(int64_t)targets[r] * N + i] += v;
     }
   }
@@ -1028,6 +1030,7 @@ k_m2l_flat(const int4* __restrict__ meta, int64_t nwarps, int K, int64_t npairs,
     }
     const unsigned heads = static_cast<unsigned>(mt.y);
     const int r_lane = mt.x + __popc(heads & (0xffffffffu >> (31 - lane))) - 1;
+    FMM_CHECK((heads & 1u) && mt.x >= 0 && r_lane < FMM_LIM(ncells), "k_m2l_flat: chunk metadata / target rank");
     const double4 ct = tcr[r_lane];
     const double4 cs = valid ? cr[s] : ct;
     double rx = 1.0, ry = 0.0, rz = 0.0;
