@@ -102,6 +102,17 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+#ifndef FMM_TRAV_PACKED_LB
+#define FMM_TRAV_PACKED_LB 1
+#endif
+// 16-byte relaxed loads / stores of an aligned {u64, u64} (a single transaction: the two halves
+// are always observed together, as CUB's decoupled look-back tile status relies on)
+__device__ __forceinline__ void ld_relaxed16(const ulonglong2* p, unsigned long long& x, unsigned long long& y) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];\n" : "=l"(x), "=l"(y) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_relaxed16(ulonglong2* p, unsigned long long x, unsigned long long y) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};\n" ::"l"(p), "l"(x), "l"(y) : "memory");
+}
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
@@ -181,6 +192,43 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
       const unsigned long long a01 = (tot_b & 0x1fffffull) | (((tot_b >> 21) & 0x1fffffull) << 32);
       const unsigned long long a2 = tot_b >> 42;
       unsigned long long p01 = 0, p2 = 0;
+#if FMM_TRAV_PACKED_LB
+      // One 16-byte word per chunk, {M2L | P2P << 32, children | state << 40}, read and written
+      // whole: a hop of the look-back is ONE load per lane (the state tags the values it travels
+      // with), where separate flag and value arrays cost two dependent L2 round trips per hop;
+      // the first wave of a large level resolves its ~1 200 chunks 32 per hop.
+      ulonglong2* lb = reinterpret_cast<ulonglong2*>(lb_val);
+      const unsigned long long t_agg = f_agg & 0xffffffu, t_inc = f_inc & 0xffffffu;
+      if (ch > 0) {
+        if (lane == 0) st_relaxed16(&lb[ch], a01, a2 | (t_agg << 40));
+        for (int64_t top = ch - 1;; top -= 32) {
+          const int64_t j = top - lane;
+          unsigned long long x = 0, y = t_inc << 40;  // lanes before chunk 0: an empty inclusive prefix
+          if (j >= 0) {
+            do {
+              ld_relaxed16(&lb[j], x, y);
+            } while ((y >> 40) != t_agg && (y >> 40) != t_inc);
+          }
+          const unsigned inc = __ballot_sync(0xffffffffu, (y >> 40) == t_inc);
+          const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest lane holding an inclusive prefix
+          unsigned long long v01 = 0, v2 = 0;
+          if (j >= 0 && lane <= stop) {
+            v01 = x;
+            v2 = y & 0xffffffffffull;
+          }
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) {
+            v01 += __shfl_xor_sync(0xffffffffu, v01, d);
+            v2 += __shfl_xor_sync(0xffffffffu, v2, d);
+          }
+          p01 += v01;
+          p2 += v2;
+          if (inc) break;
+        }
+      }
+      if (lane == 0) {
+        st_relaxed16(&lb[ch], p01 + a01, (p2 + a2) | (t_inc << 40));
+#else
       if (ch > 0) {
         if (lane == 0) {
           lb_val[4 * ch + 0] = a01;
@@ -217,6 +265,7 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
         lb_val[4 * ch + 2] = p01 + a01;
         lb_val[4 * ch + 3] = p2 + a2;
         st_release(&lb_flag[ch], f_inc);
+#endif
         sbase[0] = base_m + (p01 & 0xffffffffull);
         sbase[1] = base_p + (p01 >> 32);
         sbase[2] = p2;
@@ -502,7 +551,16 @@ void traverse(fmm_ctx* c) {
       c->lb_flag.ensure(nchunk);
       CK(cudaMemsetAsync(c->lb_flag.p, 0, sizeof(uint32_t) * c->lb_flag.cap, s));
     }
+    // the packed words carry a 24-bit state (2 * epoch + {0, 1}): zeroed on (re)allocation and
+    // when the epoch counter would wrap within this traversal
+    const bool lb_grow = c->lb_val.cap < static_cast<size_t>(4 * nchunk);
     unsigned long long* lbv = reinterpret_cast<unsigned long long*>(c->lb_val.ensure(4 * nchunk));
+    const bool lb_wrap = ((c->trav_epoch + nlev + 2) & 0x7fffffu) < static_cast<uint32_t>(nlev + 2);
+    if (lb_grow || lb_wrap) {
+      CK(cudaMemsetAsync(lbv, 0, sizeof(unsigned long long) * c->lb_val.cap, s));
+      CK(cudaMemsetAsync(c->lb_flag.p, 0, sizeof(uint32_t) * c->lb_flag.cap, s));
+      if (lb_wrap) c->trav_epoch = 0;  // the epochs of this traversal are 1 .. nlev: never state 0
+    }
     const unsigned long long one = 1;
     CK(cudaMemcpyAsync(ctr + 4, &one, sizeof(one), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(c->pairs_a.p, &root, sizeof(int2), cudaMemcpyHostToDevice, s));
