@@ -63,14 +63,16 @@ __device__ __forceinline__ void classify(const int2 pr, const double4* __restric
 // M2L or P2P key or pushes its child pairs to level L+1. The launch does not know the frontier
 // size: it reads it from the level counters written by the previous launch, so all levels are
 // queued back to back without a host round trip. A persistent grid takes chunks of pairs in
-// ticket order. With 64-bit keys (more than 2^16 cells, or mutual mode) each chunk's output
-// offsets come from a chained (decoupled look-back, warp-wide) scan over the chunks of the level,
-// so the emission order is a pure function of the frontier order: deterministic, level by level,
-// and the lists only need a STABLE sort on the target bits to become deterministic CSR (3
-// instead of 5 radix passes at C3-C5). With 32-bit keys the slots are reserved by one atomic per
-// chunk and counter, and the full (target, source) sort canonicalises the lists (cheaper at C2:
-// 4 passes of 4-byte keys against the look-back's latency). Output that would exceed a buffer's
-// capacity is dropped and flagged; the host then grows the buffers and reruns the traversal.
+// ticket order. Each chunk's output offsets come from a chained (decoupled look-back, warp-wide)
+// scan over the chunks of the level, so the emission order is a pure function of the frontier
+// order: deterministic, level by level, and the lists only need a STABLE sort on the target bits
+// to become deterministic CSR (64-bit keys, more than 2^16 cells or mutual mode: 3 instead of 5
+// radix passes; 32-bit keys: 2 instead of 4). The look-back state of a chunk is one 16-byte word
+// (values and state together), so a hop is one load. FMM_TRAV_ORDERED32/64 = 0 select the older
+// scheme instead: slots reserved by one atomic per chunk and counter and a full (target, source)
+// sort (it was the cheaper one for 32-bit keys while a hop cost two dependent loads: C2 traversal
+// 1.11 against 1.03 ms now). Output that would exceed a buffer's capacity is dropped and flagged;
+// the host then grows the buffers and reruns the traversal.
 // Counters (ctr): [0] M2L total, [1] P2P total, [2] overflow flag, [4 + L] frontier size of
 // level L (level 0 = the root pair), [64 + L] chunk tickets of level L.
 constexpr int kStepThreads = 256;
@@ -81,6 +83,9 @@ constexpr int kStepThreads = 256;
 // 4/8 pairs at 4-5 CTAs/SM)
 #ifndef FMM_TRAV_ORDERED64  // 64-bit keys: ordered look-back emission (1) or atomic slots + full sort (0)
 #define FMM_TRAV_ORDERED64 1
+#endif
+#ifndef FMM_TRAV_ORDERED32  // 32-bit keys: ordered look-back emission + target-only sort (1) or atomic slots + full sort (0)
+#define FMM_TRAV_ORDERED32 1
 #endif
 #ifndef FMM_STEP_PER64
 #define FMM_STEP_PER64 4
@@ -129,7 +134,7 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
   // 64-bit keys (more than 2^16 cells, or mutual mode): ordered emission by look-back, and the
   // lists only need a stable sort on the target bits; 32-bit keys: atomic slot reservation (the
   // full (target, source) sort canonicalises them; measured cheaper at C2)
-  constexpr bool kOrdered = sizeof(KeyT) == 8 && FMM_TRAV_ORDERED64;
+  constexpr bool kOrdered = sizeof(KeyT) == 8 ? FMM_TRAV_ORDERED64 != 0 : FMM_TRAV_ORDERED32 != 0;
   constexpr int kStepPer = step_per<KeyT>();
   constexpr int kStepChunk = step_chunk<KeyT>();
   __shared__ typename Scan::TempStorage scan_tmp;
@@ -412,7 +417,7 @@ void keys_to_csr(fmm_ctx* c, KeyT* keys, int64_t n, DBuf<int64_t>& off, DBuf<int
   size_t sb = 0;
   // 64-bit keys come in a deterministic order (ordered emission / given pairs): a stable sort on
   // the target bits keeps it within each target; 32-bit keys: the full (target, source) sort
-  const int b0 = (sizeof(KeyT) == 8 && FMM_TRAV_ORDERED64) ? sbits : 0;
+  const int b0 = (sizeof(KeyT) == 8 ? FMM_TRAV_ORDERED64 != 0 : FMM_TRAV_ORDERED32 != 0) ? sbits : 0;
   CK(cub::DeviceRadixSort::SortKeys(nullptr, sb, keys, kb, (int)n, b0, 2 * sbits, s));
   CK(cub::DeviceRadixSort::SortKeys(p2p_path ? temp_storage2(c, sb) : temp_storage(c, sb), sb, keys, kb, (int)n, b0,
                                     2 * sbits, s));
