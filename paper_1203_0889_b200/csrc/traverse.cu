@@ -76,11 +76,11 @@ __device__ __forceinline__ void classify(const int2 pr, const double4* __restric
 // Counters (ctr): [0] M2L total, [1] P2P total, [2] overflow flag, [4 + L] frontier size of
 // level L (level 0 = the root pair), [64 + L] chunk tickets of level L.
 constexpr int kStepThreads = 256;
-// pairs per thread: 2 with atomic slot reservation (32-bit keys), 4 with the ordered look-back
-// (larger chunks amortise the look-back); 8 CTAs of 256 threads per SM. The kernel is latency
-// bound (ncu at C3: issue 25 %, L2 50 % hit, ~30 cycles per issued instruction), so occupancy
-// beats the register spill this costs (tools/trav_ab.sh: traversal C2 -5 %, C5 -4 % against
-// 4/8 pairs at 4-5 CTAs/SM)
+// pairs per thread: 2 (512-pair chunks; with the one-load look-back hop larger chunks no longer
+// pay: 4 pairs per thread C3 traversal 2.89 ms, 2 -> 2.80, 1 -> 3.09); 8 CTAs of 256 threads per
+// SM: the kernel is latency bound (ncu at C3's heavy levels: issue 32-40 %, stalls: the CTA barrier
+// behind the look-back warp ~40 %, cell / spill loads ~40 %), so occupancy beats the register
+// spill it costs (tools/trav_ab.sh: 6 / 5 / 4 CTAs/SM are within +-2 % at C3 / C5 and 3-18 % slower at C2)
 #ifndef FMM_TRAV_ORDERED64  // 64-bit keys: ordered look-back emission (1) or atomic slots + full sort (0)
 #define FMM_TRAV_ORDERED64 1
 #endif
@@ -88,7 +88,7 @@ constexpr int kStepThreads = 256;
 #define FMM_TRAV_ORDERED32 1
 #endif
 #ifndef FMM_STEP_PER64
-#define FMM_STEP_PER64 4
+#define FMM_STEP_PER64 2
 #endif
 #ifndef FMM_STEP_PER32
 #define FMM_STEP_PER32 2

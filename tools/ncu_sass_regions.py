@@ -6,7 +6,13 @@ import csv, sys
 from collections import Counter
 rows = list(csv.reader(open(sys.argv[1])))
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 200
-hdr = rows[1]; data = [r for r in rows[2:] if len(r) == len(hdr)]
+hdr = rows[1]
+data = []
+for r in rows[2:]:  # first kernel only: a report with several launches repeats the two header rows
+    if r and r[0] == "Kernel Name":
+        break
+    if len(r) == len(hdr):
+        data.append(r)
 c = {h: i for i, h in enumerate(hdr)}
 iE, iS = c["Instructions Executed"], c["Warp Stall Sampling (All Samples)"]
 reasons = [h for h in hdr if h.startswith("stall_") and "Not" not in h]
