@@ -578,7 +578,8 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
     r[4] = A.ph1; r[5] = A.ax1; r[6] = A.ay1; r[7] = A.az1;
   }
   asm volatile("bar.sync 1, %0;\n" ::"r"(CT) : "memory");
-  for (int tt = tid; tt < nt; tt += CT) {
+  // one pass when CT = kThreads (an item holds at most kThreads targets), two for the narrow shape
+  auto write_target = [&](int tt) {
     const int sl = tt >> 1, h = tt & 1;
     double v[4] = {0.0, 0.0, 0.0, 0.0};
     for (int gg = 0; gg < G; ++gg) {
@@ -603,6 +604,11 @@ k_p2p_fp32_ws(const P2PItem* __restrict__ items, const P2PEnt* __restrict__ ent,
       p[2] = v[2];
       p[3] = v[3];
     }
+  };
+  if constexpr (CT >= kThreads) {
+    if (tid < nt) write_target(tid);
+  } else {
+    for (int tt = tid; tt < nt; tt += CT) write_target(tt);
   }
   if (tid == 0) P2P_TR(9);
 }
