@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 
 #include "context.cuh"
+#include "tma.cuh"
 
 namespace fmmb {
 namespace {
@@ -122,6 +123,84 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
 
+// One frontier pair: load, classify, (sharded) filter the kept target children; returns the packed
+// per-pair counts M2L (bits 0..20) | P2P (21..41) | children (42..63)
+__device__ __forceinline__ unsigned long long step_classify(bool in_range, const int2* __restrict__ fr, int64_t i,
+                                                            const double4* __restrict__ cr,
+                                                            const int32_t* __restrict__ cc,
+                                                            const int32_t* __restrict__ cb, double theta, double theta2,
+                                                            int mutual, int filter, const int32_t* __restrict__ bb,
+                                                            const int32_t* __restrict__ be, int32_t tb0, int32_t tb1,
+                                                            int2& pr, int& kind, int& nch) {
+  kind = -1;
+  nch = 0;
+  pr = make_int2(0, 0);
+  if (!in_range) return 0ull;
+  pr = fr[i];
+  FMM_CHECK(pr.x >= 0 && pr.x < FMM_LIM(ncells) && pr.y >= 0 && pr.y < FMM_LIM(ncells),
+            "k_step: frontier pair outside the cell array");
+  classify(pr, cr, cc, theta, theta2, mutual, kind, nch);
+  if (filter && kind == 2) {  // sharded: keep only target children meeting [tb0, tb1)
+    const int32_t b = cb[pr.x];
+    int kept = 0;
+    for (int q = 0; q < nch; ++q) kept += (bb[b + q] < tb1 && be[b + q] > tb0) ? 1 : 0;
+    nch = kept;
+  }
+  return kind == 0 ? 1ull : kind == 1 ? (1ull << 21) : (static_cast<unsigned long long>(nch) << 42);
+}
+
+// Emits one classified pair at the running offsets (om, op, oc), which it advances; returns true
+// if an output would pass its buffer's capacity (dropped; the run is then flagged and repeated).
+template <class KeyT>
+__device__ __forceinline__ bool step_scatter(const int2 pr, int kind, int nch, int64_t& om, int64_t& op, int64_t& oc,
+                                             int sbits, KeyT* __restrict__ m2l_keys, KeyT* __restrict__ p2p_keys,
+                                             int2* __restrict__ next, int64_t cap_m, int64_t cap_p, int64_t cap_f,
+                                             const int32_t* __restrict__ cb, const int32_t* __restrict__ cc, int filter,
+                                             const int32_t* __restrict__ bb, const int32_t* __restrict__ be, int32_t tb0,
+                                             int32_t tb1) {
+  bool over = false;
+  const KeyT key = static_cast<KeyT>(((uint64_t)(uint32_t)pr.x << sbits) | (uint32_t)pr.y);
+  if (kind == 0) {
+    if (om < cap_m) m2l_keys[om] = key; else over = true;
+    ++om;
+  } else if (kind == 1) {
+    if (op < cap_p) p2p_keys[op] = key; else over = true;
+    ++op;
+  } else if (kind >= 2) {
+    // children past the frontier capacity are dropped (and the run flagged), but every slot
+    // below the capacity is written, so a truncated frontier still holds only valid pairs
+    if (oc + nch > cap_f) over = true;
+    if (kind == 2) {
+      const int32_t b = cb[pr.x];
+      if (filter) {
+        int64_t q = oc;
+        for (int k = 0; k < cc[pr.x]; ++k)
+          if (bb[b + k] < tb1 && be[b + k] > tb0) {
+            if (q < cap_f) next[q] = make_int2(b + k, pr.y);
+            ++q;
+          }
+      } else {
+        for (int k = 0; k < nch; ++k)
+          if (oc + k < cap_f) next[oc + k] = make_int2(b + k, pr.y);
+      }
+    } else if (kind == 3) {
+      const int32_t b = cb[pr.y];
+      for (int k = 0; k < nch; ++k)
+        if (oc + k < cap_f) next[oc + k] = make_int2(pr.x, b + k);
+    } else {
+      const int32_t b = cb[pr.x], m = cc[pr.x];
+      int64_t q = oc;
+      for (int a = 0; a < m; ++a)
+        for (int c = a; c < m; ++c) {
+          if (q < cap_f) next[q] = make_int2(b + a, b + c);
+          ++q;
+        }
+    }
+    oc += nch;
+  }
+  return over;
+}
+
 template <class KeyT>
 __global__ void __launch_bounds__(kStepThreads, FMM_STEP_MINB)
 k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, const int32_t* __restrict__ cc,
@@ -162,22 +241,8 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
 #pragma unroll
     for (int j = 0; j < kStepPer; ++j) {
       const int64_t i = c0 + j * kStepThreads + threadIdx.x;
-      kind[j] = -1;
-      nch[j] = 0;
-      pr[j] = make_int2(0, 0);
-      if (i < n) {
-        pr[j] = fr[i];
-        FMM_CHECK(pr[j].x >= 0 && pr[j].x < FMM_LIM(ncells) && pr[j].y >= 0 && pr[j].y < FMM_LIM(ncells),
-                  "k_step: frontier pair outside the cell array");
-        classify(pr[j], cr, cc, theta, theta2, mutual, kind[j], nch[j]);
-        if (filter && kind[j] == 2) {  // sharded: keep only target children meeting [tb0, tb1)
-          const int32_t b = cb[pr[j].x];
-          int kept = 0;
-          for (int q = 0; q < nch[j]; ++q) kept += (bb[b + q] < tb1 && be[b + q] > tb0) ? 1 : 0;
-          nch[j] = kept;
-        }
-        mine += kind[j] == 0 ? 1ull : kind[j] == 1 ? (1ull << 21) : (static_cast<unsigned long long>(nch[j]) << 42);
-      }
+      mine += step_classify(i < n, fr, i, cr, cc, cb, theta, theta2, mutual, filter, bb, be, tb0, tb1, pr[j], kind[j],
+                            nch[j]);
     }
     unsigned long long excl, tot;
     Scan(scan_tmp).ExclusiveSum(mine, excl, tot);
@@ -288,50 +353,195 @@ k_step(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, c
     int64_t oc = static_cast<int64_t>(sbase[2] + (excl >> 42));
     bool over = false;
 #pragma unroll
-    for (int j = 0; j < kStepPer; ++j) {
-      const KeyT key = static_cast<KeyT>(((uint64_t)(uint32_t)pr[j].x << sbits) | (uint32_t)pr[j].y);
-      if (kind[j] == 0) {
-        if (om < cap_m) m2l_keys[om] = key; else over = true;
-        ++om;
-      } else if (kind[j] == 1) {
-        if (op < cap_p) p2p_keys[op] = key; else over = true;
-        ++op;
-      } else if (kind[j] >= 2) {
-        // children past the frontier capacity are dropped (and the run flagged), but every slot
-        // below the capacity is written, so a truncated frontier still holds only valid pairs
-        if (oc + nch[j] > cap_f) over = true;
-        if (kind[j] == 2) {
-          const int32_t b = cb[pr[j].x];
-          if (filter) {
-            int64_t q = oc;
-            for (int k = 0; k < cc[pr[j].x]; ++k)
-              if (bb[b + k] < tb1 && be[b + k] > tb0) {
-                if (q < cap_f) next[q] = make_int2(b + k, pr[j].y);
-                ++q;
-              }
-          } else {
-            for (int k = 0; k < nch[j]; ++k)
-              if (oc + k < cap_f) next[oc + k] = make_int2(b + k, pr[j].y);
-          }
-        } else if (kind[j] == 3) {
-          const int32_t b = cb[pr[j].y];
-          for (int k = 0; k < nch[j]; ++k)
-            if (oc + k < cap_f) next[oc + k] = make_int2(pr[j].x, b + k);
-        } else {
-          const int32_t b = cb[pr[j].x], m = cc[pr[j].x];
-          int64_t q = oc;
-          for (int a = 0; a < m; ++a)
-            for (int c = a; c < m; ++c) {
-              if (q < cap_f) next[q] = make_int2(b + a, b + c);
-              ++q;
-            }
-        }
-        oc += nch[j];
-      }
-    }
+    for (int j = 0; j < kStepPer; ++j)
+      over |= step_scatter<KeyT>(pr[j], kind[j], nch[j], om, op, oc, sbits, m2l_keys, p2p_keys, next, cap_m, cap_p, cap_f,
+                                 cb, cc, filter, bb, be, tb0, tb1);
     if (over) ctr[2] = 1ull;
     __syncthreads();  // sbase / scan storage / s_chunk reuse
   }
+}
+
+
+// Pipelined frontier step (ordered emission only): eight worker warps and one RESOLVER warp per
+// CTA. The workers classify chunk k into a shared-memory stage, scan their counts and hand the
+// chunk total to the resolver, which runs the look-back for chunk k while the workers classify
+// chunk k + 1; the workers then scatter chunk k from its stage. In k_step all eight warps wait at
+// a CTA barrier behind the look-back warp (ncu, C3's heavy levels: ~40 % of the stall samples);
+// here the look-back of a chunk overlaps the next chunk's classification and still starts right
+// after the chunk's scan, so the prefixes of later chunks are not delayed. Two stages; mbarriers
+// scanned[s] (workers -> resolver) and resolved[s] (resolver -> workers); named barrier 1 among
+// the 256 worker threads.
+#ifndef FMM_STEP_PIPE
+#define FMM_STEP_PIPE 1
+#endif
+#ifndef FMM_STEP_PIPE_MINB
+#define FMM_STEP_PIPE_MINB 7
+#endif
+constexpr int kPipeWorkers = 256;
+constexpr int kPipeThreads = kPipeWorkers + 32;
+__device__ __forceinline__ void bar_workers() { asm volatile("bar.sync 1, %0;\n" ::"r"(kPipeWorkers) : "memory"); }
+
+template <class KeyT>
+__global__ void __launch_bounds__(kPipeThreads, FMM_STEP_PIPE_MINB)
+k_step_pipe(int level, const int2* __restrict__ fr, const double4* __restrict__ cr, const int32_t* __restrict__ cc,
+            const int32_t* __restrict__ cb, double theta, double theta2, int mutual, int sbits,
+            KeyT* __restrict__ m2l_keys, KeyT* __restrict__ p2p_keys, int2* __restrict__ next,
+            unsigned long long* __restrict__ ctr, int64_t cap_m, int64_t cap_p, int64_t cap_f,
+            const int32_t* __restrict__ bb, const int32_t* __restrict__ be, int32_t tb0, int32_t tb1, int filter,
+            uint32_t epoch, unsigned long long* __restrict__ lb_val) {
+  constexpr int kPer = step_per<KeyT>();
+  constexpr int kChunk = kPipeWorkers * kPer;
+  struct Stage {
+    int2 pr[kChunk];
+    int16_t kn[kChunk];                  // kind (low 4 bits, -1 -> 15) | children << 4
+    unsigned long long excl[kPipeWorkers];
+    unsigned long long tot;
+    long long ch;                        // ticket (workers)
+    long long rch;                       // chunk index for the resolver, -1 = no more chunks
+  };
+  __shared__ Stage st[2];
+  __shared__ unsigned long long sbase[2][3];
+  __shared__ unsigned long long wsum[kPipeWorkers / 32];
+  __shared__ __align__(8) uint64_t scanned[2], resolved[2];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t n = min(static_cast<int64_t>(ctr[4 + level]), cap_f);
+  const unsigned long long base_m = ctr[0], base_p = ctr[1];  // totals of the previous levels
+  if (static_cast<int64_t>(blockIdx.x) * kChunk >= n) return;
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&scanned[b], 1);
+      mbar_init(&resolved[b], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (tid >= kPipeWorkers) {  // ---- resolver warp
+    ulonglong2* lb = reinterpret_cast<ulonglong2*>(lb_val);
+    const unsigned long long t_agg = (2u * epoch) & 0xffffffu, t_inc = (2u * epoch + 1u) & 0xffffffu;
+    for (unsigned k = 0;; ++k) {
+      const int s = k & 1;
+      mbar_wait(&scanned[s], (k >> 1) & 1u);
+      const int64_t ch = st[s].rch;
+      if (ch < 0) return;
+      const unsigned long long tot = st[s].tot;
+      const unsigned long long a01 = (tot & 0x1fffffull) | (((tot >> 21) & 0x1fffffull) << 32);
+      const unsigned long long a2 = tot >> 42;
+      unsigned long long p01 = 0, p2 = 0;
+      if (ch > 0) {
+        if (lane == 0) st_relaxed16(&lb[ch], a01, a2 | (t_agg << 40));
+        for (int64_t top = ch - 1;; top -= 32) {
+          const int64_t j = top - lane;
+          unsigned long long x = 0, y = t_inc << 40;  // lanes before chunk 0: an empty inclusive prefix
+          if (j >= 0) {
+            do {
+              ld_relaxed16(&lb[j], x, y);
+            } while ((y >> 40) != t_agg && (y >> 40) != t_inc);
+          }
+          const unsigned inc = __ballot_sync(0xffffffffu, (y >> 40) == t_inc);
+          const int stop = inc ? __ffs(inc) - 1 : 31;
+          unsigned long long v01 = 0, v2 = 0;
+          if (j >= 0 && lane <= stop) {
+            v01 = x;
+            v2 = y & 0xffffffffffull;
+          }
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) {
+            v01 += __shfl_xor_sync(0xffffffffu, v01, d);
+            v2 += __shfl_xor_sync(0xffffffffu, v2, d);
+          }
+          p01 += v01;
+          p2 += v2;
+          if (inc) break;
+        }
+      }
+      if (lane == 0) {
+        st_relaxed16(&lb[ch], p01 + a01, (p2 + a2) | (t_inc << 40));
+        sbase[s][0] = base_m + (p01 & 0xffffffffull);
+        sbase[s][1] = base_p + (p01 >> 32);
+        sbase[s][2] = p2;
+        if (ch * kChunk + kChunk >= n) {  // the level's last chunk: totals for the next launch
+          const unsigned long long i01 = p01 + a01;
+          ctr[0] = base_m + (i01 & 0xffffffffull);
+          ctr[1] = base_p + (i01 >> 32);
+          ctr[4 + level + 1] = p2 + a2;
+        }
+        mbar_arrive(&resolved[s]);
+      }
+      __syncwarp();
+    }
+  }
+
+  // ---- worker warps
+  const int w = tid >> 5;
+  bool over = false, have_prev = false;
+  for (unsigned k = 0;; ++k) {
+    const int s = k & 1;
+    // stage s was scattered in iteration k - 1 (as chunk k - 2) and the barrier closed it
+    if (tid == 0) st[s].ch = static_cast<long long>(atomicAdd(&ctr[kTicketBase + level], 1ull));
+    bar_workers();
+    const int64_t ch = st[s].ch;
+    const int64_t c0 = ch * kChunk;
+    const bool active = c0 < n;  // uniform over the workers
+    if (active) {
+      unsigned long long mine = 0;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int64_t i = c0 + j * kPipeWorkers + tid;
+        int2 pr;
+        int kind, nch;
+        mine += step_classify(i < n, fr, i, cr, cc, cb, theta, theta2, mutual, filter, bb, be, tb0, tb1, pr, kind, nch);
+        st[s].pr[j * kPipeWorkers + tid] = pr;
+        st[s].kn[j * kPipeWorkers + tid] = static_cast<int16_t>((kind & 15) | (nch << 4));
+      }
+      // exclusive scan over the 256 workers: warp scan, warp totals through shared memory
+      unsigned long long incl = mine;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+      }
+      if (lane == 31) wsum[w] = incl;
+      bar_workers();
+      unsigned long long before = 0, total = 0;
+#pragma unroll
+      for (int q = 0; q < kPipeWorkers / 32; ++q) {
+        const unsigned long long v = wsum[q];
+        before += q < w ? v : 0ull;
+        total += v;
+      }
+      st[s].excl[tid] = before + incl - mine;
+      if (tid == 0) {
+        st[s].tot = total;
+        st[s].rch = ch;
+      }
+    } else if (tid == 0) {
+      st[s].rch = -1;  // tells the resolver to leave
+    }
+    bar_workers();  // the stage is complete (and wsum may be rewritten)
+    if (tid == 0) mbar_arrive(&scanned[s]);
+    if (have_prev) {  // scatter chunk k - 1 once its prefix is resolved
+      const int sp = s ^ 1;
+      mbar_wait(&resolved[sp], ((k - 1) >> 1) & 1u);
+      const unsigned long long excl = st[sp].excl[tid];
+      int64_t om = static_cast<int64_t>(sbase[sp][0] + (excl & 0x1fffffull));
+      int64_t op = static_cast<int64_t>(sbase[sp][1] + ((excl >> 21) & 0x1fffffull));
+      int64_t oc = static_cast<int64_t>(sbase[sp][2] + (excl >> 42));
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int2 pr = st[sp].pr[j * kPipeWorkers + tid];
+        const int kn = st[sp].kn[j * kPipeWorkers + tid];
+        int kind = kn & 15;
+        if (kind == 15) kind = -1;
+        over |= step_scatter<KeyT>(pr, kind, kn >> 4, om, op, oc, sbits, m2l_keys, p2p_keys, next, cap_m, cap_p, cap_f,
+                                   cb, cc, filter, bb, be, tb0, tb1);
+      }
+    }
+    if (!active) break;
+    have_prev = true;
+    bar_workers();  // every worker is done with stage s ^ 1 before the next iteration refills it
+  }
+  if (over) ctr[2] = 1ull;
 }
 
 template <class KeyT>
@@ -573,7 +783,19 @@ void traverse(fmm_ctx* c) {
       const int2* fr = (L & 1) ? c->pairs_d.p : c->pairs_a.p;
       int2* nx = (L & 1) ? c->pairs_a.p : c->pairs_d.p;
       const uint32_t epoch = ++c->trav_epoch;
-      if (small)
+      constexpr bool kPipe32 = FMM_STEP_PIPE && FMM_TRAV_ORDERED32, kPipe64 = FMM_STEP_PIPE && FMM_TRAV_ORDERED64;
+      const int pgrid = 148 * FMM_STEP_PIPE_MINB;
+      if (small && kPipe32)
+        k_step_pipe<<<pgrid, kPipeThreads, 0, s>>>(L, fr, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
+                                                   theta * theta, mutual, sbits, (uint32_t*)c->m2l_keys.p,
+                                                   (uint32_t*)c->p2p_keys.p, nx, ctr, cap_m, cap_p, cap_f,
+                                                   c->c_body_begin.p, c->c_body_end.p, tb0, tb1, filter, epoch, lbv);
+      else if (!small && kPipe64)
+        k_step_pipe<<<pgrid, kPipeThreads, 0, s>>>(L, fr, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
+                                                   theta * theta, mutual, sbits, c->m2l_keys.p, c->p2p_keys.p, nx, ctr,
+                                                   cap_m, cap_p, cap_f, c->c_body_begin.p, c->c_body_end.p, tb0, tb1,
+                                                   filter, epoch, lbv);
+      else if (small)
         k_step<<<grid, kStepThreads, 0, s>>>(L, fr, c->c_cr.p, c->c_child_count.p, c->c_child_begin.p, theta,
                                              theta * theta, mutual, sbits, (uint32_t*)c->m2l_keys.p,
                                              (uint32_t*)c->p2p_keys.p, nx, ctr, cap_m, cap_p, cap_f,
