@@ -108,6 +108,7 @@ struct fmm_ctx {
   uint32_t trav_epoch = 0;                  // one epoch per k_step launch
   bool dbg_keys64 = false;                  // test hook: 64-bit keys on any tree
   int64_t dbg_cap = 0;                      // test hook: initial traversal buffer capacity
+  bool build_coop_ok = true;                // cooperative all-levels build kernel usable on this device
   int p2p_shape = -1;                       // FP32 P2P CTA shape: -1 automatic, 0 wide, 1 narrow
   int trav_regrows = 0;                     // rerun attempts of the last traversal
   fmmb::DBuf<int32_t> bnd;           // child boundaries of one level (9 per cell)

@@ -11,6 +11,7 @@
 // skipped). A second sort by (leaf, input index) restores the reference's within-leaf order
 // (stable counting sorts keep input order inside a leaf, tree.cpp:82-93).
 // All FP64 arithmetic uses explicit __dadd_rn/__dmul_rn so nothing is contracted to FMA.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "context.cuh"
@@ -205,6 +206,132 @@ __global__ void k_write_children(const int32_t* __restrict__ lev, int level, int
     }
   }
   }
+}
+
+// All levels in ONE cooperative launch (grid barriers between the phases of a level) instead of
+// six launches per level (memset, count, scan init, scan over the whole cell capacity, write,
+// advance: 25-30 us per level whatever its size; C2's 7 levels were half of its 0.43 ms build).
+// Per level: each CTA takes a contiguous block of the level's cells, its warps count the children
+// of their cells (same octant-boundary searches as k_count_children) and the CTA publishes its
+// children total; after the barrier every CTA sums the totals of the CTAs before it, scans its own
+// cells and materialises their children (same code as k_write_children), and CTA 0 sets the next
+// level's range. The loop ends at the first level without cells.
+#ifndef FMM_BUILD_COOP
+#define FMM_BUILD_COOP 1
+#endif
+constexpr int kCoopThreads = 256;
+__global__ void __launch_bounds__(kCoopThreads)
+k_build_levels(int32_t* __restrict__ lev, int n_crit, int sort_levels, int64_t cap, const uint64_t* __restrict__ skeys,
+               int32_t* __restrict__ nchild, int32_t* __restrict__ bnd, int32_t* __restrict__ part,
+               int32_t* __restrict__ deeper, int32_t* __restrict__ overflow, int32_t* __restrict__ c_level,
+               uint64_t* __restrict__ c_key, double4* __restrict__ c_cr, int32_t* __restrict__ bb,
+               int32_t* __restrict__ be, int32_t* __restrict__ cb, int32_t* __restrict__ cc, int32_t* __restrict__ par) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  using Reduce = cub::BlockReduce<int, kCoopThreads>;
+  using Scan = cub::BlockScan<int, kCoopThreads>;
+  __shared__ union {
+    typename Reduce::TempStorage red;
+    typename Scan::TempStorage scan;
+  } tmp;
+  __shared__ int s_base, s_total;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  constexpr int kWarps = kCoopThreads / 32;
+  int level = 0;
+  for (; level <= kLevels; ++level) {
+    // plain loads: lev is written inside this kernel (no read-only path)
+    const int32_t cbeg = *(volatile int32_t*)&lev[level], cend = *(volatile int32_t*)&lev[level + 1];
+    const int32_t m = cend - cbeg;
+    if (m <= 0) break;  // uniform over the grid
+    const int32_t cpb = (m + static_cast<int32_t>(gridDim.x) - 1) / static_cast<int32_t>(gridDim.x);
+    const int32_t k0 = min(m, static_cast<int32_t>(blockIdx.x) * cpb), k1 = min(m, k0 + cpb);
+    // ---- phase 1: children of the CTA's cells (warp per cell)
+    int mine = 0;
+    for (int32_t k = k0 + w; k < k1; k += kWarps) {
+      const int32_t ci = cbeg + k;
+      const int32_t b = bb[ci], e = be[ci];
+      bool split = e - b > n_crit && level < kLevels;  // tree.cpp:78
+      if (split && level >= sort_levels) {  // digits below the sorted ones: full sort needed
+        if (lane == 0) *deeper = 1;
+        split = false;
+      }
+      int32_t pos = e;
+      if (split && lane >= 1 && lane <= 7) pos = lower_digit(skeys, b, e, level + 1, lane);
+      if (lane == 0) pos = b;
+      if (split && lane <= 8) bnd[9 * k + lane] = pos;
+      const int32_t nxt = __shfl_down_sync(0xffffffffu, pos, 1);
+      const unsigned nonempty = __ballot_sync(0xffffffffu, split && lane < 8 && nxt > pos);
+      if (lane == 0) {
+        nchild[k] = __popc(nonempty);
+        mine += __popc(nonempty);
+      }
+    }
+    const int btot = Reduce(tmp.red).Sum(mine);
+    if (tid == 0) part[blockIdx.x] = btot;
+    grid.sync();
+    // ---- phase 2: offsets (CTAs before this one + a scan of the own cells), children, next range
+    int before = 0, all = 0;
+    for (int b = tid; b < static_cast<int>(gridDim.x); b += kCoopThreads) {
+      const int v = *(volatile int32_t*)&part[b];
+      all += v;
+      before += b < static_cast<int>(blockIdx.x) ? v : 0;
+    }
+    __syncthreads();
+    const int rb = Reduce(tmp.red).Sum(before);
+    __syncthreads();
+    const int ra = Reduce(tmp.red).Sum(all);
+    if (tid == 0) {
+      s_base = rb;
+      s_total = ra;
+    }
+    __syncthreads();
+    int carry = s_base;
+    const int32_t next_begin = cend;
+    for (int32_t kk = k0; kk < k1; kk += kCoopThreads) {
+      const int32_t k = kk + tid;
+      const int nc = k < k1 ? nchild[k] : 0;
+      int ex, agg;
+      Scan(tmp.scan).ExclusiveSum(nc, ex, agg);
+      if (nc > 0 && static_cast<int64_t>(next_begin) + carry + ex + nc <= cap) {  // else: overflow, flagged below
+        const int32_t ci = cbeg + k;
+        const double4 pc = c_cr[ci];
+        const uint64_t pkey = c_key[ci];
+        const double cr = __dmul_rn(0.5, pc.w);
+        int32_t out = next_begin + carry + ex;
+        cb[ci] = out;
+        cc[ci] = nc;
+        for (int o = 0; o < 8; ++o) {
+          const int32_t start = bnd[9 * k + o], stop = bnd[9 * k + o + 1];
+          if (stop > start) {
+            c_level[out] = level + 1;
+            c_key[out] = (pkey << 3) | (uint64_t)o;
+            c_cr[out] = make_double4(__dadd_rn(pc.x, (o & 1) ? cr : -cr), __dadd_rn(pc.y, (o & 2) ? cr : -cr),
+                                     __dadd_rn(pc.z, (o & 4) ? cr : -cr), cr);
+            bb[out] = start;
+            be[out] = stop;
+            cb[out] = 0;
+            cc[out] = 0;
+            par[out] = ci;
+            ++out;
+          }
+        }
+      }
+      carry += agg;
+      __syncthreads();
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      int64_t next = static_cast<int64_t>(cend) + s_total;
+      if (next > cap) {
+        *overflow = 1;
+        next = cend;
+      }
+      lev[level + 2] = static_cast<int32_t>(next);
+    }
+    grid.sync();
+  }
+  // the levels after the last one are empty (the host looks for the first level without children)
+  if (blockIdx.x == 0 && tid == 0)
+    for (int l = level; l <= kLevels; ++l) lev[l + 2] = lev[level + 1];
 }
 
 __global__ void k_init_root(const double* __restrict__ dom, int32_t n, int32_t* c_level, uint64_t* c_key,
@@ -408,9 +535,48 @@ void build_tree(fmm_ctx* c) {
     int done_level = -1;  // last level whose children have been counted
     bool finished = false, over = false;
     int batch = std::max(2, c->last_depth + 2);
+    bool coop = FMM_BUILD_COOP && c->build_coop_ok;
+    if (coop) {
+      static std::atomic<int> coop_blocks{0};  // CTAs per SM of k_build_levels (same on every B200)
+      if (coop_blocks.load() == 0) {
+        int nb = 0, supported = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_build_levels, kCoopThreads, 0));
+        CK(cudaDeviceGetAttribute(&supported, cudaDevAttrCooperativeLaunch, c->cfg.device));
+        coop_blocks.store(supported && nb > 0 ? std::min(nb, 4) : -1);
+      }
+      if (coop_blocks.load() < 0) {
+        coop = false;
+        c->build_coop_ok = false;
+      } else {
+        int sms = 148;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->cfg.device));
+        const int grid = sms * coop_blocks.load();
+        int32_t* part = c->i32_b.p;  // offs is unused on this path: per-CTA children totals
+        int32_t* lev_p = dlev;
+        int n_crit = c->cfg.n_crit, sl = sort_levels;
+        int64_t cap64 = ccap;
+        const uint64_t* skeys_p = skeys;
+        int32_t *cl = c->c_level.p, *bbp = c->c_body_begin.p, *bep = c->c_body_end.p, *cbp = c->c_child_begin.p,
+                *ccp = c->c_child_count.p, *parp = c->c_parent.p;
+        uint64_t* ck = c->c_key.p;
+        double4* ccr = c->c_cr.p;
+        void* args[] = {&lev_p, &n_crit, &sl, &cap64, &skeys_p, &nchild, &bnd, &part, &deeper, &overflow, &cl, &ck,
+                        &ccr, &bbp, &bep, &cbp, &ccp, &parp};
+        const cudaError_t le = cudaLaunchCooperativeKernel((const void*)k_build_levels, dim3(grid), dim3(kCoopThreads),
+                                                           args, 0, s);
+        if (le != cudaSuccess) {  // e.g. the device cannot hold the grid right now: the per-level path
+          cudaGetLastError();
+          coop = false;
+          c->build_coop_ok = false;
+        } else {
+          launches += 1;
+        }
+      }
+    }
+    if (coop) batch = kLevels + 1;  // every level is done: one read of the level table
     while (!finished) {
       const int l_end = std::min(done_level + batch, kLevels);
-      for (int L = done_level + 1; L <= l_end; ++L) {
+      for (int L = done_level + 1; L <= l_end && !coop; ++L) {
         CK(cudaMemsetAsync(nchild, 0, (ccap + 1) * sizeof(int32_t), s));
         k_count_children<<<148 * 16, 128, 0, s>>>(dlev, L, c->cfg.n_crit, sort_levels, c->c_body_begin.p,
                                                   c->c_body_end.p, skeys, nchild, bnd, deeper);
