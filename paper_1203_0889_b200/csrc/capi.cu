@@ -259,6 +259,8 @@ void evaluate_impl(fmm_ctx* c, bool reuse) {
         // (and its host round trips) proceeds on the first; M2L joins both.
         CK(cudaStreamWaitEvent(c->stream2, c->ev[EV_BUILD1], 0));
         fmmb::run_upward(c, c->stream2);
+        // M2L's detraced source rows need only the multipoles: built here, under the traversal
+        if (c->world == 1) fmmb::run_detrace(c, c->stream2);
         CK(cudaEventRecord(c->ev[EV_UP1], c->stream2));
         lists();
         CK(cudaEventRecord(c->ev[EV_TRAV1], c->stream));
@@ -690,6 +692,7 @@ int fmm_load_multipoles(fmm_ctx* c, const double* multipole) {
     CK(cudaMemcpyAsync(c->M.ensure(n), multipole, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->have_M = true;
+    ++c->M_version;
   });
 }
 
@@ -796,6 +799,7 @@ int fmm_upward_finish(fmm_ctx* c, const double* d_recv) {
     fmmb::shard_unpack(c, d_recv, c->stream);
     fmmb::run_upward(c, c->stream, 2);
     c->have_M = true;
+    ++c->M_version;
   });
 }
 

@@ -108,6 +108,7 @@ struct fmm_ctx {
   uint32_t trav_epoch = 0;                  // one epoch per k_step launch
   bool dbg_keys64 = false;                  // test hook: 64-bit keys on any tree
   int64_t dbg_cap = 0;                      // test hook: initial traversal buffer capacity
+  uint64_t M_version = 0, mt_version = ~0ull;  // multipoles written / detraced rows built from them
   bool build_coop_ok = true;                // cooperative all-levels build kernel usable on this device
   int p2p_shape = -1;                       // FP32 P2P CTA shape: -1 automatic, 0 wide, 1 narrow
   int trav_regrows = 0;                     // rerun attempts of the last traversal
@@ -195,6 +196,7 @@ void run_p2p(fmm_ctx* c, cudaStream_t s);
 // expansions.cu
 void run_upward(fmm_ctx* c, cudaStream_t s, int mode = 0);  // 0 all, 1 own cells, 2 shared cells
 void run_m2l(fmm_ctx* c, cudaStream_t s);
+void run_detrace(fmm_ctx* c, cudaStream_t s);  // M2L's detraced source rows from the current multipoles
 void run_downward(fmm_ctx* c, cudaStream_t s, int part = 3);  // 1: L2L, 2: L2P + combine, 3: both
 
 // CUB temp helpers (the second one belongs to the P2P preparation path)

@@ -403,6 +403,7 @@ void run_upward(fmm_ctx* c, cudaStream_t s, int mode) {
   if (mode != 0 && !c->shard_planned) fail(FMM_ERR_STATE, "sharded upward before the partition (run traverse)");
   dispatch_order<Upward>(c->cfg.order, c, s, mode);
   c->have_M = true;
+  ++c->M_version;
 }
 
 void run_downward(fmm_ctx* c, cudaStream_t s, int part) {

@@ -154,6 +154,23 @@ void launch_detrace(fmm_ctx* c, double* Mt, cudaStream_t s) {
   CK_LAUNCH("k_detrace");
 }
 
+// The detraced rows of the current multipoles (built once per upward pass: fmm_evaluate builds them
+// on the upward stream, under the traversal; a stand-alone fmm_m2l builds them here)
+template <int P>
+double* detraced_rows(fmm_ctx* c, cudaStream_t s) {
+  const size_t need = c->ncells * m2l_row_stride(HM<P>::NA) + 1;
+  if (c->mt_version != c->M_version || c->m2l_mt.cap < need) {
+    launch_detrace<P>(c, c->m2l_mt.ensure(need), s);
+    c->mt_version = c->M_version;
+    c->kernel_launches += 1;
+  }
+  return c->m2l_mt.p;
+}
+template <int P>
+struct Detrace {
+  static void run(fmm_ctx* c, cudaStream_t s) { detraced_rows<P>(c, s); }
+};
+
 // Dt_g for g_c <= 2 (compact HM::g_of order) by the reference's degree recurrence
 // (multi_index.cpp:64-83) rescaled by g!:
 //   n r^2 Dt_g = -(2n-1) sum_d g_d r_d Dt_{g-e_d} - (n-1) sum_d g_d (g_d - 1) Dt_{g-2e_d},
@@ -1189,12 +1206,11 @@ struct M2L {
         CK(cudaFuncSetAttribute(k_m2l_reg<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       });
       if (c->n_m2l_targets == 0) return;
-      double* Mt = c->m2l_mt.ensure(c->ncells * m2l_row_stride(HM<P>::NA) + 1);
-      launch_detrace<P>(c, Mt, s);
+      double* Mt = detraced_rows<P>(c, s);
       k_m2l_reg<P><<<ceil_div(c->n_m2l_targets, kM2LWarps), 32 * kM2LWarps, smem, s>>>(c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p,
                                                                     c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
       CK_LAUNCH("k_m2l_reg");
-      c->kernel_launches += 2;
+      c->kernel_launches += 1;
     } else {  // p >= 7 (only these orders instantiate the staged-row kernel)
     using C2 = BigCfg2<P>;
     const size_t smem2 = C2::kSmemPerWarp * C2::kWarps;
@@ -1203,8 +1219,7 @@ struct M2L {
       CK(cudaFuncSetAttribute(k_m2l_big2<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     });
     if (c->n_m2l_targets == 0) return;
-    double* Mt = c->m2l_mt.ensure(c->ncells * C2::SA + 1);
-    launch_detrace<P>(c, Mt, s);
+    double* Mt = detraced_rows<P>(c, s);
 #ifndef FMM_BIG2_FLAT
 #define FMM_BIG2_FLAT 1
 #endif
@@ -1234,7 +1249,7 @@ struct M2L {
         k_m2l_expand_flat<P><<<(unsigned)ceil_div(nt, kExpandTargets), 256, 0, s>>>(c->m2l_targets.p, nt, toff, span, Lc,
                                                                                   c->L.p);
         CK_LAUNCH("k_m2l_expand_flat");
-        c->kernel_launches += 5;
+        c->kernel_launches += 4;
         return;
       }
     }
@@ -1259,7 +1274,7 @@ struct M2L {
     k_m2l_big2<P><<<(unsigned)ceil_div(c->n_m2l_targets, C2::kWarps), 32 * C2::kWarps, smem2, s>>>(
         tg, c->n_m2l_targets, c->m2l_off.p, c->m2l_src.p, c->c_cr.p, Mt, c->L.p, Lc);
     CK_LAUNCH("k_m2l_big2");
-    c->kernel_launches += 2;
+    c->kernel_launches += 1;
     if (FMM_M2L_SPLIT_EPILOGUE) {
       k_m2l_expand<P><<<(unsigned)ceil_div(c->n_m2l_targets, kExpandTargets), 256, 0, s>>>(tg, c->n_m2l_targets, Lc,
                                                                                          c->L.p);
@@ -1271,6 +1286,11 @@ struct M2L {
 };
 
 }  // namespace
+
+void run_detrace(fmm_ctx* c, cudaStream_t s) {
+  if (!c->have_M) fail(FMM_ERR_STATE, "detrace: no multipoles (run upward first)");
+  dispatch_order<Detrace>(c->cfg.order, c, s);
+}
 
 void run_m2l(fmm_ctx* c, cudaStream_t s) {
   if (!c->have_lists) fail(FMM_ERR_STATE, "m2l: no interaction lists");
