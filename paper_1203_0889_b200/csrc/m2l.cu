@@ -426,11 +426,12 @@ k_m2l_reg(const int32_t* __restrict__ targets, int64_t ntargets, const int64_t* 
   __syncwarp();
   const int64_t wid = blockIdx.x * (int64_t)kM2LWarps + w;
   if (wid >= ntargets) return;
-  const int32_t t = targets[wid];
+  const int32_t t = targets ? targets[wid] : static_cast<int32_t>(wid);  // no target list: warp per cell
   FMM_CHECK(t >= 0 && t < FMM_LIM(ncells), "k_m2l_reg: target index");
-  const double4 ct = cr[t];
   const int64_t l0 = off[t], l1 = off[t + 1];
   FMM_CHECK(l0 >= 0 && l0 <= l1 && l1 <= FMM_LIM(n_m2l), "k_m2l_reg: list range");
+  if (l0 >= l1) return;
+  const double4 ct = cr[t];
   double lam[NA];
 #pragma unroll
   for (int i = 0; i < NA; ++i) lam[i] = 0.0;
@@ -1207,8 +1208,10 @@ struct M2L {
       });
       if (c->n_m2l_targets == 0) return;
       double* Mt = detraced_rows<P>(c, s);
-      k_m2l_reg<P><<<ceil_div(c->n_m2l_targets, kM2LWarps), 32 * kM2LWarps, smem, s>>>(c->m2l_targets.p, c->n_m2l_targets, c->m2l_off.p,
-                                                                    c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
+      const bool all_cells = c->n_m2l_targets < 0;  // finish_lists skipped the target list
+      const int64_t nt = all_cells ? c->ncells : c->n_m2l_targets;
+      k_m2l_reg<P><<<ceil_div(nt, kM2LWarps), 32 * kM2LWarps, smem, s>>>(all_cells ? nullptr : c->m2l_targets.p, nt,
+                                                                    c->m2l_off.p, c->m2l_src.p, c->c_cr.p, Mt, c->L.p);
       CK_LAUNCH("k_m2l_reg");
       c->kernel_launches += 1;
     } else {  // p >= 7 (only these orders instantiate the staged-row kernel)

@@ -702,6 +702,15 @@ void finish_lists(fmm_ctx* c, int64_t n_m2l, int64_t n_p2p) {
     c->shard_b1 = c->N;
   }
   if (split) p2p_worklist_begin(c);  // queued on the second stream before the M2L host sync
+  // p <= 6, one rank: the register M2L kernel takes a warp per CELL and leaves at once on an empty
+  // list (nearly every cell has one: 37 440 of C2's 37 449), so the target list, its select and
+  // the host read of its length are skipped (n_m2l_targets = -1: every cell)
+  if (c->world == 1 && c->cfg.order <= 6) {
+    c->n_m2l_targets = n_m2l > 0 ? -1 : 0;
+    c->have_lists = true;
+    if (!split) build_p2p_worklist(c);
+    return;
+  }
   int32_t* flag = c->i32_c.ensure(c->ncells);
   k_flag_nonempty<<<ceil_div(c->ncells, 256), 256, 0, s>>>(c->m2l_off.p, c->ncells, c->c_body_begin.p,
                                                            c->c_body_end.p, c->shard_b0, c->shard_b1, flag);
