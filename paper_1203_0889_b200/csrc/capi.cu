@@ -112,6 +112,8 @@ int fmm_create(const fmm_config* cfg, fmm_ctx** out) {
       CK(cudaEventCreateWithFlags(&c->ev_lists, cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_l2l, cudaEventDisableTiming));
       c->pstream = c->stream;
+      // test hook: the per-level tree build (the fallback when a cooperative launch is not possible)
+      if (getenv("FMM_NO_COOP_BUILD")) c->build_coop_ok = false;
       CK(cudaMallocHost(&c->hpin, 64 * sizeof(int64_t)));
       c->d_counters.ensure(32);
     } catch (...) {

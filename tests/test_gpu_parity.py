@@ -374,10 +374,15 @@ def test_pipeline_other_orders(fmmlib, orc, p):
     ctx.close()
 
 
-def test_tree_reuse_across_distributions(fmmlib, orc):
+@pytest.mark.parametrize("coop", [True, False], ids=["cooperative-build", "per-level-build"])
+def test_tree_reuse_across_distributions(fmmlib, orc, coop, monkeypatch):
     """One context, successive body sets of growing depth: the partial-digit sort keyed on the
     previous depth must fall back to the full sort (and the level batches must continue) so that
-    every tree and permutation stays bit-exact with the reference restatement."""
+    every tree and permutation stays bit-exact with the reference restatement. Both tree builders:
+    the cooperative all-levels kernel and the per-level launches it falls back to
+    (FMM_NO_COOP_BUILD, read when the context is created)."""
+    if not coop:
+        monkeypatch.setenv("FMM_NO_COOP_BUILD", "1")
     ctx = fmmlib.Context(order=4, n_crit=32, theta=0.5, precision="fp64")
     for gen, n, seed in ((1, 20000, 3), (3, 20000, 4), (5, 30000, 6), (1, 5000, 7), (3, 40000, 8)):
         bodies = fmmlib.generate_bodies(gen, n, seed)
