@@ -579,8 +579,11 @@ class _DevBuf:
         self.ptr = self.t.data_ptr()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_step_emulated(fmmlib, world):
+@pytest.mark.parametrize("world,gen,n,p,n_crit,theta",
+                         [(2, 3, 60000, 6, 64, 0.5), (3, 3, 60000, 6, 64, 0.5), (2, 4, 40000, 8, 128, 0.4),
+                          (2, 5, 30000, 10, 64, 0.5)],
+                         ids=["2-ranks-p6", "3-ranks-p6", "2-ranks-C4-shape-p8", "2-ranks-C5-shape-p10"])
+def test_sharded_step_emulated(fmmlib, world, gen, n, p, n_crit, theta):
     """The multi-GPU data path with `world` ranks emulated sequentially on one GPU (no rank waits
     on another): per-rank partition, local upward, the all-gather as a concatenation of the
     equal-size chunks, shared ancestors, then M2L/P2P/downward; the union of the ranks' own body
@@ -588,14 +591,14 @@ def test_sharded_step_emulated(fmmlib, world):
     full lists, the second reuses it (Morton boundaries) with a target-filtered traversal."""
     import torch
     fb = fmmlib
-    bodies = fb.generate_bodies(3, 60000, 21)
+    bodies = fb.generate_bodies(gen, n, 21)
     for precision, tol in (("fp64", 1e-12), ("fp32", 1e-6)):
-        full = run_gpu(fb, bodies, 64, 6, 0.5, precision)
+        full = run_gpu(fb, bodies, n_crit, p, theta, precision)
         phi_full, acc_full = full.results("tree")
         n_m2l_full = full.tree_info().n_m2l
         ctxs = []
         for r in range(world):
-            ctx = fb.Context(order=6, n_crit=64, theta=0.5, precision=precision)
+            ctx = fb.Context(order=p, n_crit=n_crit, theta=theta, precision=precision)
             ctx.set_bodies(bodies)
             ctx.set_partition(r, world)
             ctxs.append(ctx)
