@@ -283,8 +283,11 @@ k_l2l(int32_t cbeg, int32_t cend, const int32_t* __restrict__ par, const double4
 // ------------------------------------------------------------------------------ L2P ----
 // Warp per leaf, lane per body; phi_out = phi_near + sum_b L_b (x-c)^b and
 // acc_out = acc_near - grad (extension). Leaf L staged in shared memory (broadcast reads).
+#ifndef FMM_L2P_MINB
+#define FMM_L2P_MINB 6
+#endif
 template <int P>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, FMM_L2P_MINB)
 k_l2p(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __restrict__ bb,
       const int32_t* __restrict__ be, const double4* __restrict__ cr, const double4* __restrict__ bodies,
       const double* __restrict__ L, const double* __restrict__ phi_near, const double* __restrict__ acc_near,
@@ -308,7 +311,10 @@ k_l2p(const int32_t* __restrict__ leaves, int64_t nleaves, const int32_t* __rest
     double ph = 0.0, gx = 0.0, gy = 0.0, gz = 0.0;
     // P >= 8: volatile reads keep the unrolled coefficient loads in order (otherwise they are
     // hoisted ahead of the FMAs and spill)
-    using LPtr = std::conditional_t<(P >= 8), const volatile double*, const double*>;
+#ifndef FMM_L2P_VOLATILE_MIN_P
+#define FMM_L2P_VOLATILE_MIN_P 4
+#endif
+    using LPtr = std::conditional_t<(P >= FMM_L2P_VOLATILE_MIN_P), const volatile double*, const double*>;
     const LPtr Lw = sL[w];
     static_for<P>([&](auto AI) {
       constexpr int a = P - 1 - decltype(AI)::value;
