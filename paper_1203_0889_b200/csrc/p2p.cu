@@ -1095,13 +1095,19 @@ void p2p_worklist_end(fmm_ctx* c) {
   int32_t* ord_out = ord_in + (nitem + 1);
   k_iota<<<ceil_div(nitem, 256), 256, 0, s>>>(ord_in, nitem);
   size_t sb = 0;
-  // every item cost is below 2^cost_bits (C2: ~20 bits, 3 radix passes instead of 6)
+  // every item cost is below 2^cost_bits (C2: ~20 bits); only the top kCostSortBits of them are
+  // sorted (one or two radix passes instead of three to six): items of nearly equal cost keep their
+  // Morton order (stable), which schedules as well as the exact order
+#ifndef FMM_P2P_COST_SORT_BITS
+#define FMM_P2P_COST_SORT_BITS 8
+#endif
   const uint64_t cbound = static_cast<uint64_t>(c->hpin[17]);
   const int cost_bits = std::min(48, std::max(1, 64 - __builtin_clzll(cbound | 1ull)));
-  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, costs, costs_sorted, ord_in, ord_out, (int)nitem, 0,
+  const int cost_lo = std::max(0, cost_bits - FMM_P2P_COST_SORT_BITS);
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, sb, costs, costs_sorted, ord_in, ord_out, (int)nitem, cost_lo,
                                                cost_bits, s));
   CK(cub::DeviceRadixSort::SortPairsDescending(temp_storage2(c, sb), sb, costs, costs_sorted, ord_in, ord_out,
-                                               (int)nitem, 0, cost_bits, s));
+                                               (int)nitem, cost_lo, cost_bits, s));
   k_gather_items<<<ceil_div(nitem, 256), 256, 0, s>>>(items_raw, ord_out, nitem, items);
   CK_LAUNCH("k_gather_items");
   c->n_p2p_items = nitem;
